@@ -1,0 +1,195 @@
+/*
+ * dopinf_b200.h — C ABI of the B200-native dOpInf snapshot pass.
+ *
+ * Drop-in boundary for the reference's Steps II–III and the Φ_r/projection
+ * products (paths relative to /root/reference/proj). Every entry point is
+ * synchronous at the boundary (the reference has value semantics), takes plain
+ * pointers and sizes, never throws, and returns a dopinf_b200_status whose
+ * values map one-to-one onto the reference exception classes
+ * (include/dopinf/errors.hpp:9-73); the message is kept per context
+ * (dopinf_b200_last_error). Host matrices are row-major fp64 with an explicit
+ * leading dimension, as dopinf::Matrix (include/dopinf/matrix.hpp:13-53).
+ *
+ * Replaces                                               with
+ *   comm::Comm rank/size/allreduce/barrier (comm.hpp:13-31)  dopinf_b200_ctx_* + allreduce/barrier
+ *   data::partition_rows (data.hpp:47, data.cpp:86-103)      dopinf_b200_partition_rows
+ *   data::LocalBlock values (data.hpp:38-42)                 dopinf_b200_block (device resident)
+ *   transform::center_in_place (transform.hpp:27)            dopinf_b200_center
+ *   transform::compute_global_scales (transform.hpp:32-34)   dopinf_b200_global_scales
+ *   transform::scale_in_place (transform.hpp:37)             dopinf_b200_scale
+ *   pod::local_gram (pod.hpp:28)                             dopinf_b200_local_gram
+ *   pod::global_gram (pod.hpp:31)                            dopinf_b200_global_gram
+ *   pod::project (pod.hpp:49)                                dopinf_b200_project / _project_host
+ *   postprocess::reconstruct_field's Φ_r = Q·T_r (postprocess.cpp:66)
+ *                                                            dopinf_b200_basis
+ *   postprocess::basis_rows (postprocess.hpp:25-26)          dopinf_b200_basis_rows
+ *
+ * The eigensolve (pod::eig_sym_desc), rank selection, reduced_map, the OpInf
+ * solve and the ROM search stay on the reference code path: the host D
+ * returned by dopinf_b200_global_gram is the reference's Matrix D, and the
+ * T_r it produces is handed back to dopinf_b200_project / _basis.
+ */
+#ifndef DOPINF_B200_H
+#define DOPINF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DOPINF_B200_ABI_VERSION 1
+#define DOPINF_B200_UNIQUE_ID_BYTES 128
+
+typedef enum dopinf_b200_status {
+    DOPINF_B200_OK = 0,
+    DOPINF_B200_ERR_INVALID_ARGUMENT = 1,   /* InvalidArgumentError   (errors.hpp:70-73) */
+    DOPINF_B200_ERR_PARTITION = 2,          /* PartitionError         (errors.hpp:21-24) */
+    DOPINF_B200_ERR_COLLECTIVE = 3,         /* CollectiveError        (errors.hpp:28-31) */
+    DOPINF_B200_ERR_DEGENERATE_VARIABLE = 4,/* DegenerateVariableError(errors.hpp:34-37) */
+    DOPINF_B200_ERR_DEVICE = 5,             /* CUDA / NCCL failure (surfaced as dopinf::Error) */
+    DOPINF_B200_ERR_OUT_OF_MEMORY = 6       /* device allocation failure (dopinf::Error)      */
+} dopinf_b200_status;
+
+/* Collective ops, same order as comm::ReduceOp (comm.hpp:9). */
+typedef enum dopinf_b200_reduce_op {
+    DOPINF_B200_SUM = 0,
+    DOPINF_B200_MAX = 1,
+    DOPINF_B200_MIN = 2
+} dopinf_b200_reduce_op;
+
+/* How the K×K Gram partials of the ranks are combined (pod.cpp:15-18).
+ * ORDERED: ncclAllGather of the packed upper triangles, then a device sum in
+ * ascending rank order — the reduction order of the reference's in-process
+ * backend (comm_inprocess.cpp:101-112), bitwise reproducible for a fixed rank
+ * count regardless of NCCL's algorithm choice. NCCL: ncclAllReduce(Sum) of
+ * the packed triangle (half the bytes of ORDERED at p=2, fewer beyond). */
+typedef enum dopinf_b200_gram_reduce {
+    DOPINF_B200_GRAM_REDUCE_ORDERED = 0,
+    DOPINF_B200_GRAM_REDUCE_NCCL = 1
+} dopinf_b200_gram_reduce;
+
+/* Device-timed stages recorded per context (CUDA events on its stream). */
+typedef enum dopinf_b200_stage {
+    DOPINF_B200_STAGE_UPLOAD = 0,
+    DOPINF_B200_STAGE_STATS = 1,      /* center: mean + row max-abs pass        */
+    DOPINF_B200_STAGE_SCALES = 2,     /* MAX all-reduce of per-variable scales  */
+    DOPINF_B200_STAGE_APPLY = 3,      /* (x - mean) / s pass                    */
+    DOPINF_B200_STAGE_GRAM = 4,       /* DMMA upper-triangle Gram kernel        */
+    DOPINF_B200_STAGE_GRAM_REDUCE = 5,/* split-n fix-up (fixed order)           */
+    DOPINF_B200_STAGE_ALLREDUCE = 6,  /* cross-rank Gram reduction              */
+    DOPINF_B200_STAGE_UNPACK = 7,     /* packed triangle -> symmetric K×K       */
+    DOPINF_B200_STAGE_PROJECT = 8,    /* Q̂ = T_rᵀ D                             */
+    DOPINF_B200_STAGE_BASIS = 9,      /* Φ_r = Q T_r                            */
+    DOPINF_B200_STAGE_DOWNLOAD = 10,
+    DOPINF_B200_STAGE_COUNT = 11
+} dopinf_b200_stage;
+
+typedef struct dopinf_b200_ctx dopinf_b200_ctx;
+typedef struct dopinf_b200_block dopinf_b200_block;
+
+/* ---- library ---------------------------------------------------------- */
+int dopinf_b200_abi_version(void);
+const char* dopinf_b200_status_string(int status);
+/* Number of kernel launches this process has issued through the library. */
+uint64_t dopinf_b200_kernel_launches(void);
+
+/* ---- per-rank context (replaces the comm::Comm a rank runs against) ----- */
+/* Fill `id` (DOPINF_B200_UNIQUE_ID_BYTES) with an ncclUniqueId; rank 0 calls
+ * this and distributes the bytes (any transport) to the other ranks. */
+int dopinf_b200_get_unique_id(unsigned char* id);
+/* One context per rank: binds `device`, creates a stream and, when size > 1,
+ * an NCCL communicator from `id` (ignored when size == 1). */
+int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* id,
+                           dopinf_b200_ctx** out);
+void dopinf_b200_ctx_destroy(dopinf_b200_ctx* ctx);
+int dopinf_b200_ctx_rank(const dopinf_b200_ctx* ctx);
+int dopinf_b200_ctx_size(const dopinf_b200_ctx* ctx);
+const char* dopinf_b200_last_error(const dopinf_b200_ctx* ctx);
+int dopinf_b200_set_gram_reduce(dopinf_b200_ctx* ctx, int mode);
+/* Comm::allreduce / barrier (comm.hpp:20-30) on a HOST span, over NCCL. */
+int dopinf_b200_allreduce(dopinf_b200_ctx* ctx, double* data, size_t count, int op);
+int dopinf_b200_barrier(dopinf_b200_ctx* ctx);
+/* Device milliseconds of `stage` in the most recent call that ran it. */
+int dopinf_b200_stage_ms(const dopinf_b200_ctx* ctx, int stage, double* ms);
+/* The context's CUDA stream (cudaStream_t), for callers that interoperate. */
+void* dopinf_b200_ctx_stream(dopinf_b200_ctx* ctx);
+
+/* ---- sharding (data.cpp:86-103) --------------------------------------- */
+/* floor(nx/p) rows per rank, remainder on the last rank; begin/end have p
+ * entries. PARTITION unless 1 <= p <= nx. */
+int dopinf_b200_partition_rows(size_t nx, int p, size_t* begin, size_t* end);
+
+/* ---- device-resident LocalBlock (data.hpp:38-42) ----------------------- */
+/* (n_vars * nx_i) x nt fp64; block row j*nx_i + k is variable j at global
+ * spatial index row_begin + k. Device pitch is nt rounded up to even. */
+int dopinf_b200_block_create(dopinf_b200_ctx* ctx, size_t n_vars, size_t nx_i, size_t row_begin,
+                             size_t nt, dopinf_b200_block** out);
+void dopinf_b200_block_destroy(dopinf_b200_block* block);
+int dopinf_b200_block_upload(dopinf_b200_block* block, const double* host, size_t host_ld);
+/* Materialises any pending transform, then copies the values to the host. */
+int dopinf_b200_block_download(dopinf_b200_block* block, double* host, size_t host_ld);
+/* Device pointer and pitch (elements) of the block values. */
+int dopinf_b200_block_device(dopinf_b200_block* block, double** values, size_t* ld);
+/* Seeded synthetic snapshots on the device (BASELINE.json configs 1, 2, 4):
+ * Q[i,k] = amp_v * Σ_j sin(jπx_i + θ_j) e^{-γ_j t_k} cos(ω_j t_k + φ_j)
+ *          + noise * N(0,1),  t_k = k*dt, x_i = seeded U[0,1) per global point.
+ * Mode draws (θ, ω, γ, φ) are seeded per variable; amp_v = amps[v] (NULL: 1).
+ * The generator is plumbing for the bench/tests, not part of the pass. */
+int dopinf_b200_block_synth_oscillator(dopinf_b200_block* block, uint64_t seed, int n_modes,
+                                       double dt, double noise, const double* amps);
+/* Seeded i.i.d. N(0,1) plus amplitude * (rank-`rank` low-rank component)
+ * (BASELINE.json config 3). */
+int dopinf_b200_block_synth_lowrank(dopinf_b200_block* block, uint64_t seed, int rank,
+                                    double amplitude);
+
+/* ---- Step II transform (transform.cpp) --------------------------------- */
+/* center_in_place (transform.cpp:10-20): writes the per-row temporal means
+ * (rows = n_vars*nx_i; host, may be NULL). The subtraction is fused into the
+ * next pass over the block (apply or download); results are those of the
+ * reference's separate passes. */
+int dopinf_b200_center(dopinf_b200_block* block, double* means);
+/* compute_global_scales (transform.cpp:22-41): per-variable max |centered q|,
+ * MAX all-reduced over the ranks. DEGENERATE_VARIABLE when a scale is 0, with
+ * *degenerate_var set to the first such variable. scales: host [n_vars]. */
+int dopinf_b200_global_scales(dopinf_b200_block* block, double* scales, size_t* degenerate_var);
+/* scale_in_place (transform.cpp:43-49): q /= scales[var] (IEEE division). */
+int dopinf_b200_scale(dopinf_b200_block* block, const double* scales);
+
+/* ---- Step III Gram / projection (pod.cpp) ------------------------------ */
+/* local_gram (pod.cpp:11-13): D_i = Q_iᵀ Q_i, upper triangle on the FP64
+ * tensor pipe, split-n partials reduced in fixed order; kept on the device
+ * and, when d != NULL, written to the host as the full symmetric nt x nt. */
+int dopinf_b200_local_gram(dopinf_b200_block* block, double* d);
+/* global_gram (pod.cpp:15-18): reduces the context's local Gram over the
+ * ranks (identical on every rank) and optionally writes it to the host. */
+int dopinf_b200_global_gram(dopinf_b200_ctx* ctx, double* d);
+/* project (pod.cpp:103-105): Q̂ = T_rᵀ D with the context's device D;
+ * tr is host nt x r, qhat host r x nt. */
+int dopinf_b200_project(dopinf_b200_ctx* ctx, const double* tr, size_t nt, size_t r,
+                        double* qhat);
+/* project with a caller-provided host D (nt x nt). */
+int dopinf_b200_project_host(dopinf_b200_ctx* ctx, const double* tr, const double* d, size_t nt,
+                             size_t r, double* qhat);
+
+/* ---- Step V products (postprocess.cpp) --------------------------------- */
+/* Φ_r = Q T_r over the (transformed) block: rows x r. phi (host) may be NULL
+ * to keep the result on the device only (dopinf_b200_basis_device). */
+int dopinf_b200_basis(dopinf_b200_block* block, const double* tr, size_t r, double* phi);
+int dopinf_b200_basis_device(dopinf_b200_block* block, double** phi, size_t* ld);
+/* basis_rows (postprocess.cpp:12-34): out[k] = Q[rows[k]] T_r. */
+int dopinf_b200_basis_rows(dopinf_b200_block* block, const double* tr, size_t r,
+                           const size_t* rows, size_t nsel, double* out);
+
+/* ---- fused Steps II-III: one call per rank ------------------------------ */
+/* center (+ global scales + scale when scaling != 0) + local + global Gram.
+ * means [rows], scales [n_vars], d [nt x nt]: host, each may be NULL. */
+int dopinf_b200_snapshot_pass(dopinf_b200_block* block, int scaling, double* means,
+                              double* scales, double* d);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DOPINF_B200_H */

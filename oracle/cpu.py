@@ -1,0 +1,319 @@
+"""ctypes wrappers of the CPU checkers. TEST INFRASTRUCTURE ONLY.
+
+* `Oracle` — the C restatement (oracle/dopinf_oracle.c → _build/libdopinf_oracle.so),
+  compiled on demand with gcc if the prebuilt .so is missing (the GPU box has gcc).
+* `Reference` — the unmodified reference compiled from /root/reference
+  (oracle/_ref/libdopinf_refbench.so, prebuilt here; absent elsewhere → None).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "_build" / "libdopinf_oracle.so"
+REF_SO = HERE / "_ref" / "libdopinf_refbench.so"
+
+_dp = C.POINTER(C.c_double)
+_sp = C.POINTER(C.c_size_t)
+
+
+def _d(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _f(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Oracle:
+    """CPU restatement of the reference arithmetic (see dopinf_oracle.c)."""
+
+    _lib = None
+
+    def __init__(self):
+        if Oracle._lib is None:
+            if not ORACLE_SO.exists():
+                ORACLE_SO.parent.mkdir(exist_ok=True)
+                subprocess.run(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared", "-o",
+                                str(ORACLE_SO), str(HERE / "dopinf_oracle.c"), "-lm"], check=True)
+            lib = C.CDLL(str(ORACLE_SO))
+            lib.oracle_rng_new.restype = C.c_void_p
+            lib.oracle_rng_new.argtypes = [C.c_uint64]
+            lib.oracle_rng_free.argtypes = [C.c_void_p]
+            lib.oracle_rng_raw.restype = C.c_uint64
+            lib.oracle_rng_raw.argtypes = [C.c_void_p]
+            lib.oracle_rng_uniform.restype = C.c_double
+            lib.oracle_rng_uniform.argtypes = [C.c_void_p]
+            lib.oracle_rng_normal.restype = C.c_double
+            lib.oracle_rng_normal.argtypes = [C.c_void_p]
+            lib.oracle_rng_fill_normal.argtypes = [C.c_void_p, _dp, C.c_size_t]
+            lib.oracle_k_sum.restype = C.c_double
+            lib.oracle_k_sum.argtypes = [_dp, C.c_size_t]
+            lib.oracle_k_dot.restype = C.c_double
+            lib.oracle_k_dot.argtypes = [_dp, _dp, C.c_size_t]
+            lib.oracle_k_max_abs.restype = C.c_double
+            lib.oracle_k_max_abs.argtypes = [_dp, C.c_size_t]
+            lib.oracle_center_in_place.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp]
+            lib.oracle_local_maxabs.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp]
+            lib.oracle_reduce_scales.restype = C.c_long
+            lib.oracle_reduce_scales.argtypes = [_dp, C.c_int, C.c_size_t, _dp]
+            lib.oracle_scale_in_place.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp]
+            lib.oracle_inverse_transform_block.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp,
+                                                           C.c_int]
+            lib.oracle_gram.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp]
+            lib.oracle_allreduce_sum.argtypes = [_dp, C.c_int, C.c_size_t, _dp]
+            lib.oracle_matmul_tn.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
+            lib.oracle_matmul.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
+            lib.oracle_basis_rows.restype = C.c_long
+            lib.oracle_basis_rows.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _sp, C.c_size_t, _dp]
+            lib.oracle_partition_rows.restype = C.c_int
+            lib.oracle_partition_rows.argtypes = [C.c_size_t, C.c_int, _sp, _sp]
+            Oracle._lib = lib
+        self.lib = Oracle._lib
+
+    # -- rng (synth.cpp:15-34)
+    def normals(self, seed: int, count: int) -> np.ndarray:
+        r = self.lib.oracle_rng_new(seed)
+        out = np.empty(count, dtype=np.float64)
+        self.lib.oracle_rng_fill_normal(r, _d(out), count)
+        self.lib.oracle_rng_free(r)
+        return out
+
+    def rng(self, seed: int):
+        return _Rng(self.lib, seed)
+
+    # -- kernels
+    def k_sum(self, x):
+        x = _f(x)
+        return self.lib.oracle_k_sum(_d(x), x.size)
+
+    # -- transform
+    def center(self, q):
+        q = _f(q).copy()
+        rows, cols = q.shape
+        means = np.empty(rows)
+        self.lib.oracle_center_in_place(_d(q), rows, cols, _d(means))
+        return q, means
+
+    def local_maxabs(self, q, n_vars, nx_i):
+        q = _f(q)
+        out = np.empty(n_vars)
+        self.lib.oracle_local_maxabs(_d(q), n_vars, nx_i, q.shape[1], _d(out))
+        return out
+
+    def reduce_scales(self, per_rank):
+        per_rank = _f(per_rank)
+        p, n_vars = per_rank.shape
+        out = np.empty(n_vars)
+        bad = self.lib.oracle_reduce_scales(_d(per_rank), p, n_vars, _d(out))
+        return out, int(bad)
+
+    def scale(self, q, n_vars, nx_i, scales):
+        q = _f(q).copy()
+        s = _f(scales)
+        self.lib.oracle_scale_in_place(_d(q), n_vars, nx_i, q.shape[1], _d(s))
+        return q
+
+    def inverse_transform(self, values, nx_i, means, scales, scaling):
+        v = _f(values).copy()
+        self.lib.oracle_inverse_transform_block(_d(v), v.shape[0], v.shape[1], nx_i, _d(_f(means)),
+                                                _d(_f(scales)) if scaling else None, 1 if scaling else 0)
+        return v
+
+    # -- pod
+    def gram(self, q):
+        q = _f(q)
+        rows, cols = q.shape
+        d = np.empty((cols, cols))
+        self.lib.oracle_gram(_d(q), rows, cols, _d(d))
+        return d
+
+    def allreduce_sum(self, parts):
+        parts = _f(parts)
+        p = parts.shape[0]
+        out = np.empty(parts.shape[1:])
+        self.lib.oracle_allreduce_sum(_d(parts), p, out.size, _d(out))
+        return out
+
+    def matmul_tn(self, a, b):
+        a, b = _f(a), _f(b)
+        out = np.empty((a.shape[1], b.shape[1]))
+        self.lib.oracle_matmul_tn(_d(a), a.shape[0], a.shape[1], _d(b), b.shape[1], _d(out))
+        return out
+
+    def project(self, tr, d):
+        return self.matmul_tn(tr, d)
+
+    def matmul(self, a, b):
+        a, b = _f(a), _f(b)
+        out = np.empty((a.shape[0], b.shape[1]))
+        self.lib.oracle_matmul(_d(a), a.shape[0], a.shape[1], _d(b), b.shape[1], _d(out))
+        return out
+
+    def basis_rows(self, q, tr, rows):
+        q, tr = _f(q), _f(tr)
+        sel = np.ascontiguousarray(rows, dtype=np.uintp)
+        out = np.empty((sel.size, tr.shape[1]))
+        bad = self.lib.oracle_basis_rows(_d(q), q.shape[0], q.shape[1], _d(tr), tr.shape[1],
+                                         sel.ctypes.data_as(_sp), sel.size, _d(out))
+        if bad >= 0:
+            raise IndexError(f"basis_rows: row {int(sel[bad])} outside the local block")
+        return out
+
+    def partition_rows(self, nx, p):
+        b = np.zeros(max(p, 1), dtype=np.uintp)
+        e = np.zeros(max(p, 1), dtype=np.uintp)
+        rc = self.lib.oracle_partition_rows(nx, p, b.ctypes.data_as(_sp), e.ctypes.data_as(_sp))
+        if rc != 0:
+            raise ValueError(f"partition_rows({nx}, {p}) rejected (code {rc})")
+        return [(int(x), int(y)) for x, y in zip(b, e)]
+
+
+class _Rng:
+    def __init__(self, lib, seed):
+        self.lib = lib
+        self.h = lib.oracle_rng_new(seed)
+
+    def normal(self):
+        return self.lib.oracle_rng_normal(self.h)
+
+    def uniform(self):
+        return self.lib.oracle_rng_uniform(self.h)
+
+    def matrix(self, rows, cols):
+        out = np.empty(rows * cols)
+        self.lib.oracle_rng_fill_normal(self.h, _d(out), out.size)
+        return out.reshape(rows, cols)
+
+    def __del__(self):
+        try:
+            self.lib.oracle_rng_free(self.h)
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class Reference:
+    """The unmodified reference (oracle/_ref), or unavailable."""
+
+    _lib = None
+
+    @staticmethod
+    def available() -> bool:
+        return REF_SO.exists()
+
+    def __init__(self):
+        if Reference._lib is None:
+            if not REF_SO.exists():
+                raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference at build time)")
+            lib = C.CDLL(str(REF_SO))
+            lib.ref_last_error.restype = C.c_char_p
+            lib.ref_backend.restype = C.c_char_p
+            lib.ref_set_backend.argtypes = [C.c_char_p]
+            lib.ref_rng_normals.argtypes = [C.c_ulonglong, _dp, C.c_size_t]
+            lib.ref_snapshot_pass.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, C.c_int, _dp,
+                                              _dp, _dp, _dp]
+            lib.ref_gram.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp]
+            lib.ref_global_gram.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_int, _dp]
+            lib.ref_center.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp]
+            lib.ref_scale.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp]
+            lib.ref_project.argtypes = [_dp, _dp, C.c_size_t, C.c_size_t, _dp]
+            lib.ref_matmul.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
+            lib.ref_basis_rows.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _sp, C.c_size_t, _dp]
+            lib.ref_eig_reduced_map.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, _dp]
+            lib.ref_grid_search.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp, C.c_size_t,
+                                            C.c_double, C.c_size_t, _dp, _dp]
+            Reference._lib = lib
+        self.lib = Reference._lib
+
+    def _ok(self, rc):
+        if rc != 0:
+            raise RuntimeError(f"reference error {rc}: {self.lib.ref_last_error().decode()}")
+
+    def backend(self) -> str:
+        return self.lib.ref_backend().decode()
+
+    def normals(self, seed, count):
+        out = np.empty(count)
+        self.lib.ref_rng_normals(seed, _d(out), count)
+        return out
+
+    def snapshot_pass(self, q_full, n_vars, nx, workers, scaling):
+        """Steps II-III on `workers` in-process ranks; returns (q_transformed, means, scales, D, seconds)."""
+        q = _f(q_full).copy()
+        nt = q.shape[1]
+        d = np.empty((nt, nt))
+        means = np.empty(n_vars * nx)
+        scales = np.zeros(n_vars)
+        secs = np.zeros(2)
+        self._ok(self.lib.ref_snapshot_pass(_d(q), n_vars, nx, nt, workers, 1 if scaling else 0, _d(d),
+                                            _d(means), _d(scales), _d(secs)))
+        return q, means, scales, d, secs
+
+    def gram(self, q):
+        q = _f(q)
+        d = np.empty((q.shape[1], q.shape[1]))
+        self._ok(self.lib.ref_gram(_d(q), q.shape[0], q.shape[1], _d(d)))
+        return d
+
+    def global_gram(self, q, workers):
+        q = _f(q)
+        d = np.empty((q.shape[1], q.shape[1]))
+        self._ok(self.lib.ref_global_gram(_d(q), q.shape[0], q.shape[1], workers, _d(d)))
+        return d
+
+    def center(self, q):
+        q = _f(q).copy()
+        means = np.empty(q.shape[0])
+        self._ok(self.lib.ref_center(_d(q), q.shape[0], q.shape[1], _d(means)))
+        return q, means
+
+    def scale(self, q, n_vars, nx_i):
+        q = _f(q).copy()
+        s = np.empty(n_vars)
+        self._ok(self.lib.ref_scale(_d(q), n_vars, nx_i, q.shape[1], _d(s)))
+        return q, s
+
+    def project(self, tr, d):
+        tr, d = _f(tr), _f(d)
+        out = np.empty((tr.shape[1], d.shape[0]))
+        self._ok(self.lib.ref_project(_d(tr), _d(d), d.shape[0], tr.shape[1], _d(out)))
+        return out
+
+    def matmul(self, a, b):
+        a, b = _f(a), _f(b)
+        out = np.empty((a.shape[0], b.shape[1]))
+        self._ok(self.lib.ref_matmul(_d(a), a.shape[0], a.shape[1], _d(b), b.shape[1], _d(out)))
+        return out
+
+    def basis_rows(self, q, tr, rows):
+        q, tr = _f(q), _f(tr)
+        sel = np.ascontiguousarray(rows, dtype=np.uintp)
+        out = np.empty((sel.size, tr.shape[1]))
+        self._ok(self.lib.ref_basis_rows(_d(q), q.shape[0], q.shape[1], _d(tr), tr.shape[1],
+                                         sel.ctypes.data_as(_sp), sel.size, _d(out)))
+        return out
+
+    def eig_reduced_map(self, d, r):
+        d = _f(d)
+        nt = d.shape[0]
+        lam = np.empty(nt)
+        tr = np.empty((nt, max(r, 1)))
+        self._ok(self.lib.ref_eig_reduced_map(_d(d), nt, r, _d(lam), _d(tr)))
+        return lam, tr[:, :r]
+
+    def grid_search(self, qhat, b1, b2, max_growth, nt_p):
+        qhat = _f(qhat)
+        r, nt = qhat.shape
+        b1, b2 = _f(b1), _f(b2)
+        traj = np.empty((nt_p, r))
+        pe = np.empty(3)
+        self._ok(self.lib.ref_grid_search(_d(qhat), r, nt, _d(b1), b1.size, _d(b2), b2.size, max_growth, nt_p,
+                                          _d(traj), _d(pe)))
+        return traj, (pe[0], pe[1]), pe[2]

@@ -1,0 +1,380 @@
+"""Python mirror of the reference's stage API, over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference functions
+(paths relative to /root/reference/proj):
+
+  data::partition_rows            data.hpp:47,  data.cpp:86-103
+  transform::center_in_place      transform.hpp:27,    transform.cpp:10-20
+  transform::compute_global_scales transform.hpp:32-34, transform.cpp:22-41
+  transform::scale_in_place       transform.hpp:37,    transform.cpp:43-49
+  pod::local_gram / global_gram   pod.hpp:28-31,       pod.cpp:11-18
+  pod::project                    pod.hpp:49,          pod.cpp:103-105
+  postprocess::basis_rows         postprocess.hpp:25,  postprocess.cpp:12-34
+  reconstruct_field's Φ_r         postprocess.cpp:66
+
+Blocks live on the GPU (`LocalBlock` is device resident; `.values` downloads).
+The reference's comm::Comm argument is the per-rank `DeviceContext`, whose
+collectives run over NCCL. Used by the tests and bench.py; the C++ mirror for
+C++ callers is include/dopinf_b200.hpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+
+# ---- exceptions (include/dopinf/errors.hpp:9-73) ----------------------------
+class Error(RuntimeError):
+    pass
+
+
+class DataFormatError(Error):
+    pass
+
+
+class PartitionError(Error):
+    pass
+
+
+class CollectiveError(Error):
+    pass
+
+
+class DegenerateVariableError(Error):
+    pass
+
+
+class NotPsdError(Error):
+    pass
+
+
+class RankDeficiencyError(Error):
+    pass
+
+
+class SolveError(Error):
+    pass
+
+
+class InvalidArgumentError(Error):
+    pass
+
+
+class DeviceError(Error):
+    """CUDA / NCCL failure (no reference analogue)."""
+
+
+_STATUS = {
+    _lib.ERR_INVALID_ARGUMENT: InvalidArgumentError,
+    _lib.ERR_PARTITION: PartitionError,
+    _lib.ERR_COLLECTIVE: CollectiveError,
+    _lib.ERR_DEGENERATE_VARIABLE: DegenerateVariableError,
+    _lib.ERR_DEVICE: DeviceError,
+    _lib.ERR_OUT_OF_MEMORY: DeviceError,
+}
+
+
+def _check(rc: int, ctx=None, what: str = ""):
+    if rc == _lib.OK:
+        return
+    lib = _lib.load()
+    msg = lib.dopinf_b200_last_error(ctx._h).decode() if ctx is not None else ""
+    raise _STATUS.get(rc, Error)(f"{what}: {msg}" if what else msg)
+
+
+def _f64(a, shape=None) -> np.ndarray:
+    out = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None and out.shape != shape:
+        raise InvalidArgumentError(f"expected shape {shape}, got {out.shape}")
+    return out
+
+
+# ---- data.hpp -----------------------------------------------------------------
+@dataclass(frozen=True)
+class RowRange:
+    begin: int = 0
+    end: int = 0
+
+    def count(self) -> int:
+        return self.end - self.begin
+
+
+@dataclass
+class SnapshotHeader:
+    n_vars: int
+    nx: int
+    nt: int
+    var_names: list = field(default_factory=list)
+
+    def __post_init__(self):
+        if not self.var_names:
+            self.var_names = [f"var{j}" for j in range(self.n_vars)]
+
+
+def partition_rows(nx: int, p: int) -> list:
+    """data.cpp:86-103: floor(nx/p) rows per rank, remainder on the last rank."""
+    lib = _lib.load()
+    if p < 1:
+        raise PartitionError(f"partition_rows: rank count must be >= 1, got {p}")
+    if p > nx:
+        raise PartitionError(f"partition_rows: rank count {p} exceeds row count {nx}")
+    b = np.zeros(p, dtype=np.uintp)
+    e = np.zeros(p, dtype=np.uintp)
+    rc = lib.dopinf_b200_partition_rows(nx, p, _lib.sptr(b), _lib.sptr(e))
+    if rc == _lib.ERR_PARTITION:
+        raise PartitionError(f"partition_rows({nx}, {p})")
+    _check(rc)
+    return [RowRange(int(x), int(y)) for x, y in zip(b, e)]
+
+
+# ---- per-rank context (comm::Comm) ----------------------------------------------
+class DeviceContext:
+    """One rank: a B200, its stream, and (size > 1) an NCCL communicator."""
+
+    SUM, MAX, MIN = _lib.SUM, _lib.MAX, _lib.MIN
+
+    def __init__(self, device: int = 0, rank: int = 0, size: int = 1, unique_id: bytes | None = None,
+                 gram_reduce: str = "ordered"):
+        lib = _lib.load()
+        h = C.c_void_p()
+        uid = None
+        if size > 1:
+            if unique_id is None or len(unique_id) != _lib.UNIQUE_ID_BYTES:
+                raise InvalidArgumentError("size > 1 needs the rank-0 unique id bytes")
+            uid = C.create_string_buffer(bytes(unique_id), _lib.UNIQUE_ID_BYTES)
+        rc = lib.dopinf_b200_ctx_create(device, rank, size, uid, C.byref(h))
+        if rc != _lib.OK:
+            raise _STATUS.get(rc, Error)(f"ctx_create(device={device}, rank={rank}, size={size}) failed: "
+                                         f"{lib.dopinf_b200_status_string(rc).decode()}")
+        self._h = h
+        self._rank, self._size, self.device = rank, size, device
+        self.set_gram_reduce(gram_reduce)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(_lib.UNIQUE_ID_BYTES)
+        _check(_lib.load().dopinf_b200_get_unique_id(buf))
+        return buf.raw
+
+    def rank(self) -> int:
+        return self._rank
+
+    def size(self) -> int:
+        return self._size
+
+    def set_gram_reduce(self, mode: str):
+        m = {"ordered": _lib.GRAM_REDUCE_ORDERED, "nccl": _lib.GRAM_REDUCE_NCCL}[mode]
+        _check(_lib.load().dopinf_b200_set_gram_reduce(self._h, m), self)
+
+    def allreduce(self, data: np.ndarray, op: int) -> None:
+        """Comm::allreduce (comm.hpp:20-28) on a host float64 array, in place."""
+        if data.dtype != np.float64 or not data.flags.c_contiguous:
+            raise InvalidArgumentError("allreduce: needs a C-contiguous float64 array")
+        _check(_lib.load().dopinf_b200_allreduce(self._h, _lib.dptr(data), data.size, op), self, "allreduce")
+
+    def barrier(self) -> None:
+        _check(_lib.load().dopinf_b200_barrier(self._h), self, "barrier")
+
+    def stage_ms(self, stage: str) -> float:
+        v = C.c_double()
+        _check(_lib.load().dopinf_b200_stage_ms(self._h, _lib.STAGES.index(stage), C.byref(v)), self)
+        return v.value
+
+    def stream(self) -> int:
+        return _lib.load().dopinf_b200_ctx_stream(self._h) or 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().dopinf_b200_ctx_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+# ---- device-resident data::LocalBlock ----------------------------------------------
+class LocalBlock:
+    """data::LocalBlock (data.hpp:38-42) held on the device: (n_vars·nx_i) × nt fp64,
+    block row j*nx_i + k = variable j at global spatial index row_range.begin + k."""
+
+    def __init__(self, ctx: DeviceContext, n_vars: int, row_range: RowRange, nt: int, values=None,
+                 rank: int | None = None):
+        lib = _lib.load()
+        self.ctx = ctx
+        self.rank = ctx.rank() if rank is None else rank
+        self.row_range = row_range
+        self.n_vars, self.nt = n_vars, nt
+        self.nx_i = row_range.count()
+        self.rows = n_vars * self.nx_i
+        h = C.c_void_p()
+        _check(lib.dopinf_b200_block_create(ctx._h, n_vars, self.nx_i, row_range.begin, nt, C.byref(h)), ctx,
+               "block_create")
+        self._h = h
+        if values is not None:
+            self.upload(values)
+
+    def upload(self, values) -> None:
+        v = _f64(values, (self.rows, self.nt))
+        _check(_lib.load().dopinf_b200_block_upload(self._h, _lib.dptr(v), self.nt), self.ctx, "upload")
+
+    def upload_ptr(self, host_ptr: int, host_ld: int) -> None:
+        """Upload from a raw host pointer (e.g. pinned torch memory)."""
+        _check(_lib.load().dopinf_b200_block_upload(self._h, C.cast(host_ptr, _lib._dp), host_ld), self.ctx,
+               "upload")
+
+    @property
+    def values(self) -> np.ndarray:
+        out = np.empty((self.rows, self.nt), dtype=np.float64)
+        _check(_lib.load().dopinf_b200_block_download(self._h, _lib.dptr(out), self.nt), self.ctx, "download")
+        return out
+
+    def device_ptr(self):
+        p = _lib._dp()
+        ld = C.c_size_t()
+        _check(_lib.load().dopinf_b200_block_device(self._h, C.byref(p), C.byref(ld)), self.ctx)
+        return C.cast(p, C.c_void_p).value, ld.value
+
+    def synth_oscillator(self, seed: int, n_modes: int, dt: float = 1e-3, noise: float = 1e-3, amps=None):
+        a = None if amps is None else _f64(amps, (self.n_vars,))
+        _check(_lib.load().dopinf_b200_block_synth_oscillator(self._h, seed, n_modes, dt, noise,
+                                                              _lib.dptr(a)), self.ctx, "synth")
+
+    def synth_lowrank(self, seed: int, rank: int = 50, amplitude: float = 10.0):
+        _check(_lib.load().dopinf_b200_block_synth_lowrank(self._h, seed, rank, amplitude), self.ctx, "synth")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().dopinf_b200_block_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+# ---- transform.hpp -------------------------------------------------------------------
+@dataclass
+class TransformParams:
+    local_means: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    scales: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    scaling_enabled: bool = False
+
+    def row_scale(self, row: int, nx_i: int) -> float:
+        return float(self.scales[row // nx_i]) if self.scaling_enabled else 1.0
+
+
+def center_in_place(block: LocalBlock) -> np.ndarray:
+    """transform.cpp:10-20: subtract each row's temporal mean; return the means."""
+    means = np.empty(block.rows, dtype=np.float64)
+    _check(_lib.load().dopinf_b200_center(block._h, _lib.dptr(means)), block.ctx, "center_in_place")
+    return means
+
+
+def compute_global_scales(block: LocalBlock, header: SnapshotHeader, comm: DeviceContext | None = None):
+    """transform.cpp:22-41: per-variable global max-abs (MAX all-reduce over the ranks)."""
+    if comm is not None and comm is not block.ctx:
+        raise CollectiveError("compute_global_scales: comm must be the block's DeviceContext")
+    scales = np.empty(block.n_vars, dtype=np.float64)
+    bad = C.c_size_t(0)
+    rc = _lib.load().dopinf_b200_global_scales(block._h, _lib.dptr(scales), C.byref(bad))
+    if rc == _lib.ERR_DEGENERATE_VARIABLE:
+        name = header.var_names[bad.value]
+        raise DegenerateVariableError(
+            f"variable '{name}' is constant in time; max-abs scaling is undefined")
+    _check(rc, block.ctx, "compute_global_scales")
+    return scales
+
+
+def scale_in_place(block: LocalBlock, scales) -> None:
+    """transform.cpp:43-49: divide each variable's rows by its scale."""
+    s = _f64(scales, (block.n_vars,))
+    _check(_lib.load().dopinf_b200_scale(block._h, _lib.dptr(s)), block.ctx, "scale_in_place")
+
+
+# ---- pod.hpp ------------------------------------------------------------------------------
+def local_gram(block: LocalBlock) -> np.ndarray:
+    """pod.cpp:11-13: D_i = Q_iᵀ Q_i (full symmetric nt × nt)."""
+    d = np.empty((block.nt, block.nt), dtype=np.float64)
+    _check(_lib.load().dopinf_b200_local_gram(block._h, _lib.dptr(d)), block.ctx, "local_gram")
+    return d
+
+
+def global_gram(local: np.ndarray | None, comm: DeviceContext) -> np.ndarray:
+    """pod.cpp:15-18: SUM all-reduce of the local Gram (identical on all ranks).
+    The device copy of `local` (from local_gram on this context) is reduced."""
+    nt = local.shape[0] if local is not None else None
+    d = np.empty((nt, nt), dtype=np.float64) if nt is not None else None
+    if d is None:
+        raise InvalidArgumentError("global_gram: pass the local Gram returned by local_gram")
+    _check(_lib.load().dopinf_b200_global_gram(comm._h, _lib.dptr(d)), comm, "global_gram")
+    return d
+
+
+def project(tr, d, ctx: DeviceContext) -> np.ndarray:
+    """pod.cpp:103-105: Q̂ = T_rᵀ D (r × nt), reference FMA order on the device."""
+    tr = _f64(tr)
+    nt, r = tr.shape
+    d = _f64(d, (nt, nt))
+    out = np.empty((r, nt), dtype=np.float64)
+    _check(_lib.load().dopinf_b200_project_host(ctx._h, _lib.dptr(tr), _lib.dptr(d), nt, r, _lib.dptr(out)),
+           ctx, "project")
+    return out
+
+
+def project_resident(ctx: DeviceContext, tr) -> np.ndarray:
+    """Q̂ = T_rᵀ D with the context's device-resident (global) Gram."""
+    tr = _f64(tr)
+    nt, r = tr.shape
+    out = np.empty((r, nt), dtype=np.float64)
+    _check(_lib.load().dopinf_b200_project(ctx._h, _lib.dptr(tr), nt, r, _lib.dptr(out)), ctx, "project")
+    return out
+
+
+# ---- postprocess.hpp -------------------------------------------------------------------------
+def basis_rows(block: LocalBlock, tr, local_rows) -> np.ndarray:
+    """postprocess.cpp:12-34: rows of Φ_r = Q·T_r for the selected local rows."""
+    tr = _f64(tr)
+    if tr.shape[0] != block.nt:
+        raise InvalidArgumentError("basis_rows: block and map disagree on nt")
+    rows = np.ascontiguousarray(local_rows, dtype=np.uintp)
+    r = tr.shape[1]
+    out = np.empty((rows.size, r), dtype=np.float64)
+    _check(_lib.load().dopinf_b200_basis_rows(block._h, _lib.dptr(tr), r, _lib.sptr(rows), rows.size,
+                                              _lib.dptr(out)), block.ctx, "basis_rows")
+    return out
+
+
+def basis(block: LocalBlock, tr, download: bool = True):
+    """Φ_r = Q·T_r over the whole block (postprocess.cpp:66), rows × r."""
+    tr = _f64(tr)
+    if tr.shape[0] != block.nt:
+        raise InvalidArgumentError("basis: block and map disagree on nt")
+    r = tr.shape[1]
+    out = np.empty((block.rows, r), dtype=np.float64) if download else None
+    _check(_lib.load().dopinf_b200_basis(block._h, _lib.dptr(tr), r, _lib.dptr(out)), block.ctx, "basis")
+    return out
+
+
+def snapshot_pass(block: LocalBlock, scaling: bool):
+    """Steps II–III of pipeline::run_rank (pipeline.cpp:270-280) in one call:
+    returns (TransformParams, D)."""
+    means = np.empty(block.rows, dtype=np.float64)
+    scales = np.empty(block.n_vars, dtype=np.float64)
+    d = np.empty((block.nt, block.nt), dtype=np.float64)
+    _check(_lib.load().dopinf_b200_snapshot_pass(block._h, 1 if scaling else 0, _lib.dptr(means),
+                                                 _lib.dptr(scales), _lib.dptr(d)), block.ctx, "snapshot_pass")
+    params = TransformParams(means, scales if scaling else np.zeros(0), scaling)
+    return params, d
+
+
+def kernel_launches() -> int:
+    return int(_lib.load().dopinf_b200_kernel_launches())

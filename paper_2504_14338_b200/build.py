@@ -1,0 +1,86 @@
+"""In-tree build of the sm_100a extension (libdopinf_b200.so) and the oracle.
+
+The extension is compiled with nvcc for sm_100a only and linked against NCCL;
+the .so lands next to this file so it travels to the GPU box with the repo
+snapshot. The oracle (test infrastructure) is built by oracle/Makefile.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = PKG / "_build"
+LIB = PKG / "libdopinf_b200.so"
+SOURCES = ["capi.cu", "gram.cu", "transform.cu", "project.cu", "synth.cu"]
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC,-O2",
+    "-I", str(ROOT / "include"),
+]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found: the sm_100a extension cannot be built")
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build_extension(force: bool = False, verbose: bool = False) -> Path:
+    nvcc = _nvcc()
+    BUILD.mkdir(exist_ok=True)
+    headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "dopinf_b200.h"]
+    jobs = []
+    for src in SOURCES:
+        obj = BUILD / (Path(src).stem + ".o")
+        if force or _stale(obj, [CSRC / src, *headers]):
+            jobs.append([nvcc, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)])
+    with cf.ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
+        for cmd, res in zip(jobs, ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs)):
+            if res.returncode != 0:
+                raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+            if verbose and (res.stdout or res.stderr):
+                print(res.stdout, res.stderr)
+    objs = [BUILD / (Path(s).stem + ".o") for s in SOURCES]
+    if force or jobs or _stale(LIB, objs):
+        cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB),
+               *map(str, objs), "-lnccl"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    return LIB
+
+
+def build_oracle(with_reference: bool | None = None) -> None:
+    """oracle/_build (C restatement) always; oracle/_ref when /root/reference exists."""
+    oracle = ROOT / "oracle"
+    res = subprocess.run(["make", "-s", "-C", str(oracle), "oracle"], capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"oracle build failed:\n{res.stdout}\n{res.stderr}")
+    ref_src = Path(os.environ.get("DOPINF_REFERENCE", "/root/reference/proj"))
+    if with_reference is None:
+        with_reference = (ref_src / "src" / "pod.cpp").exists()
+    if with_reference:
+        res = subprocess.run(["make", "-s", "-j8", "-C", str(oracle), "ref", f"REF={ref_src}"],
+                             capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"reference oracle build failed:\n{res.stdout}\n{res.stderr}")
+
+
+if __name__ == "__main__":
+    print(build_extension(verbose=True))
+    build_oracle()

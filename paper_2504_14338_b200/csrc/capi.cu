@@ -1,0 +1,805 @@
+// capi.cu — the C ABI (include/dopinf_b200.h): per-rank contexts, device-
+// resident LocalBlocks, NCCL collectives and the stage orchestration that the
+// reference's pipeline::run_rank (proj/src/pipeline.cpp:270-298) performs on
+// the host. Every entry point is synchronous at the boundary, never throws,
+// and maps failures onto the reference's exception classes by status code.
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/dopinf_b200.h"
+#include "common.cuh"
+#include "gram.h"
+#include "project.h"
+#include "synth.h"
+#include "transform.h"
+
+using namespace dopinf_b200;
+
+namespace dopinf_b200 {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+cudaError_t set_smem_attr_once(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({func, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({func, dev});
+    return e;
+}
+
+}  // namespace dopinf_b200
+
+namespace {
+
+// Status + message carrier; thrown only inside this file.
+struct Fail {
+    int status;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int status, std::string msg) { throw Fail{status, std::move(msg)}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        fail(DOPINF_B200_ERR_OUT_OF_MEMORY, std::string(what) + ": out of device memory");
+    }
+    if (e != cudaSuccess) fail(DOPINF_B200_ERR_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void ckn(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) {
+        fail(DOPINF_B200_ERR_COLLECTIVE, std::string(what) + ": " + ncclGetErrorString(r));
+    }
+}
+
+// Grow-only device buffer.
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    template <class T>
+    T* get(size_t count, const char* what) {
+        const size_t need = std::max<size_t>(count * sizeof(T), 16);
+        if (need > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            bytes = 0;
+            ck(cudaMalloc(&p, need), what);
+            bytes = need;
+        }
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+}  // namespace
+
+struct dopinf_b200_ctx {
+    int device = 0, rank = 0, size = 1;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    int gram_reduce = DOPINF_B200_GRAM_REDUCE_ORDERED;
+    std::string err;
+
+    // Gram state
+    int K = 0;                 // nt of the Gram held on the device
+    bool have_gram = false;
+    int plan_K = -1;
+    long long plan_rows = -1;
+    gram::Plan plan;
+    int tiles_K = -1;
+    DBuf tiles, work, counters, packed, gather, dmat, dhost_in;
+    bool counters_zeroed = false;
+    // scratch
+    DBuf scales, tr, trt, qhat, sel, rows_out, span;
+    // stage timing
+    cudaEvent_t ev[DOPINF_B200_STAGE_COUNT][2] = {};
+    bool ev_done[DOPINF_B200_STAGE_COUNT] = {};
+
+    void record(int stage, int which) {
+        cudaEventRecord(ev[stage][which], stream);
+        if (which == 1) ev_done[stage] = true;
+    }
+    void sync(const char* what) { ck(cudaStreamSynchronize(stream), what); }
+};
+
+struct dopinf_b200_block {
+    dopinf_b200_ctx* ctx = nullptr;
+    size_t n_vars = 0, nx_i = 0, row_begin = 0, nt = 0, ld = 0, rows = 0;
+    double* q = nullptr;
+    DBuf means, varmax, phi;
+    int phi_ld = 0;
+    bool pending_center = false;  // means computed, subtraction not yet applied
+    bool stats_valid = false;     // varmax describes the current (logical) values
+    CUtensorMap gram_map{};
+    const double* gram_map_base = nullptr;
+};
+
+namespace {
+
+template <class F>
+int guarded(dopinf_b200_ctx* ctx, F&& fn) {
+    if (!ctx) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    try {
+        DeviceGuard dg(ctx->device);
+        fn();
+        ctx->err.clear();
+        return DOPINF_B200_OK;
+    } catch (const Fail& f) {
+        ctx->err = f.msg;
+        return f.status;
+    } catch (const std::bad_alloc&) {
+        ctx->err = "host allocation failed";
+        return DOPINF_B200_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        ctx->err = "unexpected failure";
+        return DOPINF_B200_ERR_DEVICE;
+    }
+}
+
+void require(bool ok, const std::string& msg) {
+    if (!ok) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, msg);
+}
+
+// Apply a pending centering so the device values equal the reference's block.
+void materialize(dopinf_b200_block* b) {
+    if (!b->pending_center) return;
+    auto* c = b->ctx;
+    c->record(DOPINF_B200_STAGE_APPLY, 0);
+    ck(transform::launch_apply(b->q, b->ld, static_cast<long long>(b->rows), static_cast<int>(b->nt),
+                               static_cast<long long>(b->nx_i), b->means.get<double>(b->rows, "means"),
+                               nullptr, c->num_sms, c->stream),
+       "apply");
+    c->record(DOPINF_B200_STAGE_APPLY, 1);
+    b->pending_center = false;
+}
+
+void run_stats(dopinf_b200_block* b, bool center) {
+    auto* c = b->ctx;
+    double* vm = b->varmax.get<double>(b->n_vars, "varmax");
+    double* mn = b->means.get<double>(b->rows, "means");
+    c->record(DOPINF_B200_STAGE_STATS, 0);
+    ck(cudaMemsetAsync(vm, 0, b->n_vars * sizeof(double), c->stream), "memset");
+    ck(transform::launch_stats(b->q, b->ld, static_cast<long long>(b->rows), static_cast<int>(b->nt),
+                               static_cast<long long>(b->nx_i), static_cast<int>(b->n_vars), center,
+                               mn, vm, c->num_sms, c->stream),
+       "stats");
+    c->record(DOPINF_B200_STAGE_STATS, 1);
+}
+
+void do_center(dopinf_b200_block* b, double* means_host) {
+    materialize(b);  // a second centering acts on centered values, as in the reference
+    run_stats(b, true);
+    b->pending_center = true;
+    b->stats_valid = true;
+    if (means_host) {
+        ck(cudaMemcpyAsync(means_host, b->means.get<double>(b->rows, "means"), b->rows * sizeof(double),
+                           cudaMemcpyDeviceToHost, b->ctx->stream),
+           "means D2H");
+    }
+}
+
+void do_global_scales(dopinf_b200_block* b, double* scales_host, size_t* degenerate) {
+    auto* c = b->ctx;
+    if (!b->stats_valid) {
+        run_stats(b, false);
+        b->stats_valid = true;
+    }
+    double* vm = b->varmax.get<double>(b->n_vars, "varmax");
+    double* red = c->scales.get<double>(b->n_vars, "scales");
+    c->record(DOPINF_B200_STAGE_SCALES, 0);
+    if (c->size > 1) {
+        ckn(ncclAllReduce(vm, red, b->n_vars, ncclFloat64, ncclMax, c->comm, c->stream), "allreduce(MAX)");
+    } else {
+        ck(cudaMemcpyAsync(red, vm, b->n_vars * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
+    }
+    c->record(DOPINF_B200_STAGE_SCALES, 1);
+    std::vector<double> host(b->n_vars);
+    ck(cudaMemcpyAsync(host.data(), red, b->n_vars * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+       "scales D2H");
+    c->sync("global_scales");
+    if (scales_host) std::memcpy(scales_host, host.data(), b->n_vars * sizeof(double));
+    for (size_t j = 0; j < b->n_vars; ++j) {
+        if (host[j] == 0.0) {
+            if (degenerate) *degenerate = j;
+            fail(DOPINF_B200_ERR_DEGENERATE_VARIABLE,
+                 "variable " + std::to_string(j) + " is constant in time; max-abs scaling is undefined");
+        }
+    }
+}
+
+void do_scale(dopinf_b200_block* b, const double* scales_host) {
+    auto* c = b->ctx;
+    double* ds = c->scales.get<double>(b->n_vars, "scales");
+    ck(cudaMemcpyAsync(ds, scales_host, b->n_vars * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+       "scales H2D");
+    c->record(DOPINF_B200_STAGE_APPLY, 0);
+    ck(transform::launch_apply(b->q, b->ld, static_cast<long long>(b->rows), static_cast<int>(b->nt),
+                               static_cast<long long>(b->nx_i),
+                               b->pending_center ? b->means.get<double>(b->rows, "means") : nullptr, ds,
+                               c->num_sms, c->stream),
+       "apply");
+    c->record(DOPINF_B200_STAGE_APPLY, 1);
+    b->pending_center = false;
+    b->stats_valid = false;
+}
+
+void copy_d_out(dopinf_b200_ctx* c, double* d_host) {
+    if (!d_host) return;
+    c->record(DOPINF_B200_STAGE_DOWNLOAD, 0);
+    ck(cudaMemcpyAsync(d_host, c->dmat.get<double>(static_cast<size_t>(c->K) * c->K, "D"),
+                       static_cast<size_t>(c->K) * c->K * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+       "D D2H");
+    c->record(DOPINF_B200_STAGE_DOWNLOAD, 1);
+}
+
+void unpack(dopinf_b200_ctx* c) {
+    const int K = c->K;
+    c->record(DOPINF_B200_STAGE_UNPACK, 0);
+    ck(gram::launch_unpack(c->packed.get<double>(gram::packed_count(K), "packed"), K,
+                           c->dmat.get<double>(static_cast<size_t>(K) * K, "D"), c->stream),
+       "unpack");
+    c->record(DOPINF_B200_STAGE_UNPACK, 1);
+}
+
+void do_local_gram(dopinf_b200_block* b, double* d_host) {
+    auto* c = b->ctx;
+    materialize(b);
+    const int K = static_cast<int>(b->nt);
+    const long long rows = static_cast<long long>(b->rows);
+    c->have_gram = false;
+    c->K = K;
+    double* packed = c->packed.get<double>(gram::packed_count(K), "packed");
+    if (rows == 0) {
+        ck(cudaMemsetAsync(packed, 0, gram::packed_count(K) * sizeof(double), c->stream), "memset");
+    } else {
+        if (c->tiles_K != K) {
+            const std::vector<gram::TileInfo> t = gram::plan_tiles(K);
+            ck(cudaMemcpy(c->tiles.get<gram::TileInfo>(t.size(), "tiles"), t.data(),
+                          t.size() * sizeof(gram::TileInfo), cudaMemcpyHostToDevice),
+               "tiles H2D");
+            c->tiles_K = K;
+        }
+        if (c->plan_K != K || c->plan_rows != rows) {
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            const size_t cap = std::min<size_t>(size_t(2) << 30, std::max<size_t>(free_b / 8, size_t(64) << 20));
+            c->plan = gram::make_plan(rows, K, c->num_sms, cap);
+            c->plan_K = K;
+            c->plan_rows = rows;
+        }
+        if (b->gram_map_base != b->q) {
+            ck(gram::make_tensor_map(&b->gram_map, b->q, rows, K, b->ld), "tensor map");
+            b->gram_map_base = b->q;
+        }
+        int* counters = c->counters.get<int>(2, "counters");
+        if (!c->counters_zeroed) {
+            ck(cudaMemsetAsync(counters, 0, 2 * sizeof(int), c->stream), "memset");
+            c->counters_zeroed = true;
+        }
+        double* work = c->work.get<double>(c->plan.workspace_doubles, "workspace");
+        const auto* tiles = c->tiles.get<gram::TileInfo>(c->plan.n_tiles, "tiles");
+        c->record(DOPINF_B200_STAGE_GRAM, 0);
+        ck(gram::launch_gram(c->plan, b->gram_map, tiles, work, counters, c->stream), "gram");
+        c->record(DOPINF_B200_STAGE_GRAM, 1);
+        c->record(DOPINF_B200_STAGE_GRAM_REDUCE, 0);
+        ck(gram::launch_reduce(c->plan, tiles, work, packed, c->stream), "gram reduce");
+        c->record(DOPINF_B200_STAGE_GRAM_REDUCE, 1);
+    }
+    unpack(c);
+    c->have_gram = true;
+    copy_d_out(c, d_host);
+}
+
+void do_global_gram(dopinf_b200_ctx* c, double* d_host) {
+    if (!c->have_gram) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "global_gram: no local Gram on this context");
+    const int K = c->K;
+    const size_t count = gram::packed_count(K);
+    if (c->size > 1) {
+        double* packed = c->packed.get<double>(count, "packed");
+        c->record(DOPINF_B200_STAGE_ALLREDUCE, 0);
+        if (c->gram_reduce == DOPINF_B200_GRAM_REDUCE_NCCL) {
+            ckn(ncclAllReduce(packed, packed, count, ncclFloat64, ncclSum, c->comm, c->stream),
+                "allreduce(SUM)");
+        } else {
+            double* parts = c->gather.get<double>(count * c->size, "gather");
+            ckn(ncclAllGather(packed, parts, count, ncclFloat64, c->comm, c->stream), "allgather");
+            ck(gram::launch_ordered_sum(parts, c->size, count, packed, c->stream), "ordered sum");
+        }
+        c->record(DOPINF_B200_STAGE_ALLREDUCE, 1);
+        unpack(c);
+    }
+    copy_d_out(c, d_host);
+}
+
+void do_project(dopinf_b200_ctx* c, const double* tr_host, const double* d_dev, size_t nt, size_t r,
+                double* qhat_host) {
+    require(r >= 1 && r <= nt, "project: r must lie in [1, nt]");
+    double* dtr = c->tr.get<double>(nt * r, "tr");
+    double* dq = c->qhat.get<double>(nt * r, "qhat");
+    ck(cudaMemcpyAsync(dtr, tr_host, nt * r * sizeof(double), cudaMemcpyHostToDevice, c->stream), "tr H2D");
+    c->record(DOPINF_B200_STAGE_PROJECT, 0);
+    ck(project::launch_project(dtr, d_dev, static_cast<int>(nt), static_cast<int>(r), dq, c->stream),
+       "project");
+    c->record(DOPINF_B200_STAGE_PROJECT, 1);
+    if (qhat_host) {
+        ck(cudaMemcpyAsync(qhat_host, dq, nt * r * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+           "qhat D2H");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int dopinf_b200_abi_version(void) { return DOPINF_B200_ABI_VERSION; }
+
+uint64_t dopinf_b200_kernel_launches(void) { return g_launches.load(); }
+
+const char* dopinf_b200_status_string(int status) {
+    switch (status) {
+        case DOPINF_B200_OK: return "ok";
+        case DOPINF_B200_ERR_INVALID_ARGUMENT: return "InvalidArgumentError";
+        case DOPINF_B200_ERR_PARTITION: return "PartitionError";
+        case DOPINF_B200_ERR_COLLECTIVE: return "CollectiveError";
+        case DOPINF_B200_ERR_DEGENERATE_VARIABLE: return "DegenerateVariableError";
+        case DOPINF_B200_ERR_DEVICE: return "DeviceError";
+        case DOPINF_B200_ERR_OUT_OF_MEMORY: return "OutOfMemoryError";
+        default: return "unknown status";
+    }
+}
+
+int dopinf_b200_get_unique_id(unsigned char* id) {
+    if (!id) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    static_assert(sizeof(ncclUniqueId) == DOPINF_B200_UNIQUE_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId uid;
+    if (ncclGetUniqueId(&uid) != ncclSuccess) return DOPINF_B200_ERR_COLLECTIVE;
+    std::memcpy(id, &uid, sizeof uid);
+    return DOPINF_B200_OK;
+}
+
+int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* id,
+                           dopinf_b200_ctx** out) {
+    if (!out || size < 1 || rank < 0 || rank >= size || (size > 1 && !id)) {
+        return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    auto* c = new (std::nothrow) dopinf_b200_ctx;
+    if (!c) return DOPINF_B200_ERR_OUT_OF_MEMORY;
+    c->device = device;
+    c->rank = rank;
+    c->size = size;
+    const int rc = guarded(c, [&] {
+        int ndev = 0;
+        ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) {
+            fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "device " + std::to_string(device) + " not present");
+        }
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10 || prop.minor != 0) {
+            fail(DOPINF_B200_ERR_DEVICE, std::string("device is ") + prop.name +
+                                             " (sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
+                                             "); this build targets sm_100a (B200) only");
+        }
+        c->num_sms = prop.multiProcessorCount;
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (auto& pair : c->ev) {
+            ck(cudaEventCreate(&pair[0]), "cudaEventCreate");
+            ck(cudaEventCreate(&pair[1]), "cudaEventCreate");
+        }
+        if (size > 1) {
+            ncclUniqueId uid;
+            std::memcpy(&uid, id, sizeof uid);
+            ckn(ncclCommInitRank(&c->comm, size, uid, rank), "ncclCommInitRank");
+        }
+    });
+    if (rc != DOPINF_B200_OK) {
+        std::fprintf(stderr, "dopinf_b200_ctx_create: %s\n", c->err.c_str());
+        dopinf_b200_ctx_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return DOPINF_B200_OK;
+}
+
+void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
+    if (!c) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (auto& pair : c->ev) {
+        if (pair[0]) cudaEventDestroy(pair[0]);
+        if (pair[1]) cudaEventDestroy(pair[1]);
+    }
+    for (DBuf* b : {&c->tiles, &c->work, &c->counters, &c->packed, &c->gather, &c->dmat, &c->dhost_in,
+                    &c->scales, &c->tr, &c->trt, &c->qhat, &c->sel, &c->rows_out, &c->span}) {
+        b->release();
+    }
+    if (c->stream) cudaStreamDestroy(c->stream);
+    cudaSetDevice(prev);
+    delete c;
+}
+
+int dopinf_b200_ctx_rank(const dopinf_b200_ctx* c) { return c ? c->rank : -1; }
+int dopinf_b200_ctx_size(const dopinf_b200_ctx* c) { return c ? c->size : -1; }
+const char* dopinf_b200_last_error(const dopinf_b200_ctx* c) { return c ? c->err.c_str() : "null context"; }
+void* dopinf_b200_ctx_stream(dopinf_b200_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int dopinf_b200_set_gram_reduce(dopinf_b200_ctx* c, int mode) {
+    return guarded(c, [&] {
+        require(mode == DOPINF_B200_GRAM_REDUCE_ORDERED || mode == DOPINF_B200_GRAM_REDUCE_NCCL,
+                "set_gram_reduce: unknown mode");
+        c->gram_reduce = mode;
+    });
+}
+
+int dopinf_b200_allreduce(dopinf_b200_ctx* c, double* data, size_t count, int op) {
+    return guarded(c, [&] {
+        require(op >= DOPINF_B200_SUM && op <= DOPINF_B200_MIN, "allreduce: unknown op");
+        require(count == 0 || data, "allreduce: null data");
+        if (c->size == 1 || count == 0) return;
+        double* buf = c->span.get<double>(count * (op == DOPINF_B200_SUM ? c->size + 1 : 1), "span");
+        ck(cudaMemcpyAsync(buf, data, count * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+        if (op == DOPINF_B200_SUM) {
+            // Ascending-rank order, as the reference's in-process backend sums.
+            double* parts = buf + count;
+            ckn(ncclAllGather(buf, parts, count, ncclFloat64, c->comm, c->stream), "allgather");
+            ck(gram::launch_ordered_sum(parts, c->size, count, buf, c->stream), "ordered sum");
+        } else {
+            ckn(ncclAllReduce(buf, buf, count, ncclFloat64, op == DOPINF_B200_MAX ? ncclMax : ncclMin,
+                              c->comm, c->stream),
+                "allreduce");
+        }
+        ck(cudaMemcpyAsync(data, buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        c->sync("allreduce");
+    });
+}
+
+int dopinf_b200_barrier(dopinf_b200_ctx* c) {
+    double one = 1.0;
+    return dopinf_b200_allreduce(c, &one, 1, DOPINF_B200_MAX);
+}
+
+int dopinf_b200_stage_ms(const dopinf_b200_ctx* c, int stage, double* ms) {
+    if (!c || !ms || stage < 0 || stage >= DOPINF_B200_STAGE_COUNT) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    *ms = 0.0;
+    if (!c->ev_done[stage]) return DOPINF_B200_OK;
+    float f = 0.0f;
+    if (cudaEventSynchronize(c->ev[stage][1]) != cudaSuccess ||
+        cudaEventElapsedTime(&f, c->ev[stage][0], c->ev[stage][1]) != cudaSuccess) {
+        return DOPINF_B200_ERR_DEVICE;
+    }
+    *ms = f;
+    return DOPINF_B200_OK;
+}
+
+int dopinf_b200_partition_rows(size_t nx, int p, size_t* begin, size_t* end) {
+    // data.cpp:86-103
+    if (p < 1 || static_cast<size_t>(p) > nx) return DOPINF_B200_ERR_PARTITION;
+    if (!begin || !end) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    const size_t ranks = static_cast<size_t>(p);
+    const size_t base = nx / ranks;
+    for (size_t r = 0; r < ranks; ++r) {
+        begin[r] = r * base;
+        end[r] = (r + 1 == ranks) ? nx : (r + 1) * base;
+    }
+    return DOPINF_B200_OK;
+}
+
+int dopinf_b200_block_create(dopinf_b200_ctx* c, size_t n_vars, size_t nx_i, size_t row_begin, size_t nt,
+                             dopinf_b200_block** out) {
+    if (!out) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto* b = new (std::nothrow) dopinf_b200_block;
+    if (!b) return DOPINF_B200_ERR_OUT_OF_MEMORY;
+    const int rc = guarded(c, [&] {
+        require(n_vars >= 1 && nt >= 1, "block_create: n_vars and nt must be >= 1");
+        require(nt <= (1u << 20), "block_create: nt too large");
+        b->ctx = c;
+        b->n_vars = n_vars;
+        b->nx_i = nx_i;
+        b->row_begin = row_begin;
+        b->nt = nt;
+        b->ld = (nt + 1) / 2 * 2;  // 16-byte rows for TMA and 128-bit accesses
+        b->rows = n_vars * nx_i;
+        if (b->rows > 0) {
+            ck(cudaMalloc(&b->q, b->rows * b->ld * sizeof(double)), "block values");
+            if (b->ld != nt) {
+                ck(cudaMemsetAsync(b->q, 0, b->rows * b->ld * sizeof(double), c->stream), "memset");
+            }
+        }
+        b->varmax.get<double>(n_vars, "varmax");
+        c->sync("block_create");
+    });
+    if (rc != DOPINF_B200_OK) {
+        if (b->q) cudaFree(b->q);
+        delete b;
+        return rc;
+    }
+    *out = b;
+    return DOPINF_B200_OK;
+}
+
+void dopinf_b200_block_destroy(dopinf_b200_block* b) {
+    if (!b) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(b->ctx->device);
+    cudaStreamSynchronize(b->ctx->stream);
+    if (b->q) cudaFree(b->q);
+    b->means.release();
+    b->varmax.release();
+    b->phi.release();
+    cudaSetDevice(prev);
+    delete b;
+}
+
+int dopinf_b200_block_upload(dopinf_b200_block* b, const double* host, size_t host_ld) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(host_ld >= b->nt && (b->rows == 0 || host), "block_upload: bad host buffer");
+        c->record(DOPINF_B200_STAGE_UPLOAD, 0);
+        if (b->rows > 0) {
+            if (host_ld == b->ld) {
+                ck(cudaMemcpyAsync(b->q, host, b->rows * b->ld * sizeof(double), cudaMemcpyHostToDevice,
+                                   c->stream),
+                   "upload");
+            } else {
+                ck(cudaMemcpy2DAsync(b->q, b->ld * sizeof(double), host, host_ld * sizeof(double),
+                                     b->nt * sizeof(double), b->rows, cudaMemcpyHostToDevice, c->stream),
+                   "upload");
+            }
+        }
+        c->record(DOPINF_B200_STAGE_UPLOAD, 1);
+        b->pending_center = false;
+        b->stats_valid = false;
+        c->sync("block_upload");
+    });
+}
+
+int dopinf_b200_block_download(dopinf_b200_block* b, double* host, size_t host_ld) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(host_ld >= b->nt && (b->rows == 0 || host), "block_download: bad host buffer");
+        materialize(b);
+        c->record(DOPINF_B200_STAGE_DOWNLOAD, 0);
+        if (b->rows > 0) {
+            ck(cudaMemcpy2DAsync(host, host_ld * sizeof(double), b->q, b->ld * sizeof(double),
+                                 b->nt * sizeof(double), b->rows, cudaMemcpyDeviceToHost, c->stream),
+               "download");
+        }
+        c->record(DOPINF_B200_STAGE_DOWNLOAD, 1);
+        c->sync("block_download");
+    });
+}
+
+int dopinf_b200_block_device(dopinf_b200_block* b, double** values, size_t* ld) {
+    if (!b || !values || !ld) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    return guarded(b->ctx, [&] {
+        materialize(b);
+        b->ctx->sync("block_device");
+        b->stats_valid = false;  // the caller may write through the pointer
+        *values = b->q;
+        *ld = b->ld;
+    });
+}
+
+int dopinf_b200_block_synth_oscillator(dopinf_b200_block* b, uint64_t seed, int n_modes, double dt,
+                                       double noise, const double* amps) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        if (b->rows == 0) return;
+        ck(synth::oscillator(b->q, b->ld, static_cast<long long>(b->rows), static_cast<int>(b->nt),
+                             static_cast<long long>(b->nx_i), static_cast<long long>(b->row_begin),
+                             static_cast<int>(b->n_vars), seed, n_modes, dt, noise, amps, c->num_sms,
+                             c->stream),
+           "synth");
+        b->pending_center = false;
+        b->stats_valid = false;
+        c->sync("synth");
+    });
+}
+
+int dopinf_b200_block_synth_lowrank(dopinf_b200_block* b, uint64_t seed, int rank, double amplitude) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        if (b->rows == 0) return;
+        ck(synth::lowrank(b->q, b->ld, static_cast<long long>(b->rows), static_cast<int>(b->nt),
+                          static_cast<long long>(b->nx_i), static_cast<long long>(b->row_begin), seed, rank,
+                          amplitude, c->num_sms, c->stream),
+           "synth");
+        b->pending_center = false;
+        b->stats_valid = false;
+        c->sync("synth");
+    });
+}
+
+int dopinf_b200_center(dopinf_b200_block* b, double* means) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    return guarded(b->ctx, [&] {
+        if (b->rows > 0) do_center(b, means);
+        b->ctx->sync("center");
+    });
+}
+
+int dopinf_b200_global_scales(dopinf_b200_block* b, double* scales, size_t* degenerate_var) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    return guarded(b->ctx, [&] { do_global_scales(b, scales, degenerate_var); });
+}
+
+int dopinf_b200_scale(dopinf_b200_block* b, const double* scales) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    return guarded(b->ctx, [&] {
+        require(scales != nullptr, "scale: null scales");
+        if (b->rows > 0) do_scale(b, scales);
+        b->ctx->sync("scale");
+    });
+}
+
+int dopinf_b200_local_gram(dopinf_b200_block* b, double* d) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    return guarded(b->ctx, [&] {
+        do_local_gram(b, d);
+        b->ctx->sync("local_gram");
+    });
+}
+
+int dopinf_b200_global_gram(dopinf_b200_ctx* c, double* d) {
+    return guarded(c, [&] {
+        do_global_gram(c, d);
+        c->sync("global_gram");
+    });
+}
+
+int dopinf_b200_project(dopinf_b200_ctx* c, const double* tr, size_t nt, size_t r, double* qhat) {
+    return guarded(c, [&] {
+        require(tr && qhat, "project: null buffers");
+        require(c->have_gram && static_cast<size_t>(c->K) == nt,
+                "project: no Gram of matching size on this context");
+        do_project(c, tr, c->dmat.get<double>(nt * nt, "D"), nt, r, qhat);
+        c->sync("project");
+    });
+}
+
+int dopinf_b200_project_host(dopinf_b200_ctx* c, const double* tr, const double* d, size_t nt, size_t r,
+                             double* qhat) {
+    return guarded(c, [&] {
+        require(tr && d && qhat, "project: null buffers");
+        double* dd = c->dhost_in.get<double>(nt * nt, "D in");
+        ck(cudaMemcpyAsync(dd, d, nt * nt * sizeof(double), cudaMemcpyHostToDevice, c->stream), "D H2D");
+        do_project(c, tr, dd, nt, r, qhat);
+        c->sync("project");
+    });
+}
+
+int dopinf_b200_basis(dopinf_b200_block* b, const double* tr, size_t r, double* phi) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(tr != nullptr && r >= 1, "basis: bad map");
+        materialize(b);
+        const int r_pad = project::basis_cols_pad(static_cast<int>(r));
+        // T_rᵀ, zero padded to r_pad rows, pitch = block pitch.
+        std::vector<double> trt(static_cast<size_t>(r_pad) * b->ld, 0.0);
+        for (size_t k = 0; k < b->nt; ++k)
+            for (size_t j = 0; j < r; ++j) trt[j * b->ld + k] = tr[k * r + j];
+        double* dtrt = c->trt.get<double>(trt.size(), "trt");
+        ck(cudaMemcpyAsync(dtrt, trt.data(), trt.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+           "trt H2D");
+        double* dphi = b->phi.get<double>(std::max<size_t>(b->rows, 1) * r_pad, "phi");
+        b->phi_ld = r_pad;
+        c->record(DOPINF_B200_STAGE_BASIS, 0);
+        if (b->rows > 0) {
+            ck(project::launch_basis(b->q, b->ld, static_cast<long long>(b->rows), static_cast<int>(b->nt),
+                                     dtrt, b->ld, r_pad, dphi, c->num_sms, c->stream),
+               "basis");
+        }
+        c->record(DOPINF_B200_STAGE_BASIS, 1);
+        if (phi && b->rows > 0) {
+            c->record(DOPINF_B200_STAGE_DOWNLOAD, 0);
+            ck(cudaMemcpy2DAsync(phi, r * sizeof(double), dphi, r_pad * sizeof(double), r * sizeof(double),
+                                 b->rows, cudaMemcpyDeviceToHost, c->stream),
+               "phi D2H");
+            c->record(DOPINF_B200_STAGE_DOWNLOAD, 1);
+        }
+        c->sync("basis");  // trt host staging must outlive the copy
+    });
+}
+
+int dopinf_b200_basis_device(dopinf_b200_block* b, double** phi, size_t* ld) {
+    if (!b || !phi || !ld) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    return guarded(b->ctx, [&] {
+        require(b->phi_ld > 0, "basis_device: no basis computed");
+        *phi = static_cast<double*>(b->phi.p);
+        *ld = static_cast<size_t>(b->phi_ld);
+    });
+}
+
+int dopinf_b200_basis_rows(dopinf_b200_block* b, const double* tr, size_t r, const size_t* rows, size_t nsel,
+                           double* out) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(tr != nullptr && r >= 1, "basis_rows: bad map");
+        require(nsel == 0 || (rows && out), "basis_rows: null buffers");
+        std::vector<long long> sel(nsel);
+        for (size_t k = 0; k < nsel; ++k) {
+            if (rows[k] >= b->rows) {
+                fail(DOPINF_B200_ERR_INVALID_ARGUMENT,
+                     "basis_rows: row " + std::to_string(rows[k]) + " outside the local block");
+            }
+            sel[k] = static_cast<long long>(rows[k]);
+        }
+        if (nsel == 0) return;
+        materialize(b);
+        double* dtr = c->tr.get<double>(b->nt * r, "tr");
+        long long* dsel = c->sel.get<long long>(nsel, "sel");
+        double* dout = c->rows_out.get<double>(nsel * r, "rows out");
+        ck(cudaMemcpyAsync(dtr, tr, b->nt * r * sizeof(double), cudaMemcpyHostToDevice, c->stream), "tr H2D");
+        ck(cudaMemcpyAsync(dsel, sel.data(), nsel * sizeof(long long), cudaMemcpyHostToDevice, c->stream),
+           "rows H2D");
+        ck(project::launch_basis_rows(b->q, b->ld, static_cast<int>(b->nt), dtr, static_cast<int>(r), dsel,
+                                      static_cast<int>(nsel), dout, c->stream),
+           "basis_rows");
+        ck(cudaMemcpyAsync(out, dout, nsel * r * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        c->sync("basis_rows");
+    });
+}
+
+int dopinf_b200_snapshot_pass(dopinf_b200_block* b, int scaling, double* means, double* scales, double* d) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        if (b->rows > 0) do_center(b, means);
+        if (scaling) {
+            std::vector<double> s(b->n_vars);
+            do_global_scales(b, s.data(), nullptr);
+            if (scales) std::memcpy(scales, s.data(), s.size() * sizeof(double));
+            if (b->rows > 0) do_scale(b, s.data());
+            c->sync("snapshot_pass");  // host scales must outlive the async upload
+        }
+        do_local_gram(b, nullptr);
+        do_global_gram(c, d);
+        c->sync("snapshot_pass");
+    });
+}
+
+}  // extern "C"

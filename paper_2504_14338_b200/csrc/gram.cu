@@ -1,0 +1,404 @@
+// gram.cu — D = QᵀQ, upper triangle only, on the FP64 tensor pipe (sm_100a).
+//
+// Replaces pod::local_gram → linalg::gram (reference proj/src/pod.cpp:11-13,
+// proj/src/linalg.cpp:50-58), which loops over the FULL square with
+// kernels::axpy. Here:
+//   * Q (rows × K, row-major, pitch ld) is cut into 128-column blocks; only
+//     output tiles (I, J) with I <= J are computed (K(K+1)/2 useful entries).
+//   * The contraction dimension (rows) is split into S equal chunks; a work
+//     item is (split s, tile). Items are handed out s-major from a global
+//     atomic queue, so the CTAs running at any moment read the same rows of
+//     Q (L2 reuse across the ~tiles CTAs that need them).
+//   * Each persistent CTA = 1 TMA producer warp + 16 consumer warps. The
+//     producer streams BK×128 row-slabs of the I and J column blocks through a
+//     6-stage mbarrier ring (cp.async.bulk.tensor, OOB rows/cols zero-filled);
+//     consumers run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) on 32×32 warp tiles
+//     with fragments read as conflict-free 128-bit shared loads.
+//   * Diagonal tiles skip warp tiles / mma tiles strictly below the diagonal
+//     and edge tiles skip columns >= K; the remaining warp tiles are balanced
+//     over the 4 SM sub-partitions on the host (LPT).
+//   * Each item's partial goes to a workspace in fragment order; a second
+//     kernel sums the S partials of every tile in split order s = 0..S-1 —
+//     fixed order, no atomics on data, bitwise reproducible — and writes the
+//     packed upper triangle. A third kernel expands it to the symmetric K×K
+//     D (bitwise symmetric, as linalg.hpp:17 promises for the reference).
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "gram.h"
+
+namespace dopinf_b200 {
+namespace gram {
+
+namespace {
+
+constexpr int BT = kTileEdge;         // 128 columns per block
+constexpr int BK = kRowsPerStage;     // 16 rows per stage
+constexpr int STAGES = 6;
+constexpr int CONSUMERS = kConsumerWarps;  // 16
+constexpr int THREADS = (CONSUMERS + 1) * kWarp;
+constexpr int FLAG_FIRST = 1, FLAG_LAST = 2, FLAG_DONE = 4;
+
+struct __align__(128) Smem {
+    double a[STAGES][BK * BT];
+    double b[STAGES][BK * BT];
+    uint64_t full[STAGES];
+    uint64_t empty[STAGES];
+    int meta_item[STAGES];
+    int meta_flags[STAGES];
+};
+
+// Warp-tile entry: wm | wn << 2 | diag << 4 | mma mask << 16 (0 mask = idle).
+__device__ __forceinline__ void decode(uint32_t e, int& wm, int& wn, bool& diag, uint32_t& mask) {
+    wm = e & 3;
+    wn = (e >> 2) & 3;
+    diag = (e >> 4) & 1;
+    mask = e >> 16;
+}
+
+template <bool kFull>
+__device__ __forceinline__ void stage_mma(double (&acc)[16][2], const double* __restrict__ as,
+                                          const double* __restrict__ bs, uint32_t mask) {
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+        const double2 a0 = lds128(as + ks * 4 * BT);
+        const double2 a1 = lds128(as + ks * 4 * BT + 16);
+        const double2 b0 = lds128(bs + ks * 4 * BT);
+        const double2 b1 = lds128(bs + ks * 4 * BT + 16);
+        const double a[4] = {a0.x, a0.y, a1.x, a1.y};
+        const double b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                if (kFull || ((mask >> (mi * 4 + ni)) & 1u)) {
+                    dmma_8x8x4(acc[mi * 4 + ni][0], acc[mi * 4 + ni][1], a[mi], b[ni]);
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gram_dmma_kernel(const __grid_constant__ CUtensorMap tmap, const TileInfo* __restrict__ tiles,
+                     int n_tiles, int n_items, long long n_rows, int chunk_rows,
+                     double* __restrict__ work, int* __restrict__ counters) {
+    extern __shared__ unsigned char smem_raw[];
+    Smem& s = *reinterpret_cast<Smem*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~static_cast<uintptr_t>(127));
+    const int warp = threadIdx.x / kWarp;
+    const int lane = threadIdx.x % kWarp;
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < STAGES; ++st) {
+            mbar_init(&s.full[st], 1);
+            mbar_init(&s.empty[st], CONSUMERS);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == CONSUMERS) {
+        // ---------------- TMA producer (one lane) ----------------
+        if (lane == 0) {
+            tma_prefetch_desc(&tmap);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (;;) {
+                const int item = atomicAdd(&counters[0], 1);
+                if (item >= n_items) {
+                    mbar_wait(&s.empty[stage], phase ^ 1u);
+                    s.meta_flags[stage] = FLAG_DONE;
+                    mbar_arrive(&s.full[stage]);
+                    break;
+                }
+                const int tile = item % n_tiles;
+                const int split = item / n_tiles;
+                const int I = tiles[tile].I, J = tiles[tile].J;
+                const long long row0 = static_cast<long long>(split) * chunk_rows;
+                const long long rows = min(static_cast<long long>(chunk_rows), n_rows - row0);
+                const int nkb = static_cast<int>((rows + BK - 1) / BK);
+                const bool diag = (I == J);
+                const uint32_t bytes = (diag ? 1u : 2u) * BK * BT * sizeof(double);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&s.empty[stage], phase ^ 1u);
+                    s.meta_item[stage] = item;
+                    s.meta_flags[stage] = (kb == 0 ? FLAG_FIRST : 0) | (kb == nkb - 1 ? FLAG_LAST : 0);
+                    mbar_arrive_expect_tx(&s.full[stage], bytes);
+                    const int y = static_cast<int>(row0 + static_cast<long long>(kb) * BK);
+                    tma_load_2d(s.a[stage], &tmap, I * BT, y, &s.full[stage]);
+                    if (!diag) tma_load_2d(s.b[stage], &tmap, J * BT, y, &s.full[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else {
+        // ---------------- DMMA consumers ----------------
+        const int g = lane >> 2, t = lane & 3;
+        double acc[16][2];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+        int wm = 0, wn = 0;
+        bool diag = false;
+        uint32_t mask = 0;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (;;) {
+            mbar_wait(&s.full[stage], phase);
+            const int flags = s.meta_flags[stage];
+            if (flags & FLAG_DONE) break;
+            const int item = s.meta_item[stage];
+            if (flags & FLAG_FIRST) decode(tiles[item % n_tiles].warp[warp], wm, wn, diag, mask);
+            if (mask) {
+                const double* as = s.a[stage] + t * BT + wm * 32 + 2 * g;
+                const double* bs = (diag ? s.a[stage] : s.b[stage]) + t * BT + wn * 32 + 2 * g;
+                if (mask == 0xFFFFu) {
+                    stage_mma<true>(acc, as, bs, mask);
+                } else {
+                    stage_mma<false>(acc, as, bs, mask);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.empty[stage]);
+            if ((flags & FLAG_LAST) && mask) {
+                double* w = work + (static_cast<size_t>(item) * CONSUMERS + warp) * kWarpFragDoubles +
+                            lane * 2;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    if ((mask >> i) & 1u) __stcg(reinterpret_cast<double2*>(w + i * 64),
+                                                 make_double2(acc[i][0], acc[i][1]));
+                    acc[i][0] = acc[i][1] = 0.0;
+                }
+            }
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+    }
+
+    // Self-resetting queue: the last CTA out zeroes the counters for the next launch.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int prev = atomicAdd(&counters[1], 1);
+        if (prev == static_cast<int>(gridDim.x) - 1) {
+            counters[0] = 0;
+            counters[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
+// Fixed-order split-n reduction: block = (tile, warp slot), thread = (mma, lane).
+__global__ void __launch_bounds__(512)
+    gram_reduce_kernel(const TileInfo* __restrict__ tiles, int n_tiles, int n_splits, int K,
+                       const double* __restrict__ work, double* __restrict__ packed) {
+    const int tile = blockIdx.x / CONSUMERS;
+    const int slot = blockIdx.x % CONSUMERS;
+    int wm, wn;
+    bool diag;
+    uint32_t mask;
+    decode(tiles[tile].warp[slot], wm, wn, diag, mask);
+    const int mma = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    if (!((mask >> mma) & 1u)) return;
+    const double* w = work + static_cast<size_t>(slot) * kWarpFragDoubles + mma * 64 + lane * 2;
+    const size_t item_stride = static_cast<size_t>(n_tiles) * CONSUMERS * kWarpFragDoubles;
+    const double* p = w + static_cast<size_t>(tile) * CONSUMERS * kWarpFragDoubles;
+    double2 sum = __ldcg(reinterpret_cast<const double2*>(p));
+    for (int sp = 1; sp < n_splits; ++sp) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(p + sp * item_stride));
+        sum.x += v.x;
+        sum.y += v.y;
+    }
+    const int g = lane >> 2, t = lane & 3;
+    const int mi = mma >> 2, ni = mma & 3;
+    const int row = tiles[tile].I * BT + wm * 32 + (mi >> 1) * 16 + 2 * g + (mi & 1);
+    const double vals[2] = {sum.x, sum.y};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int n = 2 * t + c;
+        const int col = tiles[tile].J * BT + wn * 32 + (ni >> 1) * 16 + 2 * n + (ni & 1);
+        if (row < K && col < K && row <= col) {
+            const size_t idx = static_cast<size_t>(row) * (2 * static_cast<size_t>(K) - row + 1) / 2 +
+                               (col - row);
+            packed[idx] = vals[c];
+        }
+    }
+}
+
+// packed upper triangle (row-major) -> full symmetric K×K, row-major, pitch K.
+__global__ void unpack_kernel(const double* __restrict__ packed, int K, double* __restrict__ d) {
+    const size_t total = static_cast<size_t>(K) * K;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t i = e / K, j = e % K;
+        const size_t r = i < j ? i : j, c = i < j ? j : i;
+        d[e] = packed[r * (2 * static_cast<size_t>(K) - r + 1) / 2 + (c - r)];
+    }
+}
+
+// Ascending-rank sum of p packed triangles (comm_inprocess.cpp:101-112 order).
+__global__ void ordered_sum_kernel(const double* __restrict__ parts, int p, size_t count,
+                                   double* __restrict__ out) {
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < count;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        double acc = parts[e];
+        for (int r = 1; r < p; ++r) acc += parts[static_cast<size_t>(r) * count + e];
+        out[e] = acc;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) {
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        }
+    }
+    return fn;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Host planning.
+
+std::vector<TileInfo> plan_tiles(int K) {
+    const int nb = (K + BT - 1) / BT;
+    std::vector<TileInfo> out;
+    for (int I = 0; I < nb; ++I) {
+        for (int J = I; J < nb; ++J) {
+            TileInfo ti{};
+            ti.I = I;
+            ti.J = J;
+            struct Entry {
+                int wm, wn, cost;
+                uint32_t mask;
+            };
+            std::vector<Entry> entries;
+            for (int wm = 0; wm < 4; ++wm) {
+                for (int wn = 0; wn < 4; ++wn) {
+                    uint32_t mask = 0;
+                    for (int mi = 0; mi < 4; ++mi) {
+                        for (int ni = 0; ni < 4; ++ni) {
+                            const int rmin = I * BT + wm * 32 + (mi >> 1) * 16 + (mi & 1);
+                            const int cmin = J * BT + wn * 32 + (ni >> 1) * 16 + (ni & 1);
+                            bool need = rmin < K && cmin < K;
+                            if (I == J) need = need && rmin <= cmin + 14;
+                            if (need) mask |= 1u << (mi * 4 + ni);
+                        }
+                    }
+                    if (mask) entries.push_back({wm, wn, __builtin_popcount(mask), mask});
+                }
+            }
+            // LPT over the 4 SM sub-partitions (warp w runs on SMSP w % 4).
+            std::stable_sort(entries.begin(), entries.end(),
+                             [](const Entry& a, const Entry& b) { return a.cost > b.cost; });
+            int load[4] = {0, 0, 0, 0}, used[4] = {0, 0, 0, 0};
+            for (const Entry& e : entries) {
+                int q = -1;
+                for (int c = 0; c < 4; ++c) {
+                    if (used[c] < 4 && (q < 0 || load[c] < load[q])) q = c;
+                }
+                const int w = q + 4 * used[q];
+                ++used[q];
+                load[q] += e.cost;
+                ti.warp[w] = static_cast<uint32_t>(e.wm) | (static_cast<uint32_t>(e.wn) << 2) |
+                             (static_cast<uint32_t>(I == J) << 4) | (e.mask << 16);
+            }
+            out.push_back(ti);
+        }
+    }
+    return out;
+}
+
+Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes) {
+    Plan p;
+    p.K = K;
+    p.n_rows = n_rows;
+    p.n_tiles = static_cast<int>(plan_tiles(K).size());
+    const long long target_items = static_cast<long long>(num_sms) * kItemsPerCta;
+    long long S = (target_items + p.n_tiles - 1) / p.n_tiles;
+    // Keep the fixed-order reduction cheap relative to the contraction.
+    S = std::min<long long>(S, std::max<long long>(1, n_rows / kMinRowsPerSplit));
+    const long long per_item = static_cast<long long>(kItemDoubles) * sizeof(double);
+    S = std::min<long long>(
+        S, std::max<long long>(1, static_cast<long long>(workspace_cap_bytes) / (per_item * p.n_tiles)));
+    S = std::max<long long>(1, S);
+    long long chunk = (n_rows + S - 1) / S;
+    chunk = std::max<long long>(BK, (chunk + BK - 1) / BK * BK);
+    S = std::max<long long>(1, (n_rows + chunk - 1) / chunk);
+    p.n_splits = static_cast<int>(S);
+    p.chunk_rows = static_cast<int>(chunk);
+    p.n_items = p.n_splits * p.n_tiles;
+    p.grid = std::min(num_sms, p.n_items);
+    p.workspace_doubles = static_cast<size_t>(p.n_items) * kItemDoubles;
+    return p;
+}
+
+cudaError_t make_tensor_map(CUtensorMap* map, const double* q, long long n_rows, int K, size_t ld) {
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(n_rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * sizeof(double))};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(BT), static_cast<cuuint32_t>(BK)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(q), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+size_t smem_bytes() { return sizeof(Smem) + 128; }
+
+cudaError_t launch_gram(const Plan& plan, const CUtensorMap& map, const TileInfo* d_tiles,
+                        double* work, int* counters, cudaStream_t stream) {
+    const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(gram_dmma_kernel),
+                                             static_cast<int>(smem_bytes()));
+    if (e != cudaSuccess) return e;
+    gram_dmma_kernel<<<plan.grid, THREADS, smem_bytes(), stream>>>(
+        map, d_tiles, plan.n_tiles, plan.n_items, plan.n_rows, plan.chunk_rows, work, counters);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(const Plan& plan, const TileInfo* d_tiles, const double* work,
+                          double* packed, cudaStream_t stream) {
+    gram_reduce_kernel<<<plan.n_tiles * CONSUMERS, 512, 0, stream>>>(d_tiles, plan.n_tiles,
+                                                                      plan.n_splits, plan.K, work,
+                                                                      packed);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const double* packed, int K, double* d, cudaStream_t stream) {
+    const size_t total = static_cast<size_t>(K) * K;
+    const int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16));
+    unpack_kernel<<<std::max(grid, 1), 256, 0, stream>>>(packed, K, d);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ordered_sum(const double* parts, int p, size_t count, double* out,
+                               cudaStream_t stream) {
+    const int grid = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 16));
+    ordered_sum_kernel<<<std::max(grid, 1), 256, 0, stream>>>(parts, p, count, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace gram
+}  // namespace dopinf_b200

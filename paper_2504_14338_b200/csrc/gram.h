@@ -1,0 +1,53 @@
+// gram.h — host interface of the DMMA Gram kernels (gram.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <vector>
+
+namespace dopinf_b200 {
+namespace gram {
+
+constexpr int kTileEdge = 128;       // columns of Q per block (CTA output tile edge)
+constexpr int kRowsPerStage = 16;    // rows of Q per TMA stage
+constexpr int kConsumerWarps = 16;   // 4×4 grid of 32×32 warp tiles
+constexpr int kWarpFragDoubles = 16 * 32 * 2;                   // 16 mma × 32 lanes × 2
+constexpr int kItemDoubles = kConsumerWarps * kWarpFragDoubles;  // 16384 (128 KiB)
+constexpr int kItemsPerCta = 16;     // queue granularity target (tail vs workspace)
+constexpr long long kMinRowsPerSplit = 768;
+
+struct TileInfo {
+    int I, J;
+    uint32_t warp[kConsumerWarps];  // wm | wn<<2 | diag<<4 | mma-mask<<16
+};
+
+struct Plan {
+    int K = 0;
+    long long n_rows = 0;
+    int n_tiles = 0;
+    int n_splits = 0;
+    int chunk_rows = 0;
+    int n_items = 0;
+    int grid = 0;
+    size_t workspace_doubles = 0;
+};
+
+std::vector<TileInfo> plan_tiles(int K);
+Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes);
+cudaError_t make_tensor_map(CUtensorMap* map, const double* q, long long n_rows, int K, size_t ld);
+size_t smem_bytes();
+cudaError_t launch_gram(const Plan& plan, const CUtensorMap& map, const TileInfo* d_tiles,
+                        double* work, int* counters, cudaStream_t stream);
+cudaError_t launch_reduce(const Plan& plan, const TileInfo* d_tiles, const double* work,
+                          double* packed, cudaStream_t stream);
+cudaError_t launch_unpack(const double* packed, int K, double* d, cudaStream_t stream);
+cudaError_t launch_ordered_sum(const double* parts, int p, size_t count, double* out,
+                               cudaStream_t stream);
+
+inline size_t packed_count(int K) { return static_cast<size_t>(K) * (K + 1) / 2; }
+
+}  // namespace gram
+}  // namespace dopinf_b200

@@ -1,0 +1,284 @@
+// project.cu — the products after the Gram (reference pod.cpp, postprocess.cpp).
+//
+//  * project_kernel: Q̂ = T_rᵀ D (pod::project → linalg::matmul_tn,
+//    pod.cpp:103-105, linalg.cpp:28-37). Each output is the reference's FMA
+//    chain over l = 0..K−1 in order (c[i][j] = fma(T_r[l][i], D[l][j], c)), so
+//    Q̂ is bit-identical to the reference's for the same T_r and D.
+//  * basis_rows_kernel: postprocess::basis_rows (postprocess.cpp:12-34), the
+//    reference's unfused acc + q·tr loop in order → bit-identical.
+//  * basis_dmma_kernel: Φ_r = Q·T_r (postprocess.cpp:66 reconstruct_field's
+//    linalg::matmul), a tall-skinny GEMM on the FP64 tensor pipe. Q row-slabs
+//    (128 rows × 16 snapshots) and the matching slab of T_rᵀ stream through a
+//    TMA ring with 128-byte swizzle; consumers read both operands with
+//    conflict-free 128-bit shared loads (two k-steps per load) and run
+//    DMMA.8x8x4. Q is read from HBM exactly once for r <= 128.
+#include <algorithm>
+
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "project.h"
+
+namespace dopinf_b200 {
+namespace project {
+
+namespace {
+
+constexpr int kProjRowsPerThread = 8;
+
+__global__ void __launch_bounds__(128)
+    project_kernel(const double* __restrict__ tr, const double* __restrict__ d, int K, int r,
+                   double* __restrict__ qhat) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i0 = blockIdx.y * kProjRowsPerThread;
+    if (j >= K) return;
+    double acc[kProjRowsPerThread];
+#pragma unroll
+    for (int ii = 0; ii < kProjRowsPerThread; ++ii) acc[ii] = 0.0;
+    const int ni = min(kProjRowsPerThread, r - i0);
+    if (ni == kProjRowsPerThread) {
+        for (int l = 0; l < K; ++l) {
+            const double dv = __ldg(d + static_cast<size_t>(l) * K + j);
+            const double* trl = tr + static_cast<size_t>(l) * r + i0;
+#pragma unroll
+            for (int ii = 0; ii < kProjRowsPerThread; ++ii) acc[ii] = fma(__ldg(trl + ii), dv, acc[ii]);
+        }
+    } else {
+        for (int l = 0; l < K; ++l) {
+            const double dv = __ldg(d + static_cast<size_t>(l) * K + j);
+            const double* trl = tr + static_cast<size_t>(l) * r + i0;
+#pragma unroll
+            for (int ii = 0; ii < kProjRowsPerThread; ++ii) {
+                if (ii < ni) acc[ii] = fma(__ldg(trl + ii), dv, acc[ii]);
+            }
+        }
+    }
+#pragma unroll
+    for (int ii = 0; ii < kProjRowsPerThread; ++ii) {
+        if (ii < ni) qhat[static_cast<size_t>(i0 + ii) * K + j] = acc[ii];
+    }
+}
+
+__global__ void basis_rows_kernel(const double* __restrict__ q, size_t ld, int K,
+                                  const double* __restrict__ tr, int r,
+                                  const long long* __restrict__ rows, int nsel,
+                                  double* __restrict__ out) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= static_cast<long long>(nsel) * r) return;
+    const int k = static_cast<int>(e / r), jj = static_cast<int>(e % r);
+    const double* qr = q + static_cast<size_t>(rows[k]) * ld;
+    double acc = 0.0;
+    for (int t = 0; t < K; ++t) acc = __dadd_rn(acc, __dmul_rn(qr[t], tr[static_cast<size_t>(t) * r + jj]));
+    out[e] = acc;
+}
+
+// ---- Φ_r = Q · T_r on DMMA ---------------------------------------------------
+constexpr int BM = 128;     // rows of Q per CTA tile
+constexpr int BKB = 16;     // snapshots per stage (128 B rows → 128B swizzle)
+constexpr int STAGES = 6;
+constexpr int CONSUMERS = 8;  // 4 (m) × 2 (n) warps; warp tile 32 × 8·NT
+constexpr int THREADS = (CONSUMERS + 1) * 32;
+
+template <int NT>
+struct __align__(1024) BasisSmem {
+    double a[STAGES][BM * BKB];            // 16 KiB per stage
+    double b[STAGES][16 * NT * BKB];       // T_rᵀ slab, BN = 16·NT rows
+    uint64_t full[STAGES];
+    uint64_t empty[STAGES];
+};
+
+// (row, chunk) of a [rows][16 doubles] tile written by TMA with 128B swizzle.
+__device__ __forceinline__ const double* swz(const double* base, int row, int chunk) {
+    return base + row * BKB + ((chunk ^ (row & 7)) << 1);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(THREADS, 1)
+    basis_dmma_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap tmap,
+                      long long rows, int K, double* __restrict__ phi, int ldp) {
+    extern __shared__ unsigned char smem_raw[];
+    BasisSmem<NT>& s = *reinterpret_cast<BasisSmem<NT>*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    constexpr int BN = 16 * NT;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const long long n_rb = (rows + BM - 1) / BM;
+    const int nkb = (K + BKB - 1) / BKB;
+    const int col0 = blockIdx.y * BN;
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < STAGES; ++st) {
+            mbar_init(&s.full[st], 1);
+            mbar_init(&s.empty[st], CONSUMERS);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == CONSUMERS) {
+        if (lane == 0) {
+            tma_prefetch_desc(&qmap);
+            tma_prefetch_desc(&tmap);
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t bytes = (BM + BN) * BKB * sizeof(double);
+            for (long long rb = blockIdx.x; rb < n_rb; rb += gridDim.x) {
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&s.empty[stage], phase ^ 1u);
+                    mbar_arrive_expect_tx(&s.full[stage], bytes);
+                    tma_load_2d(s.a[stage], &qmap, kb * BKB, static_cast<int>(rb * BM), &s.full[stage]);
+                    tma_load_2d(s.b[stage], &tmap, kb * BKB, col0, &s.full[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else {
+        const int g = lane >> 2, t = lane & 3;
+        const int wm = warp & 3, wn = warp >> 2;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (long long rb = blockIdx.x; rb < n_rb; rb += gridDim.x) {
+            double acc[4][NT][2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(&s.full[stage], phase);
+                const double* as = s.a[stage];
+                const double* bs = s.b[stage];
+#pragma unroll
+                for (int kh = 0; kh < 2; ++kh) {
+                    const int chunk = kh * 4 + t;
+                    double2 a[4], b[NT];
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) a[mi] = lds128(swz(as, wm * 32 + mi * 8 + g, chunk));
+#pragma unroll
+                    for (int ni = 0; ni < NT; ++ni) b[ni] = lds128(swz(bs, wn * 8 * NT + ni * 8 + g, chunk));
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) {
+#pragma unroll
+                        for (int ni = 0; ni < NT; ++ni) {
+                            dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
+                            dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.empty[stage]);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+                const long long row = rb * BM + wm * 32 + mi * 8 + g;
+                if (row < rows) {
+                    double* dst = phi + static_cast<size_t>(row) * ldp + col0 + wn * 8 * NT + 2 * t;
+#pragma unroll
+                    for (int ni = 0; ni < NT; ++ni) {
+                        __stcs(reinterpret_cast<double2*>(dst + ni * 8),
+                               make_double2(acc[mi][ni][0], acc[mi][ni][1]));
+                    }
+                }
+            }
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) {
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        }
+    }
+    return fn;
+}
+
+cudaError_t map_2d(CUtensorMap* map, const double* base, long long rows, int cols, size_t ld,
+                   int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * sizeof(double))};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(BKB), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int NT>
+cudaError_t launch_basis_nt(const double* q, size_t ld, long long rows, int K, const double* trt,
+                            size_t ldt, int col_blocks, double* phi, int ldp, int num_sms,
+                            cudaStream_t stream) {
+    CUtensorMap qmap, tmap;
+    cudaError_t e = map_2d(&qmap, q, rows, K, ld, BM);
+    if (e != cudaSuccess) return e;
+    e = map_2d(&tmap, trt, static_cast<long long>(col_blocks) * 16 * NT, K, ldt, 16 * NT);
+    if (e != cudaSuccess) return e;
+    const size_t smem = sizeof(BasisSmem<NT>) + 1024;
+    e = set_smem_attr_once(reinterpret_cast<const void*>(basis_dmma_kernel<NT>), static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const long long n_rb = (rows + BM - 1) / BM;
+    const int gx = static_cast<int>(std::max<long long>(
+        1, std::min<long long>(n_rb, std::max(1, num_sms / col_blocks))));
+    basis_dmma_kernel<NT><<<dim3(gx, col_blocks), THREADS, smem, stream>>>(qmap, tmap, rows, K, phi, ldp);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int basis_cols_pad(int r) {
+    if (r <= 128) return std::max(16, (r + 15) / 16 * 16);
+    return (r + 127) / 128 * 128;
+}
+
+cudaError_t launch_project(const double* tr, const double* d, int K, int r, double* qhat,
+                           cudaStream_t stream) {
+    dim3 grid((K + 127) / 128, (r + kProjRowsPerThread - 1) / kProjRowsPerThread);
+    project_kernel<<<grid, 128, 0, stream>>>(tr, d, K, r, qhat);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_basis_rows(const double* q, size_t ld, int K, const double* tr, int r,
+                              const long long* rows, int nsel, double* out, cudaStream_t stream) {
+    const long long total = static_cast<long long>(nsel) * r;
+    if (total == 0) return cudaSuccess;
+    basis_rows_kernel<<<static_cast<int>((total + 127) / 128), 128, 0, stream>>>(q, ld, K, tr, r,
+                                                                                rows, nsel, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_basis(const double* q, size_t ld, long long rows, int K, const double* trt,
+                         size_t ldt, int r_pad, double* phi, int num_sms, cudaStream_t stream) {
+    if (r_pad > 128) {
+        return launch_basis_nt<8>(q, ld, rows, K, trt, ldt, r_pad / 128, phi, r_pad, num_sms, stream);
+    }
+    switch (r_pad / 16) {
+        case 1: return launch_basis_nt<1>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
+        case 2: return launch_basis_nt<2>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
+        case 3: return launch_basis_nt<3>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
+        case 4: return launch_basis_nt<4>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
+        case 5: return launch_basis_nt<5>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
+        case 6: return launch_basis_nt<6>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
+        case 7: return launch_basis_nt<7>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
+        default: return launch_basis_nt<8>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
+    }
+}
+
+}  // namespace project
+}  // namespace dopinf_b200

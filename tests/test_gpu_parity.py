@@ -1,0 +1,228 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same input bytes. Tolerances are the north-star's (BASELINE.json): Gram
+relative Frobenius <= 1e-12, Q̂/Φ_r <= 1e-9; transform, projection and
+basis_rows are expected (and asserted) bit-identical to the reference order.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_frob
+
+pytestmark = pytest.mark.gpu
+
+GRAM_TOL = 1e-12   # north_star: Gram relative Frobenius error
+BASIS_TOL = 1e-9   # north_star: Φ_r / Q̂ after sign normalisation
+
+
+def api():
+    from paper_2504_14338_b200 import api as a
+
+    return a
+
+
+def make_block(ctx, q, n_vars=1):
+    a = api()
+    rows, nt = q.shape
+    nx = rows // n_vars
+    return a.LocalBlock(ctx, n_vars, a.RowRange(0, nx), nt, values=q)
+
+
+# ---- Step II transform: bit-identical to transform.cpp -----------------------------
+@pytest.mark.parametrize("n_vars,nx,nt", [(1, 20, 7), (2, 15, 11), (2, 12, 9), (3, 33, 64), (4, 257, 130),
+                                          (2, 1000, 601), (1, 5, 1), (1, 3, 2), (2, 64, 4)])
+def test_transform_bitwise(ctx, oracle, n_vars, nx, nt):
+    a = api()
+    rng = np.random.default_rng(nx * 31 + nt)
+    q = rng.standard_normal((n_vars * nx, nt)) * rng.uniform(0.1, 1e3) + rng.uniform(-5, 5)
+    block = make_block(ctx, q, n_vars)
+    header = a.SnapshotHeader(n_vars, nx, nt)
+    means = a.center_in_place(block)
+    oq, om = oracle.center(q)
+    assert np.array_equal(means, om)
+    assert np.array_equal(block.values, oq)  # centering alone, materialised
+    if nt == 1:  # one snapshot: every centered row is 0 -> the reference throws
+        with pytest.raises(a.DegenerateVariableError, match="var0"):
+            a.compute_global_scales(block, header, ctx)
+        return
+    scales = a.compute_global_scales(block, header, ctx)
+    os_, bad = oracle.reduce_scales(oracle.local_maxabs(oq, n_vars, nx)[None, :])
+    assert bad == -1 and np.array_equal(scales, os_)
+    a.scale_in_place(block, scales)
+    assert np.array_equal(block.values, oracle.scale(oq, n_vars, nx, os_))
+
+
+def test_transform_fused_pass_matches_separate_passes(ctx, oracle):
+    # center -> scales -> scale without an intermediate download (the fused apply pass)
+    a = api()
+    rng = np.random.default_rng(5)
+    q = rng.standard_normal((2 * 300, 77)) * 3 + 1
+    block = make_block(ctx, q, 2)
+    a.center_in_place(block)
+    s = a.compute_global_scales(block, a.SnapshotHeader(2, 300, 77))
+    a.scale_in_place(block, s)
+    oq, _ = oracle.center(q)
+    assert np.array_equal(block.values, oracle.scale(oq, 2, 300, oracle.local_maxabs(oq, 2, 300)))
+
+
+def test_known_answers(ctx):
+    # test_transform.cpp:40-50, 87-96
+    a = api()
+    b = make_block(ctx, np.array([[1.0, 3.0], [2.0, 2.0]]), 1)
+    assert list(a.center_in_place(b)) == [2.0, 2.0]
+    assert np.array_equal(b.values, [[-1.0, 1.0], [0.0, 0.0]])
+    b = make_block(ctx, np.array([[-4.0, 2.0, 1.0]]), 1)
+    s = a.compute_global_scales(b, a.SnapshotHeader(1, 1, 3))
+    assert list(s) == [4.0]
+    a.scale_in_place(b, s)
+    assert np.array_equal(b.values, [[-1.0, 0.5, 0.25]])
+
+
+def test_degenerate_variable_names_it(ctx):
+    # test_transform.cpp:115-128
+    a = api()
+    b = make_block(ctx, np.array([[4.0, 4, 4], [1, 2, 3]]), 2)
+    a.center_in_place(b)
+    with pytest.raises(a.DegenerateVariableError, match="var0"):
+        a.compute_global_scales(b, a.SnapshotHeader(2, 1, 3))
+
+
+def test_scaled_bound_attained(ctx):
+    # test_transform.cpp:98-113
+    a = api()
+    rng = np.random.default_rng(8)
+    b = make_block(ctx, rng.standard_normal((30, 11)), 2)
+    a.center_in_place(b)
+    a.scale_in_place(b, a.compute_global_scales(b, a.SnapshotHeader(2, 15, 11)))
+    v = b.values
+    assert np.all(np.abs(v) <= 1.0) and np.max(np.abs(v)) == 1.0
+
+
+# ---- Step III Gram ---------------------------------------------------------------------
+GRAM_SHAPES = [(20, 6), (13, 7), (57, 23), (500, 50), (33, 20), (100, 12), (450, 48), (77, 31), (9, 9),
+               (1, 1), (3, 5), (2000, 127), (2000, 128), (2000, 129), (1500, 255), (700, 256), (4000, 300),
+               (6000, 600), (12345, 200), (32, 1)]
+
+
+@pytest.mark.parametrize("m,k", GRAM_SHAPES)
+def test_gram_matches_oracle(ctx, oracle, m, k):
+    a = api()
+    rng = np.random.default_rng(m * 1000 + k)
+    q = rng.standard_normal((m, k))
+    b = make_block(ctx, q)
+    d = a.local_gram(b)
+    ref = oracle.gram(q)
+    assert rel_frob(d, ref) <= GRAM_TOL
+    assert np.array_equal(d, d.T)  # bitwise symmetric (linalg.hpp:17)
+    d2 = a.global_gram(d, ctx)
+    assert np.array_equal(d, d2)   # one rank: the reduction is the identity
+    assert np.array_equal(a.local_gram(b), d)  # deterministic split-n order
+
+
+def test_gram_rank_deficient(ctx, oracle):
+    # acceptance.cpp:207-221 rank-deficient shapes: q = A (m×r) B (r×nt)
+    a = api()
+    for i, (m, nt, r) in enumerate([(500, 50, 5), (300, 30, 3), (120, 40, 10), (64, 16, 1)]):
+        rng = oracle.rng(1012 + i)
+        q = oracle.matmul(rng.matrix(m, r), rng.matrix(r, nt))
+        d = a.local_gram(make_block(ctx, q))
+        assert rel_frob(d, oracle.gram(q)) <= GRAM_TOL
+
+
+def test_gram_empty_block(ctx):
+    a = api()
+    b = a.LocalBlock(ctx, 2, a.RowRange(0, 0), 9)
+    assert np.array_equal(a.local_gram(b), np.zeros((9, 9)))
+
+
+def test_gram_multi_var_and_scaled(ctx, oracle):
+    a = api()
+    rng = np.random.default_rng(17)
+    nv, nx, nt = 4, 777, 96
+    q = rng.standard_normal((nv * nx, nt)) * np.repeat([1e-2, 1.0, 1e3, 1e5], nx)[:, None]
+    b = make_block(ctx, q, nv)
+    params, d = a.snapshot_pass(b, scaling=True)
+    oq, om = oracle.center(q)
+    os_, _ = oracle.reduce_scales(oracle.local_maxabs(oq, nv, nx)[None, :])
+    oq = oracle.scale(oq, nv, nx, os_)
+    assert np.array_equal(params.local_means, om) and np.array_equal(params.scales, os_)
+    assert np.array_equal(b.values, oq)
+    assert rel_frob(d, oracle.gram(oq)) <= GRAM_TOL
+
+
+# ---- projection / basis ---------------------------------------------------------------------
+@pytest.mark.parametrize("nt,r", [(6, 3), (50, 10), (128, 40), (600, 10), (257, 80)])
+def test_project_bitwise(ctx, oracle, nt, r):
+    a = api()
+    rng = np.random.default_rng(nt + r)
+    q = rng.standard_normal((3 * nt, nt))
+    d = oracle.gram(q)
+    tr = rng.standard_normal((nt, r))
+    assert np.array_equal(a.project(tr, d, ctx), oracle.project(tr, d))
+
+
+def test_project_resident_uses_device_gram(ctx, oracle):
+    a = api()
+    rng = np.random.default_rng(3)
+    q = rng.standard_normal((400, 40))
+    b = make_block(ctx, q)
+    d = a.global_gram(a.local_gram(b), ctx)
+    tr = rng.standard_normal((40, 7))
+    assert np.array_equal(a.project_resident(ctx, tr), oracle.project(tr, d))
+
+
+@pytest.mark.parametrize("rows,nt,r", [(24, 8, 5), (1000, 64, 10), (5000, 300, 20), (3000, 257, 40),
+                                       (2048, 1200, 80), (130, 17, 3), (777, 33, 130)])
+def test_basis_matches_oracle(ctx, oracle, rows, nt, r):
+    a = api()
+    rng = np.random.default_rng(rows + nt + r)
+    q = rng.standard_normal((rows, nt))
+    tr = rng.standard_normal((nt, r)) / np.sqrt(nt)
+    b = make_block(ctx, q)
+    phi = a.basis(b, tr)
+    ref = oracle.matmul(q, tr)
+    assert rel_frob(phi, ref) <= 1e-13
+    assert np.max(np.abs(phi - ref)) <= BASIS_TOL * np.max(np.abs(ref))
+    sel = rng.integers(0, rows, size=min(rows, 17))
+    assert np.array_equal(a.basis_rows(b, tr, sel), oracle.basis_rows(q, tr, sel))
+
+
+def test_basis_rows_rejects_bad_rows(ctx):
+    # test_postprocess.cpp:58-65
+    a = api()
+    b = make_block(ctx, np.array([[1.0, 0], [0, 1], [1, 1], [2, 2]]))
+    with pytest.raises(a.InvalidArgumentError):
+        a.basis_rows(b, np.zeros((3, 2)), [0])
+    with pytest.raises(a.InvalidArgumentError):
+        a.basis_rows(b, np.zeros((2, 2)), [4])
+
+
+def test_partition_rows_known_answers():
+    # test_data.cpp:19-47
+    a = api()
+    assert [(x.begin, x.end) for x in a.partition_rows(10, 3)] == [(0, 3), (3, 6), (6, 10)]
+    big = a.partition_rows(146339, 4)
+    assert [x.count() for x in big] == [36584, 36584, 36584, 36587]
+    for bad in (0, -1):
+        with pytest.raises(a.PartitionError):
+            a.partition_rows(10, bad)
+    with pytest.raises(a.PartitionError):
+        a.partition_rows(3, 4)
+
+
+# ---- device generator + config-1 sized end to end ---------------------------------------------------
+def test_config1_pass_against_oracle(ctx, oracle):
+    """BASELINE config 1 shape: 2 vars × 16,384 points, K = 600, scaling on."""
+    a = api()
+    nv, nx, nt = 2, 16384, 600
+    b = a.LocalBlock(ctx, nv, a.RowRange(0, nx), nt)
+    b.synth_oscillator(seed=1, n_modes=20, dt=1e-3, noise=1e-3)
+    raw = b.values
+    params, d = a.snapshot_pass(b, scaling=True)
+    oq, om = oracle.center(raw)
+    os_, _ = oracle.reduce_scales(oracle.local_maxabs(oq, nv, nx)[None, :])
+    oq = oracle.scale(oq, nv, nx, os_)
+    assert np.array_equal(params.local_means, om)
+    assert np.array_equal(params.scales, os_)
+    assert np.array_equal(b.values, oq)
+    ref = oracle.gram(oq)
+    assert rel_frob(d, ref) <= GRAM_TOL

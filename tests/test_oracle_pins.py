@@ -1,0 +1,199 @@
+"""Pin the CPU oracle (oracle/dopinf_oracle.c) before trusting it:
+  1. bit-for-bit against the golden vectors the UNMODIFIED reference produced
+     (tests/golden/reference_vectors.npz, tests/golden/make_golden.py);
+  2. against the reference's own known-answer tests (test_transform.cpp,
+     test_linalg.cpp, test_pod.cpp, test_data.cpp);
+  3. bit-for-bit against the compiled reference itself on random shapes, when
+     oracle/_ref is present (build container).
+CPU only.
+"""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+GOLDEN = np.load(Path(__file__).parent / "golden" / "reference_vectors.npz")
+
+
+def slices(q, n_vars, nx, plan):
+    nt = q.shape[1]
+    out = []
+    for b, e in plan:
+        parts = [q[j * nx + b: j * nx + e] for j in range(n_vars)]
+        out.append(np.concatenate(parts).reshape(-1, nt) if parts else np.zeros((0, nt)))
+    return out
+
+
+def oracle_pass(oracle, q, n_vars, nx, p, scaling=True):
+    """Steps II-III over p ranks with the oracle, the reference's data flow
+    (pipeline.cpp:270-280; MAX and ascending-rank SUM as comm_inprocess.cpp)."""
+    plan = oracle.partition_rows(nx, p)
+    blocks = slices(q, n_vars, nx, plan)
+    cent = [oracle.center(b) for b in blocks]
+    scales = None
+    if scaling:
+        per_rank = np.stack([oracle.local_maxabs(c, n_vars, e - b) for (c, _), (b, e) in zip(cent, plan)])
+        scales, bad = oracle.reduce_scales(per_rank)
+        assert bad == -1
+        cent = [(oracle.scale(c, n_vars, e - b, scales), m) for (c, m), (b, e) in zip(cent, plan)]
+    d = oracle.allreduce_sum(np.stack([oracle.gram(c) for c, _ in cent]))
+    full = np.empty_like(q)
+    means = np.empty(q.shape[0])
+    for (c, m), (b, e) in zip(cent, plan):
+        nxi = e - b
+        for j in range(n_vars):
+            full[j * nx + b: j * nx + e] = c[j * nxi:(j + 1) * nxi]
+            means[j * nx + b: j * nx + e] = m[j * nxi:(j + 1) * nxi]
+    return full, means, scales, d
+
+
+@pytest.mark.parametrize("row", list(range(4)))
+def test_transform_golden(oracle, row):
+    nv, nx, nt, seed = (int(v) for v in GOLDEN["transform_meta"][row])
+    tag = {12: "t12", 8: "t8", 21: "t21", 77: "t77"}[seed]
+    q = oracle.rng(seed).matrix(nv * nx, nt)
+    qc, mc = oracle.center(q)
+    assert np.array_equal(qc, GOLDEN[f"transform_{tag}_centered"])
+    assert np.array_equal(mc, GOLDEN[f"transform_{tag}_center_means"])
+    for p in (1, 2, 3):
+        if f"transform_{tag}_p{p}_q" not in GOLDEN:
+            continue
+        full, means, scales, d = oracle_pass(oracle, q, nv, nx, p)
+        assert np.array_equal(full, GOLDEN[f"transform_{tag}_p{p}_q"])
+        assert np.array_equal(means, GOLDEN[f"transform_{tag}_p{p}_means"])
+        assert np.array_equal(scales, GOLDEN[f"transform_{tag}_p{p}_scales"])
+        assert np.array_equal(d, GOLDEN[f"transform_{tag}_p{p}_gram"])
+
+
+@pytest.mark.parametrize("tag,m,k,seed", [("g41", 20, 6, 41), ("g5", 13, 7, 5), ("g73", 30, 8, 73),
+                                          ("g6", 26, 20, 6)])
+def test_gram_golden(oracle, tag, m, k, seed):
+    q = oracle.rng(seed).matrix(m, k)
+    for p in (1, 2, 4):
+        plan = oracle.partition_rows(m, p)
+        d = oracle.allreduce_sum(np.stack([oracle.gram(q[b:e]) for b, e in plan]))
+        assert np.array_equal(d, GOLDEN[f"gram_{tag}_p{p}"])
+        if p == 1:
+            assert np.array_equal(d, d.T)
+
+
+def sweep_input(oracle, i):
+    m, nt, rk = (int(v) for v in GOLDEN["sweep_meta"][i])
+    rng = oracle.rng(1000 + i)
+    if rk == 0:
+        return rng.matrix(m, nt)
+    a = rng.matrix(m, rk)
+    return oracle.matmul(a, rng.matrix(rk, nt))
+
+
+@pytest.mark.parametrize("i", list(range(20)))
+def test_sweep_golden(oracle, i):
+    q = sweep_input(oracle, i)
+    d1 = oracle.gram(q)
+    assert np.array_equal(d1, GOLDEN[f"sweep_{i}_gram_p1"])
+    plan = oracle.partition_rows(q.shape[0], 7)
+    d7 = oracle.allreduce_sum(np.stack([oracle.gram(q[b:e]) for b, e in plan]))
+    assert np.array_equal(d7, GOLDEN[f"sweep_{i}_gram_p7"])
+    tr = GOLDEN[f"sweep_{i}_tr"]
+    assert np.array_equal(oracle.project(tr, d1), GOLDEN[f"sweep_{i}_qhat"])
+    sel = GOLDEN[f"sweep_{i}_basis_sel"]
+    assert np.array_equal(oracle.basis_rows(q, tr, sel), GOLDEN[f"sweep_{i}_basis_rows"])
+
+
+def test_pipeline_golden(oracle):
+    nv, nx, nt, r = (int(v) for v in GOLDEN["pipeline_meta"])
+    full, _, _, d = oracle_pass(oracle, GOLDEN["pipeline_input"], nv, nx, 1)
+    assert np.array_equal(full, GOLDEN["pipeline_q"])
+    assert np.array_equal(d, GOLDEN["pipeline_gram"])
+    assert np.array_equal(oracle.project(GOLDEN["pipeline_tr"], d), GOLDEN["pipeline_qhat"])
+
+
+# ---- known-answer tests of the reference suites -------------------------------------------
+def test_kat_transform(oracle):
+    q, m = oracle.center(np.array([[1.0, 3.0], [2.0, 2.0]]))        # test_transform.cpp:40-44
+    assert list(m) == [2.0, 2.0] and np.array_equal(q, [[-1.0, 1.0], [0.0, 0.0]])
+    q, m = oracle.center(np.array([[-3.0, 1.0, 3.0, -1.0]]))       # :46-49
+    assert list(m) == [0.0] and np.array_equal(q, [[-3.0, 1.0, 3.0, -1.0]])
+    # :69-85 cross-rank MAX: ranks hold [-3, 1] and [-2, 5] of one variable
+    s, bad = oracle.reduce_scales(np.array([[oracle.local_maxabs(np.array([[-3.0, 1.0]]), 1, 1)[0]],
+                                            [oracle.local_maxabs(np.array([[-2.0, 5.0]]), 1, 1)[0]]]))
+    assert list(s) == [5.0] and bad == -1
+    q = np.array([[-4.0, 2.0, 1.0]])                                  # :87-96
+    s, _ = oracle.reduce_scales(oracle.local_maxabs(q, 1, 1)[None, :])
+    assert list(s) == [4.0] and np.array_equal(oracle.scale(q, 1, 1, s), [[-1.0, 0.5, 0.25]])
+    q, _ = oracle.center(np.array([[4.0, 4, 4], [1, 2, 3]]))          # :115-128 degenerate var0
+    _, bad = oracle.reduce_scales(oracle.local_maxabs(q, 2, 1)[None, :])
+    assert bad == 0
+
+
+def test_kat_scaled_bound(oracle):
+    # test_transform.cpp:98-113 with the reference stream Rng(8)
+    q, _ = oracle.center(oracle.rng(8).matrix(30, 11))
+    s, _ = oracle.reduce_scales(oracle.local_maxabs(q, 2, 15)[None, :])
+    v = oracle.scale(q, 2, 15, s)
+    assert np.all(np.abs(v) <= 1.0) and np.max(np.abs(v)) == 1.0
+
+
+def test_kat_forward_inverse(oracle):
+    # test_transform.cpp:130-150
+    raw = oracle.rng(21).matrix(24, 9)
+    q, m = oracle.center(raw)
+    s, _ = oracle.reduce_scales(oracle.local_maxabs(q, 2, 12)[None, :])
+    back = oracle.inverse_transform(oracle.scale(q, 2, 12, s), 12, m, s, True)
+    assert np.allclose(back, raw, rtol=1e-12, atol=0)
+
+
+def test_kat_linalg(oracle):
+    # test_linalg.cpp:14-38
+    a = np.array([[1.0, 2, 3], [4, 5, 6]])
+    b = np.array([[7.0, 8], [9, 10], [11, 12]])
+    assert np.array_equal(oracle.matmul(a, b), [[58, 64], [139, 154]])
+    tn = oracle.matmul_tn(a, np.eye(2))
+    assert tn[0, 0] == 1 and tn[0, 1] == 4 and tn[2, 1] == 6
+    g = oracle.gram(oracle.rng(5).matrix(13, 7))                     # :40-62
+    assert np.array_equal(g, g.T)
+
+
+def test_kat_partition(oracle):
+    # test_data.cpp:19-62
+    assert oracle.partition_rows(8, 2) == [(0, 4), (4, 8)]
+    assert oracle.partition_rows(10, 3) == [(0, 3), (3, 6), (6, 10)]
+    assert [e - b for b, e in oracle.partition_rows(146339, 4)] == [36584, 36584, 36584, 36587]
+    assert oracle.partition_rows(5, 1) == [(0, 5)]
+    for nx, p in ((10, 0), (10, -1), (3, 4)):
+        with pytest.raises(ValueError):
+            oracle.partition_rows(nx, p)
+    for nx in (1, 2, 7, 64, 101):
+        for p in range(1, nx + 1):
+            plan = oracle.partition_rows(nx, p)
+            assert plan[0][0] == 0 and plan[-1][1] == nx
+            assert all(plan[i][0] == plan[i - 1][1] for i in range(1, p))
+            assert all(e - b == nx // p for b, e in plan[:-1])
+
+
+# ---- direct pin against the compiled reference (build container only) -----------------------------
+def test_rng_matches_reference(oracle, reference):
+    for seed in (1, 12, 1000, 4242):
+        assert np.array_equal(oracle.normals(seed, 2001), reference.normals(seed, 2001))
+
+
+@pytest.mark.parametrize("m,k", [(20, 7), (13, 7), (57, 23), (500, 50), (3, 1), (1, 5), (33, 4), (129, 130)])
+def test_oracle_bitwise_vs_reference(oracle, reference, m, k):
+    rng = np.random.default_rng(m * 7 + k)
+    q = rng.standard_normal((m, k)) * 10 + 3
+    assert np.array_equal(oracle.gram(q), reference.gram(q))
+    assert all(np.array_equal(x, y) for x, y in zip(oracle.center(q), reference.center(q)))
+    tr = rng.standard_normal((k, min(5, k)))
+    d = oracle.gram(q)
+    assert np.array_equal(oracle.project(tr, d), reference.project(tr, d))
+    assert np.array_equal(oracle.matmul(q, tr), reference.matmul(q, tr))
+    assert np.array_equal(oracle.basis_rows(q, tr, [0, m - 1]), reference.basis_rows(q, tr, [0, m - 1]))
+
+
+@pytest.mark.parametrize("nv,nx,nt,p", [(2, 15, 11, 1), (2, 15, 11, 2), (3, 40, 33, 3), (4, 50, 17, 4)])
+def test_oracle_pass_vs_reference(oracle, reference, nv, nx, nt, p):
+    q = np.random.default_rng(nv + nx + nt + p).standard_normal((nv * nx, nt)) * 5 - 2
+    rq, rm, rs, rd, _ = reference.snapshot_pass(q, nv, nx, p, True)
+    oq, om, os_, od = oracle_pass(oracle, q, nv, nx, p)
+    assert np.array_equal(rq, oq) and np.array_equal(rm, om) and np.array_equal(rs, os_)
+    assert np.array_equal(rd, od)
