@@ -1,0 +1,296 @@
+// dopinf_b200.hpp — header-only C++ host layer over the C ABI (dopinf_b200.h)
+// with the reference's stage signatures, so the reference pipeline can call it
+// in place of its own Steps II–III (paths relative to /root/reference/proj):
+//
+//   dopinf_b200::transform::center_in_place(block)              transform.hpp:27
+//   dopinf_b200::transform::compute_global_scales(block, hdr, comm)  transform.hpp:32-34
+//   dopinf_b200::transform::scale_in_place(block, scales)       transform.hpp:37
+//   dopinf_b200::pod::local_gram(block)                          pod.hpp:28
+//   dopinf_b200::pod::global_gram(local, comm)                   pod.hpp:31
+//   dopinf_b200::pod::project(tr, d)                             pod.hpp:49
+//   dopinf_b200::postprocess::basis_rows(block, tr, rows)        postprocess.hpp:25-26
+//   dopinf_b200::postprocess::basis(block, tr)  (Φ_r of reconstruct_field, postprocess.cpp:66)
+//   dopinf_b200::data::partition_rows(nx, p)                     data.hpp:47
+//
+// The functions are templates over the caller's block / matrix / header types
+// (duck-typed on the members the reference's data::LocalBlock, Matrix and
+// SnapshotHeader have), so they accept the reference's own types without this
+// header including them. Value semantics are kept: a transform mutates the
+// caller's host block. Each rank thread binds its Context first
+// (dopinf_b200::Bind), mirroring one Comm per rank under run_on_workers.
+//
+// Errors: with DOPINF_B200_REFERENCE_ERRORS defined (after including the
+// reference's "dopinf/errors.hpp"), failures throw the reference classes
+// (dopinf::InvalidArgumentError, PartitionError, CollectiveError,
+// DegenerateVariableError, dopinf::Error); otherwise the same-named classes in
+// namespace dopinf_b200.
+#pragma once
+
+#include <cstddef>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "dopinf_b200.h"
+
+namespace dopinf_b200 {
+
+#if defined(DOPINF_B200_REFERENCE_ERRORS)
+using Error = ::dopinf::Error;
+using InvalidArgumentError = ::dopinf::InvalidArgumentError;
+using PartitionError = ::dopinf::PartitionError;
+using CollectiveError = ::dopinf::CollectiveError;
+using DegenerateVariableError = ::dopinf::DegenerateVariableError;
+#else
+struct Error : std::runtime_error {
+    explicit Error(const std::string& m) : std::runtime_error(m) {}
+};
+struct InvalidArgumentError : Error {
+    using Error::Error;
+};
+struct PartitionError : Error {
+    using Error::Error;
+};
+struct CollectiveError : Error {
+    using Error::Error;
+};
+struct DegenerateVariableError : Error {
+    using Error::Error;
+};
+#endif
+
+[[noreturn]] inline void raise(int status, const std::string& msg) {
+    switch (status) {
+        case DOPINF_B200_ERR_INVALID_ARGUMENT: throw InvalidArgumentError(msg);
+        case DOPINF_B200_ERR_PARTITION: throw PartitionError(msg);
+        case DOPINF_B200_ERR_COLLECTIVE: throw CollectiveError(msg);
+        case DOPINF_B200_ERR_DEGENERATE_VARIABLE: throw DegenerateVariableError(msg);
+        default: throw Error(msg);
+    }
+}
+
+// ---- per-rank context ---------------------------------------------------------
+class Context {
+public:
+    Context(int device, int rank = 0, int size = 1, const unsigned char* nccl_id = nullptr) {
+        const int rc = dopinf_b200_ctx_create(device, rank, size, nccl_id, &ctx_);
+        if (rc != DOPINF_B200_OK) raise(rc, std::string("dopinf_b200_ctx_create: ") + dopinf_b200_status_string(rc));
+    }
+    ~Context() { dopinf_b200_ctx_destroy(ctx_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+
+    static std::vector<unsigned char> unique_id() {
+        std::vector<unsigned char> id(DOPINF_B200_UNIQUE_ID_BYTES);
+        check(dopinf_b200_get_unique_id(id.data()), nullptr, "get_unique_id");
+        return id;
+    }
+
+    int rank() const { return dopinf_b200_ctx_rank(ctx_); }
+    int size() const { return dopinf_b200_ctx_size(ctx_); }
+    dopinf_b200_ctx* handle() const { return ctx_; }
+
+    // comm::Comm::allreduce (comm.hpp:20-28): 0 = Sum, 1 = Max, 2 = Min.
+    void allreduce(double* data, std::size_t count, int op) {
+        check(dopinf_b200_allreduce(ctx_, data, count, op), ctx_, "allreduce");
+    }
+    void barrier() { check(dopinf_b200_barrier(ctx_), ctx_, "barrier"); }
+    double stage_ms(dopinf_b200_stage s) const {
+        double ms = 0.0;
+        dopinf_b200_stage_ms(ctx_, s, &ms);
+        return ms;
+    }
+
+    static void check(int rc, const dopinf_b200_ctx* c, const char* what) {
+        if (rc != DOPINF_B200_OK) {
+            raise(rc, std::string(what) + ": " + (c ? dopinf_b200_last_error(c) : dopinf_b200_status_string(rc)));
+        }
+    }
+
+private:
+    dopinf_b200_ctx* ctx_ = nullptr;
+};
+
+namespace detail {
+inline Context*& bound() {
+    thread_local Context* ctx = nullptr;
+    return ctx;
+}
+inline Context& ctx() {
+    if (!bound()) throw InvalidArgumentError("dopinf_b200: no Context bound on this thread (use dopinf_b200::Bind)");
+    return *bound();
+}
+}  // namespace detail
+
+// RAII binding of a rank's Context to the calling thread.
+class Bind {
+public:
+    explicit Bind(Context& c) : prev_(detail::bound()) { detail::bound() = &c; }
+    ~Bind() { detail::bound() = prev_; }
+
+private:
+    Context* prev_;
+};
+
+// Device mirror of one host LocalBlock (data.hpp:38-42).
+class DeviceBlock {
+public:
+    DeviceBlock(Context& c, std::size_t n_vars, std::size_t nx_i, std::size_t row_begin, std::size_t nt)
+        : ctx_(c) {
+        Context::check(dopinf_b200_block_create(c.handle(), n_vars, nx_i, row_begin, nt, &b_), c.handle(),
+                       "block_create");
+    }
+    ~DeviceBlock() { dopinf_b200_block_destroy(b_); }
+    DeviceBlock(const DeviceBlock&) = delete;
+    DeviceBlock& operator=(const DeviceBlock&) = delete;
+    DeviceBlock(DeviceBlock&& o) noexcept : ctx_(o.ctx_), b_(o.b_) { o.b_ = nullptr; }
+
+    void upload(const double* host, std::size_t ld) {
+        Context::check(dopinf_b200_block_upload(b_, host, ld), ctx_.handle(), "upload");
+    }
+    void download(double* host, std::size_t ld) {
+        Context::check(dopinf_b200_block_download(b_, host, ld), ctx_.handle(), "download");
+    }
+    dopinf_b200_block* handle() const { return b_; }
+    Context& context() const { return ctx_; }
+
+private:
+    Context& ctx_;
+    dopinf_b200_block* b_ = nullptr;
+};
+
+namespace detail {
+// n_vars of a block: rows / nx_i (the reference derives it from the header).
+template <class LocalBlockT>
+std::size_t n_vars_of(const LocalBlockT& block) {
+    const std::size_t nx_i = block.row_range.count();
+    return nx_i == 0 ? 1 : block.values.rows() / nx_i;
+}
+
+template <class LocalBlockT>
+DeviceBlock uploaded(const LocalBlockT& block, std::size_t n_vars) {
+    DeviceBlock d(ctx(), n_vars, block.row_range.count(), block.row_range.begin, block.values.cols());
+    d.upload(block.values.data(), block.values.cols());
+    return d;
+}
+}  // namespace detail
+
+namespace data {
+// data.cpp:86-103. Returns a vector of (begin, end) as PlanT's element type.
+template <class RowRangeT>
+std::vector<RowRangeT> partition_rows(std::size_t nx, int p) {
+    if (p < 1) throw PartitionError("partition_rows: rank count must be >= 1, got " + std::to_string(p));
+    if (static_cast<std::size_t>(p) > nx) {
+        throw PartitionError("partition_rows: rank count " + std::to_string(p) + " exceeds row count " +
+                             std::to_string(nx));
+    }
+    std::vector<std::size_t> b(static_cast<std::size_t>(p)), e(static_cast<std::size_t>(p));
+    Context::check(dopinf_b200_partition_rows(nx, p, b.data(), e.data()), nullptr, "partition_rows");
+    std::vector<RowRangeT> plan(static_cast<std::size_t>(p));
+    for (std::size_t r = 0; r < plan.size(); ++r) {
+        plan[r].begin = b[r];
+        plan[r].end = e[r];
+    }
+    return plan;
+}
+}  // namespace data
+
+namespace transform {
+// transform.cpp:10-20
+template <class LocalBlockT>
+std::vector<double> center_in_place(LocalBlockT& block) {
+    DeviceBlock d = detail::uploaded(block, detail::n_vars_of(block));
+    std::vector<double> means(block.values.rows());
+    Context::check(dopinf_b200_center(d.handle(), means.data()), d.context().handle(), "center_in_place");
+    d.download(block.values.data(), block.values.cols());
+    return means;
+}
+
+// transform.cpp:22-41 (MAX all-reduce over NCCL; `comm` must be this rank's).
+template <class LocalBlockT, class HeaderT, class CommT>
+std::vector<double> compute_global_scales(const LocalBlockT& block, const HeaderT& header, CommT& comm) {
+    if (comm.size() != detail::ctx().size() || comm.rank() != detail::ctx().rank()) {
+        throw CollectiveError("compute_global_scales: comm does not match the bound device context");
+    }
+    const std::size_t n_vars = static_cast<std::size_t>(header.n_vars);
+    DeviceBlock d = detail::uploaded(block, n_vars);
+    std::vector<double> scales(n_vars);
+    std::size_t bad = 0;
+    const int rc = dopinf_b200_global_scales(d.handle(), scales.data(), &bad);
+    if (rc == DOPINF_B200_ERR_DEGENERATE_VARIABLE) {
+        throw DegenerateVariableError("variable '" + header.var_names[bad] +
+                                      "' is constant in time; max-abs scaling is undefined");
+    }
+    Context::check(rc, d.context().handle(), "compute_global_scales");
+    return scales;
+}
+
+// transform.cpp:43-49
+template <class LocalBlockT>
+void scale_in_place(LocalBlockT& block, const std::vector<double>& scales) {
+    DeviceBlock d = detail::uploaded(block, scales.size());
+    Context::check(dopinf_b200_scale(d.handle(), scales.data()), d.context().handle(), "scale_in_place");
+    d.download(block.values.data(), block.values.cols());
+}
+}  // namespace transform
+
+namespace pod {
+// pod.cpp:11-13: returns MatrixT (the block's values type) nt x nt.
+template <class LocalBlockT>
+auto local_gram(const LocalBlockT& block) -> std::decay_t<decltype(block.values)> {
+    using MatrixT = std::decay_t<decltype(block.values)>;
+    const std::size_t nt = block.values.cols();
+    DeviceBlock d = detail::uploaded(block, detail::n_vars_of(block));
+    MatrixT out(nt, nt);
+    Context::check(dopinf_b200_local_gram(d.handle(), out.data()), d.context().handle(), "local_gram");
+    return out;
+}
+
+// pod.cpp:15-18: reduces the device copy of the last local Gram of this rank.
+template <class MatrixT, class CommT>
+MatrixT global_gram(MatrixT local, CommT& comm) {
+    if (comm.size() != detail::ctx().size()) throw CollectiveError("global_gram: comm size mismatch");
+    Context::check(dopinf_b200_global_gram(detail::ctx().handle(), local.data()), detail::ctx().handle(),
+                   "global_gram");
+    return local;
+}
+
+// pod.cpp:103-105: Q̂ = T_rᵀ D, the reference's FMA order (bit-identical).
+template <class MatrixT>
+MatrixT project(const MatrixT& tr, const MatrixT& d) {
+    if (tr.rows() != d.rows() || d.rows() != d.cols()) throw InvalidArgumentError("matmul_tn: row counts differ");
+    MatrixT out(tr.cols(), d.cols());
+    Context::check(dopinf_b200_project_host(detail::ctx().handle(), tr.data(), d.data(), d.rows(), tr.cols(),
+                                            out.data()),
+                   detail::ctx().handle(), "project");
+    return out;
+}
+}  // namespace pod
+
+namespace postprocess {
+// postprocess.cpp:12-34 (bit-identical order).
+template <class LocalBlockT, class MatrixT>
+MatrixT basis_rows(const LocalBlockT& block, const MatrixT& tr, const std::vector<std::size_t>& local_rows) {
+    if (block.values.cols() != tr.rows()) throw InvalidArgumentError("basis_rows: block and map disagree on nt");
+    DeviceBlock d = detail::uploaded(block, detail::n_vars_of(block));
+    MatrixT out(local_rows.size(), tr.cols());
+    Context::check(dopinf_b200_basis_rows(d.handle(), tr.data(), tr.cols(), local_rows.data(), local_rows.size(),
+                                          out.data()),
+                   d.context().handle(), "basis_rows");
+    return out;
+}
+
+// Φ_r = Q · T_r (postprocess.cpp:66), DMMA tall GEMM.
+template <class LocalBlockT, class MatrixT>
+MatrixT basis(const LocalBlockT& block, const MatrixT& tr) {
+    if (block.values.cols() != tr.rows()) throw InvalidArgumentError("matmul: inner dimensions differ");
+    DeviceBlock d = detail::uploaded(block, detail::n_vars_of(block));
+    MatrixT out(block.values.rows(), tr.cols());
+    Context::check(dopinf_b200_basis(d.handle(), tr.data(), tr.cols(), out.data()), d.context().handle(), "basis");
+    return out;
+}
+}  // namespace postprocess
+
+}  // namespace dopinf_b200

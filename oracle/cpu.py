@@ -41,7 +41,7 @@ class Oracle:
         if Oracle._lib is None:
             if not ORACLE_SO.exists():
                 ORACLE_SO.parent.mkdir(exist_ok=True)
-                subprocess.run(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared", "-o",
+                subprocess.run(["gcc", "-O2", "-std=c11", "-mfma", "-ffp-contract=off", "-fPIC", "-shared", "-o",
                                 str(ORACLE_SO), str(HERE / "dopinf_oracle.c"), "-lm"], check=True)
             lib = C.CDLL(str(ORACLE_SO))
             lib.oracle_rng_new.restype = C.c_void_p

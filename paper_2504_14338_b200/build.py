@@ -33,6 +33,20 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found: the sm_100a extension cannot be built")
 
 
+def _nccl_dir():
+    """The NCCL torch ships (nvidia-nccl wheel), so one libnccl.so.2 serves both
+    torch and this library in a process; the system copy only as a fallback."""
+    try:
+        import nvidia.nccl as n
+
+        d = Path(list(n.__path__)[0])
+        if (d / "lib" / "libnccl.so.2").exists() and (d / "include" / "nccl.h").exists():
+            return d
+    except Exception:  # noqa: BLE001
+        pass
+    return None
+
+
 def _stale(target: Path, deps) -> bool:
     if not target.exists():
         return True
@@ -43,12 +57,14 @@ def _stale(target: Path, deps) -> bool:
 def build_extension(force: bool = False, verbose: bool = False) -> Path:
     nvcc = _nvcc()
     BUILD.mkdir(exist_ok=True)
+    nccl = _nccl_dir()
+    flags = list(NVCC_FLAGS) + (["-I", str(nccl / "include")] if nccl else [])
     headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "dopinf_b200.h"]
     jobs = []
     for src in SOURCES:
         obj = BUILD / (Path(src).stem + ".o")
         if force or _stale(obj, [CSRC / src, *headers]):
-            jobs.append([nvcc, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)])
+            jobs.append([nvcc, *flags, "-c", str(CSRC / src), "-o", str(obj)])
     with cf.ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         for cmd, res in zip(jobs, ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs)):
             if res.returncode != 0:
@@ -58,7 +74,11 @@ def build_extension(force: bool = False, verbose: bool = False) -> Path:
     objs = [BUILD / (Path(s).stem + ".o") for s in SOURCES]
     if force or jobs or _stale(LIB, objs):
         cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB),
-               *map(str, objs), "-lnccl"]
+               *map(str, objs)]
+        if nccl:
+            cmd += [f"-L{nccl / 'lib'}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{nccl / 'lib'}"]
+        else:
+            cmd += ["-lnccl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")

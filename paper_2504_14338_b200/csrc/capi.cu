@@ -92,6 +92,37 @@ struct DBuf {
     }
 };
 
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Grow-only pinned host staging buffer (pageable D2H through the driver runs
+// at a few GB/s; a pinned hop plus a host memcpy is several times faster).
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need) {
+        if (need > bytes) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            bytes = 0;
+            ck(cudaMallocHost(&p, need), "pinned staging");
+            bytes = need;
+        }
+        return p;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
 struct DeviceGuard {
     int prev = 0;
     explicit DeviceGuard(int dev) {
@@ -122,6 +153,20 @@ struct dopinf_b200_ctx {
     bool counters_zeroed = false;
     // scratch
     DBuf scales, tr, trt, qhat, sel, rows_out, span;
+    PinnedBuf staging;
+
+    // Device → host copy that completes before returning (callers sync anyway).
+    void d2h(void* dst, const void* src, size_t bytes, const char* what) {
+        if (bytes < (size_t(1) << 20) || is_pinned(dst)) {
+            ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream), what);
+            ck(cudaStreamSynchronize(stream), what);
+            return;
+        }
+        void* st = staging.get(bytes);
+        ck(cudaMemcpyAsync(st, src, bytes, cudaMemcpyDeviceToHost, stream), what);
+        ck(cudaStreamSynchronize(stream), what);
+        std::memcpy(dst, st, bytes);
+    }
     // stage timing
     cudaEvent_t ev[DOPINF_B200_STAGE_COUNT][2] = {};
     bool ev_done[DOPINF_B200_STAGE_COUNT] = {};
@@ -257,9 +302,8 @@ void do_scale(dopinf_b200_block* b, const double* scales_host) {
 void copy_d_out(dopinf_b200_ctx* c, double* d_host) {
     if (!d_host) return;
     c->record(DOPINF_B200_STAGE_DOWNLOAD, 0);
-    ck(cudaMemcpyAsync(d_host, c->dmat.get<double>(static_cast<size_t>(c->K) * c->K, "D"),
-                       static_cast<size_t>(c->K) * c->K * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
-       "D D2H");
+    const size_t n = static_cast<size_t>(c->K) * c->K;
+    c->d2h(d_host, c->dmat.get<double>(n, "D"), n * sizeof(double), "D D2H");
     c->record(DOPINF_B200_STAGE_DOWNLOAD, 1);
 }
 
@@ -352,10 +396,7 @@ void do_project(dopinf_b200_ctx* c, const double* tr_host, const double* d_dev, 
     ck(project::launch_project(dtr, d_dev, static_cast<int>(nt), static_cast<int>(r), dq, c->stream),
        "project");
     c->record(DOPINF_B200_STAGE_PROJECT, 1);
-    if (qhat_host) {
-        ck(cudaMemcpyAsync(qhat_host, dq, nt * r * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
-           "qhat D2H");
-    }
+    if (qhat_host) c->d2h(qhat_host, dq, nt * r * sizeof(double), "qhat D2H");
 }
 
 }  // namespace
@@ -449,6 +490,7 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
                     &c->scales, &c->tr, &c->trt, &c->qhat, &c->sel, &c->rows_out, &c->span}) {
         b->release();
     }
+    c->staging.release();
     if (c->stream) cudaStreamDestroy(c->stream);
     cudaSetDevice(prev);
     delete c;

@@ -24,39 +24,30 @@ namespace project {
 
 namespace {
 
-constexpr int kProjRowsPerThread = 8;
+constexpr int kProjRowsPerThread = 2;
+constexpr int kProjThreads = 64;
 
-__global__ void __launch_bounds__(128)
+// One thread per (2 rows of Q̂, column j): two independent in-order FMA chains
+// over l; D[l][j] coalesced across the block, T_r[l][i] broadcast. The chain
+// latency (K dependent DFMAs) bounds the kernel, so the grid is made wide.
+__global__ void __launch_bounds__(kProjThreads)
     project_kernel(const double* __restrict__ tr, const double* __restrict__ d, int K, int r,
                    double* __restrict__ qhat) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int i0 = blockIdx.y * kProjRowsPerThread;
     if (j >= K) return;
-    double acc[kProjRowsPerThread];
-#pragma unroll
-    for (int ii = 0; ii < kProjRowsPerThread; ++ii) acc[ii] = 0.0;
-    const int ni = min(kProjRowsPerThread, r - i0);
-    if (ni == kProjRowsPerThread) {
-        for (int l = 0; l < K; ++l) {
-            const double dv = __ldg(d + static_cast<size_t>(l) * K + j);
-            const double* trl = tr + static_cast<size_t>(l) * r + i0;
-#pragma unroll
-            for (int ii = 0; ii < kProjRowsPerThread; ++ii) acc[ii] = fma(__ldg(trl + ii), dv, acc[ii]);
-        }
-    } else {
-        for (int l = 0; l < K; ++l) {
-            const double dv = __ldg(d + static_cast<size_t>(l) * K + j);
-            const double* trl = tr + static_cast<size_t>(l) * r + i0;
-#pragma unroll
-            for (int ii = 0; ii < kProjRowsPerThread; ++ii) {
-                if (ii < ni) acc[ii] = fma(__ldg(trl + ii), dv, acc[ii]);
-            }
-        }
+    double acc0 = 0.0, acc1 = 0.0;
+    const bool two = i0 + 1 < r;
+    const double* dj = d + j;
+    const double* trl = tr + i0;
+#pragma unroll 8
+    for (int l = 0; l < K; ++l) {
+        const double dv = __ldg(dj + static_cast<size_t>(l) * K);
+        acc0 = fma(__ldg(trl + static_cast<size_t>(l) * r), dv, acc0);
+        if (two) acc1 = fma(__ldg(trl + static_cast<size_t>(l) * r + 1), dv, acc1);
     }
-#pragma unroll
-    for (int ii = 0; ii < kProjRowsPerThread; ++ii) {
-        if (ii < ni) qhat[static_cast<size_t>(i0 + ii) * K + j] = acc[ii];
-    }
+    qhat[static_cast<size_t>(i0) * K + j] = acc0;
+    if (two) qhat[static_cast<size_t>(i0 + 1) * K + j] = acc1;
 }
 
 __global__ void basis_rows_kernel(const double* __restrict__ q, size_t ld, int K,
@@ -247,8 +238,8 @@ int basis_cols_pad(int r) {
 
 cudaError_t launch_project(const double* tr, const double* d, int K, int r, double* qhat,
                            cudaStream_t stream) {
-    dim3 grid((K + 127) / 128, (r + kProjRowsPerThread - 1) / kProjRowsPerThread);
-    project_kernel<<<grid, 128, 0, stream>>>(tr, d, K, r, qhat);
+    dim3 grid((K + kProjThreads - 1) / kProjThreads, (r + kProjRowsPerThread - 1) / kProjRowsPerThread);
+    project_kernel<<<grid, kProjThreads, 0, stream>>>(tr, d, K, r, qhat);
     note_launch();
     return cudaGetLastError();
 }
