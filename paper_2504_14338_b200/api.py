@@ -86,6 +86,12 @@ def _check(rc: int, ctx=None, what: str = ""):
     raise _STATUS.get(rc, Error)(f"{what}: {msg}" if what else msg)
 
 
+def _out(a: np.ndarray, shape) -> np.ndarray:
+    if a.dtype != np.float64 or not a.flags.c_contiguous or a.shape != tuple(shape):
+        raise InvalidArgumentError(f"output buffer must be C-contiguous float64 of shape {tuple(shape)}")
+    return a
+
+
 def _f64(a, shape=None) -> np.ndarray:
     out = np.ascontiguousarray(a, dtype=np.float64)
     if shape is not None and out.shape != shape:
@@ -330,11 +336,12 @@ def project(tr, d, ctx: DeviceContext) -> np.ndarray:
     return out
 
 
-def project_resident(ctx: DeviceContext, tr) -> np.ndarray:
-    """Q̂ = T_rᵀ D with the context's device-resident (global) Gram."""
+def project_resident(ctx: DeviceContext, tr, out: np.ndarray | None = None) -> np.ndarray:
+    """Q̂ = T_rᵀ D with the context's device-resident (global) Gram. `out`
+    (r × nt float64, e.g. pinned) is filled when given."""
     tr = _f64(tr)
     nt, r = tr.shape
-    out = np.empty((r, nt), dtype=np.float64)
+    out = np.empty((r, nt), dtype=np.float64) if out is None else _out(out, (r, nt))
     _check(_lib.load().dopinf_b200_project(ctx._h, _lib.dptr(tr), nt, r, _lib.dptr(out)), ctx, "project")
     return out
 
@@ -364,12 +371,14 @@ def basis(block: LocalBlock, tr, download: bool = True):
     return out
 
 
-def snapshot_pass(block: LocalBlock, scaling: bool):
+def snapshot_pass(block: LocalBlock, scaling: bool, out: dict | None = None):
     """Steps II–III of pipeline::run_rank (pipeline.cpp:270-280) in one call:
-    returns (TransformParams, D)."""
-    means = np.empty(block.rows, dtype=np.float64)
-    scales = np.empty(block.n_vars, dtype=np.float64)
-    d = np.empty((block.nt, block.nt), dtype=np.float64)
+    returns (TransformParams, D). `out` may carry preallocated (e.g. pinned)
+    "means", "scales" and "d" arrays to fill."""
+    out = out or {}
+    means = _out(out["means"], (block.rows,)) if "means" in out else np.empty(block.rows, dtype=np.float64)
+    scales = _out(out["scales"], (block.n_vars,)) if "scales" in out else np.empty(block.n_vars, dtype=np.float64)
+    d = _out(out["d"], (block.nt, block.nt)) if "d" in out else np.empty((block.nt, block.nt), dtype=np.float64)
     _check(_lib.load().dopinf_b200_snapshot_pass(block._h, 1 if scaling else 0, _lib.dptr(means),
                                                  _lib.dptr(scales), _lib.dptr(d)), block.ctx, "snapshot_pass")
     params = TransformParams(means, scales if scaling else np.zeros(0), scaling)

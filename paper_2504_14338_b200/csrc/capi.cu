@@ -337,7 +337,8 @@ void do_local_gram(dopinf_b200_block* b, double* d_host) {
         if (c->plan_K != K || c->plan_rows != rows) {
             size_t free_b = 0, total_b = 0;
             cudaMemGetInfo(&free_b, &total_b);
-            const size_t cap = std::min<size_t>(size_t(2) << 30, std::max<size_t>(free_b / 8, size_t(64) << 20));
+            const size_t cap =
+                std::min<size_t>(gram::kWorkspaceCapBytes, std::max<size_t>(free_b / 8, size_t(64) << 20));
             c->plan = gram::make_plan(rows, K, c->num_sms, cap);
             c->plan_K = K;
             c->plan_rows = rows;

@@ -10,10 +10,11 @@
 //     atomic queue, so the CTAs running at any moment read the same rows of
 //     Q (L2 reuse across the ~tiles CTAs that need them).
 //   * Each persistent CTA = 1 TMA producer warp + 16 consumer warps. The
-//     producer streams BK×128 row-slabs of the I and J column blocks through a
-//     6-stage mbarrier ring (cp.async.bulk.tensor, OOB rows/cols zero-filled);
-//     consumers run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) on 32×32 warp tiles
-//     with fragments read as conflict-free 128-bit shared loads.
+//     producer streams BK×128 row-slabs of the I and J column blocks (8 boxes
+//     of 16 columns, 128-byte swizzle) through a 6-stage mbarrier ring
+//     (cp.async.bulk.tensor, OOB rows/cols zero-filled); consumers run
+//     mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) on 32×32 warp tiles with
+//     fragments read as conflict-free 128-bit shared loads.
 //   * Diagonal tiles skip warp tiles / mma tiles strictly below the diagonal
 //     and edge tiles skip columns >= K; the remaining warp tiles are balanced
 //     over the 4 SM sub-partitions on the host (LPT).
@@ -24,6 +25,7 @@
 //     D (bitwise symmetric, as linalg.hpp:17 promises for the reference).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -43,7 +45,7 @@ constexpr int CONSUMERS = kConsumerWarps;  // 16
 constexpr int THREADS = (CONSUMERS + 1) * kWarp;
 constexpr int FLAG_FIRST = 1, FLAG_LAST = 2, FLAG_DONE = 4;
 
-struct __align__(128) Smem {
+struct __align__(1024) Smem {
     double a[STAGES][BK * BT];
     double b[STAGES][BK * BT];
     uint64_t full[STAGES];
@@ -60,15 +62,26 @@ __device__ __forceinline__ void decode(uint32_t e, int& wm, int& wn, bool& diag,
     mask = e >> 16;
 }
 
+// Operand tile of one stage: 8 TMA boxes of BK rows × 16 doubles (one 128 B
+// line per row) written with the 128-byte swizzle: element (row, col) of box
+// col/16 sits in 16-byte chunk ((col%16)/2) ^ (row%8) of its line.
+//
+// Fragment loads: lane (g, t) reads, for mma k-step ks, Q row
+// (ks/2)*8 + ks%2 + 2t — so within a quarter-warp the four rows have
+// row%8 ∈ {0,2,4,6} (or {1,3,5,7}) — and columns 2g, 2g+1 as one 128-bit load.
+// The swizzle then puts the quarter-warp's 8 loads in 8 distinct chunks:
+// conflict-free (4 wavefronts per 512 B). ks permutes the contraction order
+// only; the output mapping is unchanged.
 template <bool kFull>
 __device__ __forceinline__ void stage_mma(double (&acc)[16][2], const double* __restrict__ as,
-                                          const double* __restrict__ bs, uint32_t mask) {
+                                          const double* __restrict__ bs, int xg0, int xg1, uint32_t mask) {
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
-        const double2 a0 = lds128(as + ks * 4 * BT);
-        const double2 a1 = lds128(as + ks * 4 * BT + 16);
-        const double2 b0 = lds128(bs + ks * 4 * BT);
-        const double2 b1 = lds128(bs + ks * 4 * BT + 16);
+        const int off = ((ks >> 1) * 8 + (ks & 1)) * 16 + ((ks & 1) ? xg1 : xg0);
+        const double2 a0 = lds128(as + off);
+        const double2 a1 = lds128(as + off + BK * 16);
+        const double2 b0 = lds128(bs + off);
+        const double2 b1 = lds128(bs + off + BK * 16);
         const double a[4] = {a0.x, a0.y, a1.x, a1.y};
         const double b[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
@@ -89,7 +102,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                      double* __restrict__ work, int* __restrict__ counters) {
     extern __shared__ unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~static_cast<uintptr_t>(127));
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int warp = threadIdx.x / kWarp;
     const int lane = threadIdx.x % kWarp;
 
@@ -130,8 +143,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                     s.meta_flags[stage] = (kb == 0 ? FLAG_FIRST : 0) | (kb == nkb - 1 ? FLAG_LAST : 0);
                     mbar_arrive_expect_tx(&s.full[stage], bytes);
                     const int y = static_cast<int>(row0 + static_cast<long long>(kb) * BK);
-                    tma_load_2d(s.a[stage], &tmap, I * BT, y, &s.full[stage]);
-                    if (!diag) tma_load_2d(s.b[stage], &tmap, J * BT, y, &s.full[stage]);
+#pragma unroll
+                    for (int box = 0; box < BT / 16; ++box) {
+                        tma_load_2d(s.a[stage] + box * BK * 16, &tmap, I * BT + box * 16, y, &s.full[stage]);
+                    }
+                    if (!diag) {
+#pragma unroll
+                        for (int box = 0; box < BT / 16; ++box) {
+                            tma_load_2d(s.b[stage] + box * BK * 16, &tmap, J * BT + box * 16, y, &s.full[stage]);
+                        }
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -142,6 +163,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else {
         // ---------------- DMMA consumers ----------------
         const int g = lane >> 2, t = lane & 3;
+        const int xg0 = (g ^ (2 * t)) << 1, xg1 = (g ^ (2 * t + 1)) << 1;
         double acc[16][2];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
@@ -157,12 +179,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int item = s.meta_item[stage];
             if (flags & FLAG_FIRST) decode(tiles[item % n_tiles].warp[warp], wm, wn, diag, mask);
             if (mask) {
-                const double* as = s.a[stage] + t * BT + wm * 32 + 2 * g;
-                const double* bs = (diag ? s.a[stage] : s.b[stage]) + t * BT + wn * 32 + 2 * g;
+                const double* as = s.a[stage] + (2 * wm) * BK * 16 + 2 * t * 16;
+                const double* bs = (diag ? s.a[stage] : s.b[stage]) + (2 * wn) * BK * 16 + 2 * t * 16;
                 if (mask == 0xFFFFu) {
-                    stage_mma<true>(acc, as, bs, mask);
+                    stage_mma<true>(acc, as, bs, xg0, xg1, mask);
                 } else {
-                    stage_mma<false>(acc, as, bs, mask);
+                    stage_mma<false>(acc, as, bs, xg0, xg1, mask);
                 }
             }
             __syncwarp();
@@ -329,8 +351,12 @@ Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes)
     p.K = K;
     p.n_rows = n_rows;
     p.n_tiles = static_cast<int>(plan_tiles(K).size());
+    // Enough items for load balance, and chunks short enough (kTargetChunkRows)
+    // that the CTAs working on one split stay within an L2-resident window of
+    // rows (measured: 31.8K-row chunks re-read Q ~4x from HBM, 8K-row ~1.5x).
     const long long target_items = static_cast<long long>(num_sms) * kItemsPerCta;
     long long S = (target_items + p.n_tiles - 1) / p.n_tiles;
+    S = std::max<long long>(S, (n_rows + kTargetChunkRows - 1) / kTargetChunkRows);
     // Keep the fixed-order reduction cheap relative to the contraction.
     S = std::min<long long>(S, std::max<long long>(1, n_rows / kMinRowsPerSplit));
     const long long per_item = static_cast<long long>(kItemDoubles) * sizeof(double);
@@ -338,6 +364,10 @@ Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes)
         S, std::max<long long>(1, static_cast<long long>(workspace_cap_bytes) / (per_item * p.n_tiles)));
     S = std::max<long long>(1, S);
     long long chunk = (n_rows + S - 1) / S;
+    if (const char* env = std::getenv("DOPINF_B200_GRAM_CHUNK_ROWS")) {  // tuning knob
+        const long long c = std::atoll(env);
+        if (c > 0) chunk = c;
+    }
     chunk = std::max<long long>(BK, (chunk + BK - 1) / BK * BK);
     S = std::max<long long>(1, (n_rows + chunk - 1) / chunk);
     p.n_splits = static_cast<int>(S);
@@ -353,16 +383,16 @@ cudaError_t make_tensor_map(CUtensorMap* map, const double* q, long long n_rows,
     if (!fn) return cudaErrorNotSupported;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(n_rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * sizeof(double))};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(BT), static_cast<cuuint32_t>(BK)};
+    const cuuint32_t box[2] = {16u, static_cast<cuuint32_t>(BK)};  // 128 B rows → 128B swizzle
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(q), dims,
                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-size_t smem_bytes() { return sizeof(Smem) + 128; }
+size_t smem_bytes() { return sizeof(Smem) + 1024; }
 
 cudaError_t launch_gram(const Plan& plan, const CUtensorMap& map, const TileInfo* d_tiles,
                         double* work, int* counters, cudaStream_t stream) {

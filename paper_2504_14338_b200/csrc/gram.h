@@ -18,6 +18,8 @@ constexpr int kWarpFragDoubles = 16 * 32 * 2;                   // 16 mma × 32 
 constexpr int kItemDoubles = kConsumerWarps * kWarpFragDoubles;  // 16384 (128 KiB)
 constexpr int kItemsPerCta = 16;     // queue granularity target (tail vs workspace)
 constexpr long long kMinRowsPerSplit = 768;
+constexpr long long kTargetChunkRows = 8192;  // L2 window of rows shared by a split's CTAs
+constexpr size_t kWorkspaceCapBytes = size_t(1) << 30;
 
 struct TileInfo {
     int I, J;

@@ -26,9 +26,29 @@ namespace {
 
 constexpr int kStatsWarps = 8;           // warps per block
 constexpr int kRowsPerWarp = 8;          // one 4-lane group per row
-constexpr int kColsPerIter = 32;
-constexpr int kPad = kColsPerIter + 4;   // row pitch in smem: 36 doubles (conflict-free)
+constexpr int kColsPerIter = 64;         // 8 rows × 64 columns = 4 KiB per warp per chunk
+constexpr int kPad = kColsPerIter + 4;   // row pitch in smem: 68 doubles (conflict-free reads)
+constexpr int kLoads = kRowsPerWarp * kColsPerIter / 64;  // 16-byte loads per lane per chunk
 constexpr int kMaxSmemVars = 64;
+
+// Lane's share of one chunk: rows r0 + 2(u/2) + lane/16, columns c0 + 32(u%2) + 2(lane%16).
+__device__ __forceinline__ void load_chunk(double2 (&v)[kLoads], const double* __restrict__ q, size_t ld,
+                                           long long rows, int K, long long r0, int c0, int lane) {
+#pragma unroll
+    for (int u = 0; u < kLoads; ++u) {
+        const long long lr = r0 + (u >> 1) * 2 + (lane >> 4);
+        const int col = c0 + (u & 1) * 32 + (lane & 15) * 2;
+        v[u] = make_double2(0.0, 0.0);
+        if (lr < rows) {
+            const double* src = q + static_cast<size_t>(lr) * ld + col;
+            if (col + 1 < K) {
+                v[u] = __ldcs(reinterpret_cast<const double2*>(src));
+            } else if (col < K) {
+                v[u].x = __ldcs(src);
+            }
+        }
+    }
+}
 
 __global__ void __launch_bounds__(kStatsWarps * 32)
     stats_kernel(const double* __restrict__ q, size_t ld, long long rows, int K, long long nx_i,
@@ -54,34 +74,24 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
         double lacc = 0.0;
         double mx = -__longlong_as_double(0x7ff0000000000000LL);
         double mn = __longlong_as_double(0x7ff0000000000000LL);
+        double2 v[kLoads];
+        load_chunk(v, q, ld, rows, K, r0, 0, lane);
         for (int c0 = 0; c0 < K; c0 += kColsPerIter) {
-            // Cooperative coalesced load of 8 rows × 32 columns: half-warp per row,
-            // 16-byte loads (ld is even, so column pairs are 16-byte aligned).
+            // Coalesced chunk (half-warp per 256 B row segment) → padded smem, then
+            // prefetch the next chunk into registers while this one is reduced.
 #pragma unroll
-            for (int rr = 0; rr < kRowsPerWarp; rr += 2) {
-                const int sub = lane >> 4;  // which of the two rows
-                const int cp = (lane & 15) * 2;
-                const long long lr = r0 + rr + sub;
-                const int col = c0 + cp;
-                double2 v = make_double2(0.0, 0.0);
-                if (lr < rows) {
-                    const double* src = q + static_cast<size_t>(lr) * ld + col;
-                    if (col + 1 < K) {
-                        v = __ldg(reinterpret_cast<const double2*>(src));
-                    } else if (col < K) {
-                        v.x = __ldg(src);
-                    }
-                }
-                *reinterpret_cast<double2*>(&wb[rr + sub][cp]) = v;
+            for (int u = 0; u < kLoads; ++u) {
+                *reinterpret_cast<double2*>(&wb[(u >> 1) * 2 + (lane >> 4)][(u & 1) * 32 + (lane & 15) * 2]) = v[u];
             }
             __syncwarp();
+            if (c0 + kColsPerIter < K) load_chunk(v, q, ld, rows, K, r0, c0 + kColsPerIter, lane);
             if (row_ok) {
 #pragma unroll
-                for (int s = 0; s < 8; ++s) {
+                for (int s = 0; s < kColsPerIter / 4; ++s) {
                     const int col = c0 + 4 * s + j;
                     if (col < K) {
                         const double x = wb[g][4 * s + j];
-                        if (col < K4) lacc += x;  // lane j of the AVX2 accumulator
+                        if (col < K4) lacc += x;  // lane j of the AVX2 accumulator, in order
                         mx = fmax(mx, x);
                         mn = fmin(mn, x);
                     }
@@ -124,7 +134,11 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
 }
 
 // x ← (x − mean[row]) / scale[var]  (or x − mean when scales == nullptr).
-// Warp per row, 16-byte accesses; odd K handled by a scalar last column.
+// Warp per row; each lane issues kApplyBatch independent 16-byte loads before
+// any store (streaming hints: the block is touched once per pass).
+constexpr int kApplyBatch = 4;
+
+template <bool kScale>
 __global__ void __launch_bounds__(256)
     apply_kernel(double* __restrict__ q, size_t ld, long long rows, int K, long long nx_i,
                  const double* __restrict__ means, const double* __restrict__ scales) {
@@ -133,34 +147,28 @@ __global__ void __launch_bounds__(256)
     const long long nwarps = static_cast<long long>(gridDim.x) * blockDim.x / 32;
     const int pairs = K / 2;
     for (long long row = warp0; row < rows; row += nwarps) {
-        const double mean = means ? means[row] : 0.0;
-        const double neg = -mean;
+        const double neg = means ? -means[row] : -0.0;
+        const double s = kScale ? scales[row / nx_i] : 1.0;
         double2* p = reinterpret_cast<double2*>(q + static_cast<size_t>(row) * ld);
-        if (scales) {
-            const double s = scales[row / nx_i];
-#pragma unroll 4
-            for (int c = lane; c < pairs; c += 32) {
-                double2 v = p[c];
-                v.x = (v.x + neg) / s;
-                v.y = (v.y + neg) / s;
-                p[c] = v;
+        for (int c = lane; c < pairs; c += 32 * kApplyBatch) {
+            double2 v[kApplyBatch];
+#pragma unroll
+            for (int u = 0; u < kApplyBatch; ++u) {
+                if (c + 32 * u < pairs) v[u] = __ldcs(p + c + 32 * u);
             }
-            if ((K & 1) && lane == 0) {
-                double* last = q + static_cast<size_t>(row) * ld + (K - 1);
-                *last = (*last + neg) / s;
+#pragma unroll
+            for (int u = 0; u < kApplyBatch; ++u) {
+                if (c + 32 * u < pairs) {
+                    double2 w;
+                    w.x = kScale ? (v[u].x + neg) / s : v[u].x + neg;
+                    w.y = kScale ? (v[u].y + neg) / s : v[u].y + neg;
+                    __stcs(p + c + 32 * u, w);
+                }
             }
-        } else {
-#pragma unroll 4
-            for (int c = lane; c < pairs; c += 32) {
-                double2 v = p[c];
-                v.x = v.x + neg;
-                v.y = v.y + neg;
-                p[c] = v;
-            }
-            if ((K & 1) && lane == 0) {
-                double* last = q + static_cast<size_t>(row) * ld + (K - 1);
-                *last = *last + neg;
-            }
+        }
+        if ((K & 1) && lane == 0) {
+            double* last = q + static_cast<size_t>(row) * ld + (K - 1);
+            *last = kScale ? (*last + neg) / s : *last + neg;
         }
     }
 }
@@ -184,7 +192,11 @@ cudaError_t launch_apply(double* q, size_t ld, long long rows, int K, long long 
                          cudaStream_t stream) {
     const long long want = (rows + 7) / 8;
     const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(want, num_sms * 16LL)));
-    apply_kernel<<<grid, 256, 0, stream>>>(q, ld, rows, K, nx_i, means, scales);
+    if (scales) {
+        apply_kernel<true><<<grid, 256, 0, stream>>>(q, ld, rows, K, nx_i, means, scales);
+    } else {
+        apply_kernel<false><<<grid, 256, 0, stream>>>(q, ld, rows, K, nx_i, means, scales);
+    }
     note_launch();
     return cudaGetLastError();
 }

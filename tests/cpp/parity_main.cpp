@@ -1,0 +1,294 @@
+// parity_main.cpp — the drop-in, compiled against the reference's own headers
+// and library (oracle/_ref/libdopinf_ref.a, built from /root/reference) plus
+// libdopinf_b200.so through include/dopinf_b200.hpp. TEST INFRASTRUCTURE.
+//
+// It replays reference test scenarios with Steps II–III (and Φ_r / Q̂) swapped
+// for the B200 ones and checks them against the unmodified reference on the
+// same bytes, printing one PASS/FAIL line per check like
+// tests/acceptance.cpp. Exit status 0 iff all pass. Needs one B200.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "dopinf/comm.hpp"
+#include "dopinf/data.hpp"
+#include "dopinf/errors.hpp"
+#include "dopinf/linalg.hpp"
+#include "dopinf/pod.hpp"
+#include "dopinf/postprocess.hpp"
+#include "dopinf/rom_search.hpp"
+#include "dopinf/synth.hpp"
+#include "dopinf/transform.hpp"
+
+#define DOPINF_B200_REFERENCE_ERRORS 1
+#include "dopinf_b200.hpp"
+
+using namespace dopinf;
+
+namespace {
+
+int g_fail = 0;
+
+void report(bool ok, const std::string& name, const std::string& detail) {
+    std::printf("%s  %s  (%s)\n", ok ? "PASS" : "FAIL", name.c_str(), detail.c_str());
+    std::fflush(stdout);
+    if (!ok) ++g_fail;
+}
+
+std::string fmt(double v) {
+    char b[32];
+    std::snprintf(b, sizeof b, "%.3g", v);
+    return b;
+}
+
+Matrix random_matrix(synth::Rng& rng, std::size_t rows, std::size_t cols) {
+    Matrix m(rows, cols);
+    for (double& v : m.flat()) v = rng.normal();
+    return m;
+}
+
+data::LocalBlock whole(const Matrix& q, std::size_t nx) {
+    data::LocalBlock b;
+    b.row_range = {0, nx};
+    b.values = q;
+    return b;
+}
+
+data::SnapshotHeader header_for(std::size_t n_vars, std::size_t nx, std::size_t nt) {
+    data::SnapshotHeader h;
+    h.n_vars = n_vars;
+    h.nx = nx;
+    h.nt = nt;
+    for (std::size_t j = 0; j < n_vars; ++j) h.var_names.push_back("var" + std::to_string(j));
+    return h;
+}
+
+double rel_frob(const Matrix& a, const Matrix& b) {
+    double num = 0.0, den = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        num += (a.data()[i] - b.data()[i]) * (a.data()[i] - b.data()[i]);
+        den += b.data()[i] * b.data()[i];
+    }
+    return std::sqrt(num / std::max(den, 1e-300));
+}
+
+// Row-wise sign-folded gap relative to the row scale (acceptance.cpp:90-101).
+double sign_folded_rel(const Matrix& got, const Matrix& want) {
+    double worst = 0.0;
+    for (std::size_t i = 0; i < got.rows(); ++i) {
+        double d = 0, f = 0, s = 0;
+        for (std::size_t j = 0; j < got.cols(); ++j) {
+            d = std::max(d, std::abs(got(i, j) - want(i, j)));
+            f = std::max(f, std::abs(got(i, j) + want(i, j)));
+            s = std::max(s, std::abs(want(i, j)));
+        }
+        worst = std::max(worst, std::min(d, f) / std::max(s, 1e-300));
+    }
+    return worst;
+}
+
+// Steps II–III through the reference functions or the B200 ones, one rank.
+struct PassOut {
+    Matrix q, d;
+    std::vector<double> means, scales;
+};
+
+PassOut pass_reference(const Matrix& raw, std::size_t nv, std::size_t nx, bool scaling) {
+    PassOut o;
+    data::LocalBlock b = whole(raw, nx);
+    comm::run_on_workers(1, [&](comm::Comm& c) {
+        o.means = transform::center_in_place(b);
+        if (scaling) {
+            o.scales = transform::compute_global_scales(b, header_for(nv, nx, raw.cols()), c);
+            transform::scale_in_place(b, o.scales);
+        }
+        o.d = pod::global_gram(pod::local_gram(b), c);
+    });
+    o.q = b.values;
+    return o;
+}
+
+PassOut pass_b200(const Matrix& raw, std::size_t nv, std::size_t nx, bool scaling) {
+    PassOut o;
+    data::LocalBlock b = whole(raw, nx);
+    comm::run_on_workers(1, [&](comm::Comm& c) {
+        o.means = dopinf_b200::transform::center_in_place(b);
+        if (scaling) {
+            o.scales = dopinf_b200::transform::compute_global_scales(b, header_for(nv, nx, raw.cols()), c);
+            dopinf_b200::transform::scale_in_place(b, o.scales);
+        }
+        o.d = dopinf_b200::pod::global_gram(dopinf_b200::pod::local_gram(b), c);
+    });
+    o.q = b.values;
+    return o;
+}
+
+}  // namespace
+
+int main() {
+    std::printf("parity: reference pipeline stages vs dopinf_b200 drop-ins (1 B200)\n");
+    dopinf_b200::Context gpu(0);
+    dopinf_b200::Bind bind(gpu);
+
+    // 1. Step II on the reference's transform test data (test_transform.cpp:52-150), bitwise.
+    {
+        bool ok = true;
+        std::string detail;
+        for (auto [seed, nv, nx, nt] : std::vector<std::array<std::size_t, 4>>{
+                 {12, 1, 20, 7}, {8, 2, 15, 11}, {21, 2, 12, 9}, {77, 3, 40, 33}, {5, 4, 999, 130}}) {
+            synth::Rng rng(seed);
+            const Matrix raw = random_matrix(rng, nv * nx, nt);
+            const PassOut r = pass_reference(raw, nv, nx, true);
+            const PassOut g = pass_b200(raw, nv, nx, true);
+            ok = ok && r.q == g.q && r.means == g.means && r.scales == g.scales;
+            const double e = rel_frob(g.d, r.d);
+            ok = ok && e <= 1e-12;
+            detail += "seed " + std::to_string(seed) + " gram " + fmt(e) + "; ";
+        }
+        report(ok, "transform bit-identical, Gram rel <= 1e-12", detail + "means/scales/block bitwise");
+    }
+
+    // 2. Degenerate variable throws the reference class naming it (test_transform.cpp:115-128).
+    {
+        data::LocalBlock b = whole(Matrix(2, 3, {4, 4, 4, 1, 2, 3}), 1);
+        bool thrown = false;
+        comm::run_on_workers(1, [&](comm::Comm& c) {
+            dopinf_b200::transform::center_in_place(b);
+            try {
+                (void)dopinf_b200::transform::compute_global_scales(b, header_for(2, 1, 3), c);
+            } catch (const DegenerateVariableError& e) {
+                thrown = std::string(e.what()).find("var0") != std::string::npos;
+            }
+        });
+        report(thrown, "DegenerateVariableError names the variable", "dopinf::DegenerateVariableError");
+    }
+
+    // 3. acceptance.cpp sweep (20 shapes, seeds 1000+i): Gram vs the reference at
+    //    p in {1,2,4,7}; eig on the reference path; Q̂ and Φ_r rows vs the reference.
+    {
+        struct Shape {
+            std::size_t m, nt, rk;
+        };
+        const std::vector<Shape> shapes = {
+            {500, 50, 0}, {350, 40, 0}, {500, 13, 0}, {120, 30, 0}, {64, 24, 0}, {57, 23, 0}, {200, 50, 0},
+            {480, 36, 0}, {33, 20, 0}, {100, 12, 0}, {450, 48, 0}, {77, 31, 0}, {500, 50, 5}, {300, 30, 3},
+            {120, 40, 10}, {64, 16, 1}, {500, 24, 8}, {90, 45, 12}, {250, 50, 2}, {48, 12, 4}};
+        double gram_gap = 0, lam_gap = 0, qhat_gap = 0, rows_gap = 0, phi_gap = 0;
+        bool bitwise_proj = true;
+        for (std::size_t i = 0; i < shapes.size(); ++i) {
+            synth::Rng rng(1000 + i);
+            const Shape s = shapes[i];
+            Matrix q = s.rk == 0 ? random_matrix(rng, s.m, s.nt)
+                                 : linalg::matmul(random_matrix(rng, s.m, s.rk), random_matrix(rng, s.rk, s.nt));
+            const data::LocalBlock blk = whole(q, s.m);
+            Matrix dg;
+            comm::run_on_workers(1, [&](comm::Comm& c) {
+                dg = dopinf_b200::pod::global_gram(dopinf_b200::pod::local_gram(blk), c);
+            });
+            for (int p : {1, 2, 4, 7}) {
+                const auto plan = data::partition_rows(s.m, p);
+                Matrix dr;
+                comm::run_on_workers(p, [&](comm::Comm& c) {
+                    data::LocalBlock b;
+                    const auto rr = plan[static_cast<std::size_t>(c.rank())];
+                    b.row_range = rr;
+                    b.values = Matrix(rr.count(), s.nt);
+                    for (std::size_t k = 0; k < rr.count(); ++k)
+                        std::copy(q.row(rr.begin + k), q.row(rr.begin + k) + s.nt, b.values.row(k));
+                    Matrix d = pod::global_gram(pod::local_gram(b), c);
+                    if (c.rank() == 0) dr = d;
+                });
+                gram_gap = std::max(gram_gap, rel_frob(dg, dr));
+            }
+            const Matrix dref = linalg::gram(q);
+            const auto sg = pod::eig_sym_desc(dg);
+            const auto sr = pod::eig_sym_desc(dref);
+            for (std::size_t k = 0; k < sr.eigenvalues.size(); ++k)
+                lam_gap = std::max(lam_gap, std::abs(sg.eigenvalues[k] - sr.eigenvalues[k]) / sr.eigenvalues[0]);
+            std::size_t rank = 0;
+            for (double l : sr.eigenvalues) rank += std::sqrt(std::max(l, 0.0)) > 1e-8 * std::sqrt(sr.eigenvalues[0]);
+            const std::size_t r = std::min<std::size_t>(std::max<std::size_t>(rank, 1), 10);
+            const Matrix trr = pod::reduced_map(sr, r);
+            const Matrix trg = pod::reduced_map(sg, r);
+            // projection with the same inputs is bit-identical
+            bitwise_proj = bitwise_proj && dopinf_b200::pod::project(trr, dref) == pod::project(trr, dref);
+            // end to end (B200 D -> reference eig -> B200 Q̂) vs the reference chain
+            qhat_gap = std::max(qhat_gap, sign_folded_rel(dopinf_b200::pod::project(trg, dg), pod::project(trr, dref)));
+            std::vector<std::size_t> sel;
+            for (std::size_t k = 0; k < s.m; k += std::max<std::size_t>(1, s.m / 9)) sel.push_back(k);
+            const Matrix rg = dopinf_b200::postprocess::basis_rows(blk, trr, sel);
+            const Matrix rr_ = postprocess::basis_rows(blk, trr, sel);
+            rows_gap = std::max(rows_gap, rg == rr_ ? 0.0 : 1.0);
+            const Matrix pg = dopinf_b200::postprocess::basis(blk, trr);
+            phi_gap = std::max(phi_gap, rel_frob(pg, linalg::matmul(q, trr)));
+        }
+        report(gram_gap <= 1e-12, "sweep Gram vs reference p in {1,2,4,7}", "rel Frobenius " + fmt(gram_gap) + " <= 1e-12");
+        report(lam_gap <= 1e-10, "sweep eigenvalues (reference eig of B200 D)", "rel to lambda1 " + fmt(lam_gap) + " <= 1e-10");
+        report(bitwise_proj, "project bit-identical to pod::project", "20 shapes");
+        report(qhat_gap <= 1e-9, "sweep Q-hat end to end, sign-folded", fmt(qhat_gap) + " <= 1e-9");
+        report(rows_gap == 0.0, "basis_rows bit-identical to postprocess::basis_rows", "20 shapes");
+        report(phi_gap <= 1e-12, "Phi_r = Q T_r vs linalg::matmul", "rel Frobenius " + fmt(phi_gap));
+    }
+
+    // 4. Steps II-IV: B200 Steps II-III + reference eig/project/grid_search vs the
+    //    all-reference chain on a synthetic quadratic dataset (acceptance.cpp canonical spec).
+    {
+        synth::QuadraticSpec spec;
+        spec.n_vars = 2;
+        spec.nx = 400;
+        spec.r_true = 3;
+        spec.nt = 200;
+        spec.nt_p = 400;
+        spec.seed = 12;
+        const auto made = synth::make_quadratic(spec);
+        Matrix raw(spec.n_vars * spec.nx, spec.nt);
+        for (std::size_t v = 0; v < spec.n_vars; ++v)
+            for (std::size_t i = 0; i < spec.nx; ++i)
+                for (std::size_t t = 0; t < spec.nt; ++t) raw(v * spec.nx + i, t) = made.variables[v](i, t);
+        double traj_gap = 0, err_gap = 0, lam_gap = 0;
+        bool pair_same = true;
+        std::size_t r_ref = 0, r_gpu = 0;
+        for (bool scaling : {false, true}) {
+            const PassOut r = pass_reference(raw, spec.n_vars, spec.nx, scaling);
+            const PassOut g = pass_b200(raw, spec.n_vars, spec.nx, scaling);
+            const auto sr = pod::eig_sym_desc(r.d), sg = pod::eig_sym_desc(g.d);
+            r_ref = pod::select_rank(sr.eigenvalues, 0.9995).r;
+            r_gpu = pod::select_rank(sg.eigenvalues, 0.9995).r;
+            for (std::size_t k = 0; k < sr.eigenvalues.size(); ++k)
+                lam_gap = std::max(lam_gap, std::abs(sg.eigenvalues[k] - sr.eigenvalues[k]) / sr.eigenvalues[0]);
+            const Matrix qr = pod::project(pod::reduced_map(sr, r_ref), r.d);
+            const Matrix qg = dopinf_b200::pod::project(pod::reduced_map(sg, r_gpu), g.d);
+            rom_search::SearchConfig cfg{rom_search::default_b1(), rom_search::default_b2(), 1.2, spec.nt_p};
+            rom_search::SearchOutcome orf, ogp;
+            comm::run_on_workers(1, [&](comm::Comm& c) {
+                orf = rom_search::grid_search(qr, cfg, c);
+                ogp = rom_search::grid_search(qg, cfg, c);
+            });
+            pair_same = pair_same && r_ref == r_gpu && orf.pair_opt.beta1 == ogp.pair_opt.beta1 &&
+                        orf.pair_opt.beta2 == ogp.pair_opt.beta2;
+            err_gap = std::max(err_gap, std::abs(orf.train_err - ogp.train_err) / orf.train_err);
+            // trajectories: per-mode sign normalisation (columns are POD coordinates)
+            double num = 0, den = 0;
+            for (std::size_t k = 0; k < orf.trajectory.cols(); ++k) {
+                double dp = 0, dm = 0;
+                for (std::size_t t = 0; t < orf.trajectory.rows(); ++t) {
+                    dp += std::pow(ogp.trajectory(t, k) - orf.trajectory(t, k), 2);
+                    dm += std::pow(ogp.trajectory(t, k) + orf.trajectory(t, k), 2);
+                    den += orf.trajectory(t, k) * orf.trajectory(t, k);
+                }
+                num += std::min(dp, dm);
+            }
+            traj_gap = std::max(traj_gap, std::sqrt(num / den));
+        }
+        report(lam_gap <= 1e-10, "pipeline eigenvalues", "rel to lambda1 " + fmt(lam_gap) + " <= 1e-10");
+        report(pair_same, "pipeline r and optimal (beta1, beta2) identical", "r = " + std::to_string(r_gpu));
+        report(err_gap <= 1e-8, "pipeline training error", "rel " + fmt(err_gap) + " <= 1e-8");
+        report(traj_gap <= 1e-8, "ROM prediction over 2x horizon", "rel " + fmt(traj_gap) + " <= 1e-8");
+    }
+
+    std::printf("parity: %s\n", g_fail == 0 ? "all checks passed" : "FAILURES");
+    return g_fail == 0 ? 0 : 1;
+}
