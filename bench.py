@@ -299,8 +299,7 @@ def run_ours(args, wl):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            block.upload_ptr(host.data_ptr(), nt)
-            api.snapshot_pass(block, scaling=True, out=outs)
+            api.snapshot_pass_host(block, host.data_ptr(), scaling=True, out=outs, host_ld=nt)
             api.project_resident(ctx, tr, out=qhat_out)
         e1.record(stream)
         torch.cuda.synchronize(local)
@@ -309,8 +308,8 @@ def run_ours(args, wl):
                "h2d_bytes_per_step": int(8 * n_total * nt + 8 * nt * r),
                "d2h_bytes_per_step": int(world * (8 * nt * nt + 8 * r * nt + 8 * n_local + 8 * nv)),
                "ms_per_step": round(e2e_ms / args.steps, 3),
-               "path": "pinned host -> dopinf_b200_block_upload -> dopinf_b200_snapshot_pass -> "
-                       "dopinf_b200_project (D and Q̂ back to host)"}
+               "path": "pinned host -> dopinf_b200_snapshot_pass_host (chunked H2D overlapped with "
+                       "transform + Gram) -> dopinf_b200_project (D and Q̂ back to pinned host)"}
         del host
 
     cpu = None

@@ -83,7 +83,8 @@ typedef enum dopinf_b200_stage {
     DOPINF_B200_STAGE_PROJECT = 8,    /* Q̂ = T_rᵀ D                             */
     DOPINF_B200_STAGE_BASIS = 9,      /* Φ_r = Q T_r                            */
     DOPINF_B200_STAGE_DOWNLOAD = 10,
-    DOPINF_B200_STAGE_COUNT = 11
+    DOPINF_B200_STAGE_STREAM = 11,    /* whole streamed pass (first H2D -> D ready) */
+    DOPINF_B200_STAGE_COUNT = 12
 } dopinf_b200_stage;
 
 typedef struct dopinf_b200_ctx dopinf_b200_ctx;
@@ -187,6 +188,18 @@ int dopinf_b200_basis_rows(dopinf_b200_block* block, const double* tr, size_t r,
  * means [rows], scales [n_vars], d [nt x nt]: host, each may be NULL. */
 int dopinf_b200_snapshot_pass(dopinf_b200_block* block, int scaling, double* means,
                               double* scales, double* d);
+/* The same Steps II-III with the block's values arriving from HOST memory
+ * (row-major, pitch host_ld): rows stream in chunks on a copy stream while the
+ * compute stream centers each landed chunk and accumulates its Gram; scaling
+ * is folded into the Gram (D = Σ_v G_v / s_v², G_v the Gram of variable v's
+ * centered rows) so no pass waits for the global scales, and each variable is
+ * scaled as soon as its MAX is final. The block ends resident and transformed
+ * exactly as dopinf_b200_snapshot_pass leaves it (bit-identical values, means
+ * and scales; D within the same tolerance). Host memory should be pinned for
+ * the copies to overlap. On DegenerateVariableError, variables finished before
+ * the degenerate one are left scaled. */
+int dopinf_b200_snapshot_pass_host(dopinf_b200_block* block, const double* host, size_t host_ld,
+                                   int scaling, double* means, double* scales, double* d);
 
 #ifdef __cplusplus
 }

@@ -385,5 +385,26 @@ def snapshot_pass(block: LocalBlock, scaling: bool, out: dict | None = None):
     return params, d
 
 
+def snapshot_pass_host(block: LocalBlock, host_values, scaling: bool, out: dict | None = None,
+                       host_ld: int | None = None):
+    """snapshot_pass with the block's values streamed in from HOST memory
+    (`host_values`: a (rows × nt) float64 array, or a raw pointer int with
+    `host_ld`), chunk H2D overlapping the transform and Gram of landed chunks.
+    Leaves the block resident and transformed; returns (TransformParams, D)."""
+    out = out or {}
+    if isinstance(host_values, int):
+        ptr, ld = C.cast(host_values, _lib._dp), int(host_ld or block.nt)
+    else:
+        hv = _f64(host_values, (block.rows, block.nt))
+        ptr, ld = _lib.dptr(hv), block.nt
+    means = _out(out["means"], (block.rows,)) if "means" in out else np.empty(block.rows, dtype=np.float64)
+    scales = _out(out["scales"], (block.n_vars,)) if "scales" in out else np.empty(block.n_vars, dtype=np.float64)
+    d = _out(out["d"], (block.nt, block.nt)) if "d" in out else np.empty((block.nt, block.nt), dtype=np.float64)
+    rc = _lib.load().dopinf_b200_snapshot_pass_host(block._h, ptr, ld, 1 if scaling else 0, _lib.dptr(means),
+                                                    _lib.dptr(scales), _lib.dptr(d))
+    _check(rc, block.ctx, "snapshot_pass_host")
+    return TransformParams(means, scales if scaling else np.zeros(0), scaling), d
+
+
 def kernel_launches() -> int:
     return int(_lib.load().dopinf_b200_kernel_launches())

@@ -101,6 +101,34 @@ def build_oracle(with_reference: bool | None = None) -> None:
             raise RuntimeError(f"reference oracle build failed:\n{res.stdout}\n{res.stderr}")
 
 
+def build_parity_harness() -> Path | None:
+    """tests/cpp/_build/parity: the C++ drop-in compiled against the reference's
+    headers and oracle/_ref/libdopinf_ref.a (test infrastructure; needs the
+    reference sources, so it is built here and travels as a binary)."""
+    ref_src = Path(os.environ.get("DOPINF_REFERENCE", "/root/reference/proj"))
+    lib_ref = ROOT / "oracle" / "_ref" / "libdopinf_ref.a"
+    if not (ref_src / "include" / "dopinf" / "pod.hpp").exists() or not lib_ref.exists():
+        return None
+    import scipy
+
+    blas = Path(scipy.__file__).resolve().parent.parent / "scipy.libs"
+    blas_lib = next(blas.glob("libscipy_openblas*.so"))
+    out = ROOT / "tests" / "cpp" / "_build" / "parity"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    src = ROOT / "tests" / "cpp" / "parity_main.cpp"
+    if not _stale(out, [src, LIB, ROOT / "include" / "dopinf_b200.hpp", lib_ref]):
+        return out
+    cmd = ["g++", "-std=gnu++20", "-O2", f"-I{ROOT / 'oracle' / 'shim'}", f"-I{ref_src / 'include'}",
+           f"-I{ROOT / 'include'}", str(src), str(lib_ref), f"-L{PKG}", "-ldopinf_b200",
+           "-Wl,-rpath,$ORIGIN/../../../paper_2504_14338_b200", f"-L{blas}", f"-l:{blas_lib.name}", f"-Wl,-rpath,{blas}", "-lpthread",
+           "-o", str(out)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"parity harness build failed:\n{res.stderr}")
+    return out
+
+
 if __name__ == "__main__":
     print(build_extension(verbose=True))
     build_oracle()
+    print(build_parity_harness())

@@ -138,6 +138,9 @@ struct dopinf_b200_ctx {
     int device = 0, rank = 0, size = 1;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;    // streamed pass: H2D of chunk c+1 overlaps chunk c
+    std::vector<cudaEvent_t> chunk_events;  // one per streamed chunk (grow-only)
+    DBuf gv;                                // per-variable packed Grams of the streamed pass
     ncclComm_t comm = nullptr;
     int gram_reduce = DOPINF_B200_GRAM_REDUCE_ORDERED;
     std::string err;
@@ -316,6 +319,24 @@ void unpack(dopinf_b200_ctx* c) {
     c->record(DOPINF_B200_STAGE_UNPACK, 1);
 }
 
+void ensure_tiles(dopinf_b200_ctx* c, int K) {
+    if (c->tiles_K == K) return;
+    const std::vector<gram::TileInfo> t = gram::plan_tiles(K);
+    ck(cudaMemcpy(c->tiles.get<gram::TileInfo>(t.size(), "tiles"), t.data(), t.size() * sizeof(gram::TileInfo),
+                  cudaMemcpyHostToDevice),
+       "tiles H2D");
+    c->tiles_K = K;
+}
+
+int* ensure_counters(dopinf_b200_ctx* c) {
+    int* counters = c->counters.get<int>(2, "counters");
+    if (!c->counters_zeroed) {
+        ck(cudaMemsetAsync(counters, 0, 2 * sizeof(int), c->stream), "memset");
+        c->counters_zeroed = true;
+    }
+    return counters;
+}
+
 void do_local_gram(dopinf_b200_block* b, double* d_host) {
     auto* c = b->ctx;
     materialize(b);
@@ -327,13 +348,7 @@ void do_local_gram(dopinf_b200_block* b, double* d_host) {
     if (rows == 0) {
         ck(cudaMemsetAsync(packed, 0, gram::packed_count(K) * sizeof(double), c->stream), "memset");
     } else {
-        if (c->tiles_K != K) {
-            const std::vector<gram::TileInfo> t = gram::plan_tiles(K);
-            ck(cudaMemcpy(c->tiles.get<gram::TileInfo>(t.size(), "tiles"), t.data(),
-                          t.size() * sizeof(gram::TileInfo), cudaMemcpyHostToDevice),
-               "tiles H2D");
-            c->tiles_K = K;
-        }
+        ensure_tiles(c, K);
         if (c->plan_K != K || c->plan_rows != rows) {
             size_t free_b = 0, total_b = 0;
             cudaMemGetInfo(&free_b, &total_b);
@@ -347,11 +362,7 @@ void do_local_gram(dopinf_b200_block* b, double* d_host) {
             ck(gram::make_tensor_map(&b->gram_map, b->q, rows, K, b->ld), "tensor map");
             b->gram_map_base = b->q;
         }
-        int* counters = c->counters.get<int>(2, "counters");
-        if (!c->counters_zeroed) {
-            ck(cudaMemsetAsync(counters, 0, 2 * sizeof(int), c->stream), "memset");
-            c->counters_zeroed = true;
-        }
+        int* counters = ensure_counters(c);
         double* work = c->work.get<double>(c->plan.workspace_doubles, "workspace");
         const auto* tiles = c->tiles.get<gram::TileInfo>(c->plan.n_tiles, "tiles");
         c->record(DOPINF_B200_STAGE_GRAM, 0);
@@ -385,6 +396,140 @@ void do_global_gram(dopinf_b200_ctx* c, double* d_host) {
         unpack(c);
     }
     copy_d_out(c, d_host);
+}
+
+// ---- streamed Steps II-III (dopinf_b200_snapshot_pass_host) ------------------------
+constexpr long long kStreamChunkRows = 32768;  // rows per H2D chunk (315 MB at K = 1200)
+constexpr long long kStreamSplitRows = 2048;   // rows per Gram item inside a chunk
+
+struct StreamChunk {
+    int var;
+    long long r0, rows;
+    bool first_of_var, last_of_var;
+};
+
+std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b) {
+    std::vector<StreamChunk> out;
+    for (size_t v = 0; v < b->n_vars; ++v) {
+        const long long v0 = static_cast<long long>(v * b->nx_i), v1 = v0 + static_cast<long long>(b->nx_i);
+        for (long long r0 = v0; r0 < v1; r0 += kStreamChunkRows) {
+            const long long rows = std::min(kStreamChunkRows, v1 - r0);
+            out.push_back({static_cast<int>(v), r0, rows, r0 == v0, r0 + rows == v1});
+        }
+    }
+    return out;
+}
+
+// Chunks of rows land on the copy stream; on the compute stream each landed
+// chunk gets its row means / max-abs (stats pass), is centered in place, and
+// its Gram items accumulate (chunk order) into the split slots of its
+// variable. When a variable's last chunk is done its slots are reduced into
+// G_v, its MAX goes over the ranks, and its rows are scaled. D = Σ_v G_v/s_v².
+void do_stream_pass(dopinf_b200_block* b, const double* host, size_t host_ld, bool scaling, double* means_host,
+                    double* scales_host) {
+    auto* c = b->ctx;
+    const int K = static_cast<int>(b->nt);
+    const size_t count = gram::packed_count(K);
+    b->pending_center = false;
+    b->stats_valid = false;
+    c->have_gram = false;
+    c->K = K;
+    const std::vector<StreamChunk> chunks = stream_chunks(b);
+    while (c->chunk_events.size() < chunks.size()) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        c->chunk_events.push_back(e);
+    }
+    ensure_tiles(c, K);
+    int* counters = ensure_counters(c);
+    const auto* tiles = c->tiles.get<gram::TileInfo>(gram::plan_tiles(K).size(), "tiles");
+    const long long first_rows = std::min<long long>(kStreamChunkRows, static_cast<long long>(b->nx_i));
+    const gram::Plan full = gram::make_stream_plan(std::max<long long>(first_rows, 1), K, c->num_sms,
+                                                   kStreamSplitRows);
+    double* work = c->work.get<double>(full.workspace_doubles, "workspace");
+    double* gv = c->gv.get<double>(count * b->n_vars, "per-variable Grams");
+    double* vm = b->varmax.get<double>(b->n_vars, "varmax");
+    double* ds = c->scales.get<double>(b->n_vars, "scales");
+    double* mn = b->means.get<double>(std::max<size_t>(b->rows, 1), "means");
+    double* packed = c->packed.get<double>(count, "packed");
+
+    c->record(DOPINF_B200_STAGE_STREAM, 0);
+    ck(cudaMemsetAsync(vm, 0, b->n_vars * sizeof(double), c->stream), "memset");
+    ck(cudaMemsetAsync(gv, 0, count * b->n_vars * sizeof(double), c->stream), "memset");
+    // The copy stream must not overwrite the block before earlier work on it is done.
+    cudaEvent_t ready = c->chunk_events[0];
+    ck(cudaEventRecord(ready, c->stream), "event");
+    ck(cudaStreamWaitEvent(c->copy_stream, ready, 0), "event wait");
+    for (size_t k = 0; k < chunks.size(); ++k) {
+        const StreamChunk& ch = chunks[k];
+        ck(cudaMemcpy2DAsync(b->q + ch.r0 * b->ld, b->ld * sizeof(double), host + ch.r0 * host_ld,
+                             host_ld * sizeof(double), b->nt * sizeof(double), ch.rows, cudaMemcpyHostToDevice,
+                             c->copy_stream),
+           "chunk H2D");
+        ck(cudaEventRecord(c->chunk_events[k], c->copy_stream), "event");
+    }
+    gram::Plan first_plan = full;
+    for (size_t k = 0; k < chunks.size(); ++k) {
+        const StreamChunk& ch = chunks[k];
+        ck(cudaStreamWaitEvent(c->stream, c->chunk_events[k], 0), "event wait");
+        double* qk = b->q + ch.r0 * b->ld;
+        // chunk = one variable's rows: present it to the kernels as a 1-variable block
+        ck(transform::launch_stats(qk, b->ld, ch.rows, K, ch.rows, 1, true, mn + ch.r0, vm + ch.var, c->num_sms,
+                                   c->stream),
+           "stats");
+        ck(transform::launch_apply(qk, b->ld, ch.rows, K, ch.rows, mn + ch.r0, nullptr, c->num_sms, c->stream),
+           "center");
+        CUtensorMap map;
+        ck(gram::make_tensor_map(&map, qk, ch.rows, K, b->ld), "tensor map");
+        const gram::Plan plan = gram::make_stream_plan(ch.rows, K, c->num_sms, kStreamSplitRows);
+        if (ch.first_of_var) first_plan = plan;
+        ck(gram::launch_gram(plan, map, tiles, work, counters, c->stream, !ch.first_of_var), "gram");
+        if (ch.last_of_var) {
+            ck(gram::launch_reduce(first_plan, tiles, work, gv + static_cast<size_t>(ch.var) * count, c->stream),
+               "gram reduce");
+            if (scaling) {
+                if (c->size > 1) {
+                    ckn(ncclAllReduce(vm + ch.var, ds + ch.var, 1, ncclFloat64, ncclMax, c->comm, c->stream),
+                        "allreduce(MAX)");
+                } else {
+                    ck(cudaMemcpyAsync(ds + ch.var, vm + ch.var, sizeof(double), cudaMemcpyDeviceToDevice,
+                                       c->stream),
+                       "copy");
+                }
+                const long long v0 = static_cast<long long>(ch.var) * static_cast<long long>(b->nx_i);
+                ck(transform::launch_apply(b->q + v0 * b->ld, b->ld, static_cast<long long>(b->nx_i), K,
+                                           static_cast<long long>(b->nx_i), nullptr, ds + ch.var, c->num_sms,
+                                           c->stream),
+                   "scale");
+            }
+        }
+    }
+    if (b->rows == 0 && scaling) {  // an empty rank still joins the MAX collectives
+        for (size_t v = 0; v < b->n_vars; ++v) {
+            if (c->size > 1) {
+                ckn(ncclAllReduce(vm + v, ds + v, 1, ncclFloat64, ncclMax, c->comm, c->stream), "allreduce(MAX)");
+            } else {
+                ck(cudaMemcpyAsync(ds + v, vm + v, sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
+            }
+        }
+    }
+    ck(gram::launch_combine_vars(gv, static_cast<int>(b->n_vars), count, scaling ? ds : nullptr, packed,
+                                 c->stream),
+       "combine");
+    c->record(DOPINF_B200_STAGE_STREAM, 1);
+    c->have_gram = true;
+    if (means_host && b->rows > 0) c->d2h(means_host, mn, b->rows * sizeof(double), "means D2H");
+    if (scaling) {
+        std::vector<double> s(b->n_vars);
+        c->d2h(s.data(), ds, b->n_vars * sizeof(double), "scales D2H");
+        if (scales_host) std::memcpy(scales_host, s.data(), s.size() * sizeof(double));
+        for (size_t j = 0; j < b->n_vars; ++j) {
+            if (s[j] == 0.0) {
+                fail(DOPINF_B200_ERR_DEGENERATE_VARIABLE,
+                     "variable " + std::to_string(j) + " is constant in time; max-abs scaling is undefined");
+            }
+        }
+    }
 }
 
 void do_project(dopinf_b200_ctx* c, const double* tr_host, const double* d_dev, size_t nt, size_t r,
@@ -457,6 +602,7 @@ int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* 
         }
         c->num_sms = prop.multiProcessorCount;
         ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         for (auto& pair : c->ev) {
             ck(cudaEventCreate(&pair[0]), "cudaEventCreate");
             ck(cudaEventCreate(&pair[1]), "cudaEventCreate");
@@ -492,6 +638,12 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
         b->release();
     }
     c->staging.release();
+    c->gv.release();
+    for (cudaEvent_t e : c->chunk_events) cudaEventDestroy(e);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamDestroy(c->copy_stream);
+    }
     if (c->stream) cudaStreamDestroy(c->stream);
     cudaSetDevice(prev);
     delete c;
@@ -842,6 +994,19 @@ int dopinf_b200_snapshot_pass(dopinf_b200_block* b, int scaling, double* means, 
         do_local_gram(b, nullptr);
         do_global_gram(c, d);
         c->sync("snapshot_pass");
+    });
+}
+
+int dopinf_b200_snapshot_pass_host(dopinf_b200_block* b, const double* host, size_t host_ld, int scaling,
+                                   double* means, double* scales, double* d) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(host_ld >= b->nt && (b->rows == 0 || host), "snapshot_pass_host: bad host buffer");
+        do_stream_pass(b, host, host_ld, scaling != 0, means, scales);
+        unpack(c);
+        do_global_gram(c, d);
+        c->sync("snapshot_pass_host");
     });
 }
 

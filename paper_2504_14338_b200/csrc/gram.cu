@@ -99,7 +99,7 @@ __device__ __forceinline__ void stage_mma(double (&acc)[16][2], const double* __
 __global__ void __launch_bounds__(THREADS, 1)
     gram_dmma_kernel(const __grid_constant__ CUtensorMap tmap, const TileInfo* __restrict__ tiles,
                      int n_tiles, int n_items, long long n_rows, int chunk_rows,
-                     double* __restrict__ work, int* __restrict__ counters) {
+                     double* __restrict__ work, int* __restrict__ counters, int accumulate) {
     extern __shared__ unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -194,8 +194,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                             lane * 2;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    if ((mask >> i) & 1u) __stcg(reinterpret_cast<double2*>(w + i * 64),
-                                                 make_double2(acc[i][0], acc[i][1]));
+                    if ((mask >> i) & 1u) {
+                        double2* p = reinterpret_cast<double2*>(w + i * 64);
+                        double2 v = make_double2(acc[i][0], acc[i][1]);
+                        if (accumulate) {  // streamed chunks: slot += this chunk's partial, chunk order
+                            const double2 old = __ldcg(p);
+                            v.x = old.x + v.x;
+                            v.y = old.y + v.y;
+                        }
+                        __stcg(p, v);
+                    }
                     acc[i][0] = acc[i][1] = 0.0;
                 }
             }
@@ -264,6 +272,21 @@ __global__ void unpack_kernel(const double* __restrict__ packed, int K, double* 
         const size_t i = e / K, j = e % K;
         const size_t r = i < j ? i : j, c = i < j ? j : i;
         d[e] = packed[r * (2 * static_cast<size_t>(K) - r + 1) / 2 + (c - r)];
+    }
+}
+
+// Streamed pass: D = Σ_v G_v / (s_v·s_v) over the per-variable Grams of the
+// centered rows, variables in order (scales == nullptr: plain Σ_v G_v).
+__global__ void combine_vars_kernel(const double* __restrict__ gv, int n_vars, size_t count,
+                                    const double* __restrict__ scales, double* __restrict__ out) {
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < count;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        for (int v = 0; v < n_vars; ++v) {
+            const double g = gv[static_cast<size_t>(v) * count + e];
+            acc += scales ? g / (scales[v] * scales[v]) : g;
+        }
+        out[e] = acc;
     }
 }
 
@@ -395,12 +418,35 @@ cudaError_t make_tensor_map(CUtensorMap* map, const double* q, long long n_rows,
 size_t smem_bytes() { return sizeof(Smem) + 1024; }
 
 cudaError_t launch_gram(const Plan& plan, const CUtensorMap& map, const TileInfo* d_tiles,
-                        double* work, int* counters, cudaStream_t stream) {
+                        double* work, int* counters, cudaStream_t stream, bool accumulate) {
     const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(gram_dmma_kernel),
                                              static_cast<int>(smem_bytes()));
     if (e != cudaSuccess) return e;
     gram_dmma_kernel<<<plan.grid, THREADS, smem_bytes(), stream>>>(
-        map, d_tiles, plan.n_tiles, plan.n_items, plan.n_rows, plan.chunk_rows, work, counters);
+        map, d_tiles, plan.n_tiles, plan.n_items, plan.n_rows, plan.chunk_rows, work, counters,
+        accumulate ? 1 : 0);
+    note_launch();
+    return cudaGetLastError();
+}
+
+Plan make_stream_plan(long long chunk_rows, int K, int num_sms, long long split_rows) {
+    Plan p;
+    p.K = K;
+    p.n_rows = chunk_rows;
+    p.n_tiles = static_cast<int>(plan_tiles(K).size());
+    const long long split = std::max<long long>(BK, (split_rows + BK - 1) / BK * BK);
+    p.chunk_rows = static_cast<int>(split);
+    p.n_splits = static_cast<int>(std::max<long long>(1, (chunk_rows + split - 1) / split));
+    p.n_items = p.n_splits * p.n_tiles;
+    p.grid = std::min(num_sms, p.n_items);
+    p.workspace_doubles = static_cast<size_t>(p.n_items) * kItemDoubles;
+    return p;
+}
+
+cudaError_t launch_combine_vars(const double* gv, int n_vars, size_t count, const double* scales,
+                                double* out, cudaStream_t stream) {
+    const int grid = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 16));
+    combine_vars_kernel<<<std::max(grid, 1), 256, 0, stream>>>(gv, n_vars, count, scales, out);
     note_launch();
     return cudaGetLastError();
 }

@@ -42,7 +42,13 @@ Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes)
 cudaError_t make_tensor_map(CUtensorMap* map, const double* q, long long n_rows, int K, size_t ld);
 size_t smem_bytes();
 cudaError_t launch_gram(const Plan& plan, const CUtensorMap& map, const TileInfo* d_tiles,
-                        double* work, int* counters, cudaStream_t stream);
+                        double* work, int* counters, cudaStream_t stream, bool accumulate = false);
+// Plan for one streamed chunk of `chunk_rows` rows cut into splits of
+// `split_rows`; its items accumulate into the same split slots chunk after chunk.
+Plan make_stream_plan(long long chunk_rows, int K, int num_sms, long long split_rows);
+// D = Σ_v gv[v] / scales[v]² (scales == nullptr: Σ_v gv[v]), variables in order.
+cudaError_t launch_combine_vars(const double* gv, int n_vars, size_t count, const double* scales,
+                                double* out, cudaStream_t stream);
 cudaError_t launch_reduce(const Plan& plan, const TileInfo* d_tiles, const double* work,
                           double* packed, cudaStream_t stream);
 cudaError_t launch_unpack(const double* packed, int K, double* d, cudaStream_t stream);

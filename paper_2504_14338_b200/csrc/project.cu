@@ -3,15 +3,17 @@
 //  * project_kernel: Q̂ = T_rᵀ D (pod::project → linalg::matmul_tn,
 //    pod.cpp:103-105, linalg.cpp:28-37). Each output is the reference's FMA
 //    chain over l = 0..K−1 in order (c[i][j] = fma(T_r[l][i], D[l][j], c)), so
-//    Q̂ is bit-identical to the reference's for the same T_r and D.
+//    Q̂ is bit-identical to the reference's for the same T_r and D. D and T_r
+//    slabs are staged through shared memory so the chains run at FMA latency.
 //  * basis_rows_kernel: postprocess::basis_rows (postprocess.cpp:12-34), the
 //    reference's unfused acc + q·tr loop in order → bit-identical.
 //  * basis_dmma_kernel: Φ_r = Q·T_r (postprocess.cpp:66 reconstruct_field's
 //    linalg::matmul), a tall-skinny GEMM on the FP64 tensor pipe. Q row-slabs
-//    (128 rows × 16 snapshots) and the matching slab of T_rᵀ stream through a
+//    (BM rows × 16 snapshots) and the matching slab of T_rᵀ stream through a
 //    TMA ring with 128-byte swizzle; consumers read both operands with
 //    conflict-free 128-bit shared loads (two k-steps per load) and run
-//    DMMA.8x8x4. Q is read from HBM exactly once for r <= 128.
+//    DMMA.8x8x4. One CTA covers all r columns (padded to a multiple of 8 only),
+//    so Q is read from HBM exactly once.
 #include <algorithm>
 
 #include <cudaTypedefs.h>
@@ -24,30 +26,46 @@ namespace project {
 
 namespace {
 
-constexpr int kProjRowsPerThread = 2;
-constexpr int kProjThreads = 64;
+// ---- Q̂ = T_rᵀ D, reference order ---------------------------------------------
+constexpr int kPjCols = 32;   // columns j per block (one warp = 32 consecutive j)
+constexpr int kPjRows = 4;    // rows i per thread (independent FMA chains)
+constexpr int kPjWarps = 4;   // row groups per block → 16 rows of Q̂ per block
+constexpr int kPjL = 64;      // l-slab staged in shared memory
 
-// One thread per (2 rows of Q̂, column j): two independent in-order FMA chains
-// over l; D[l][j] coalesced across the block, T_r[l][i] broadcast. The chain
-// latency (K dependent DFMAs) bounds the kernel, so the grid is made wide.
-__global__ void __launch_bounds__(kProjThreads)
+__global__ void __launch_bounds__(kPjCols * kPjWarps)
     project_kernel(const double* __restrict__ tr, const double* __restrict__ d, int K, int r,
                    double* __restrict__ qhat) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i0 = blockIdx.y * kProjRowsPerThread;
-    if (j >= K) return;
-    double acc0 = 0.0, acc1 = 0.0;
-    const bool two = i0 + 1 < r;
-    const double* dj = d + j;
-    const double* trl = tr + i0;
-#pragma unroll 8
-    for (int l = 0; l < K; ++l) {
-        const double dv = __ldg(dj + static_cast<size_t>(l) * K);
-        acc0 = fma(__ldg(trl + static_cast<size_t>(l) * r), dv, acc0);
-        if (two) acc1 = fma(__ldg(trl + static_cast<size_t>(l) * r + 1), dv, acc1);
+    __shared__ double ds[kPjL][kPjCols];
+    __shared__ double ts[kPjL][kPjRows * kPjWarps];
+    const int lane = threadIdx.x % 32, wg = threadIdx.x / 32;
+    const int j0 = blockIdx.x * kPjCols, i0 = blockIdx.y * kPjRows * kPjWarps;
+    const int j = j0 + lane;
+    double acc[kPjRows] = {0.0, 0.0, 0.0, 0.0};
+    for (int l0 = 0; l0 < K; l0 += kPjL) {
+        const int nl = min(kPjL, K - l0);
+        for (int e = threadIdx.x; e < kPjL * kPjCols; e += blockDim.x) {
+            const int l = e / kPjCols, c = e % kPjCols;
+            ds[l][c] = (l < nl && j0 + c < K) ? d[static_cast<size_t>(l0 + l) * K + j0 + c] : 0.0;
+        }
+        for (int e = threadIdx.x; e < kPjL * kPjRows * kPjWarps; e += blockDim.x) {
+            const int l = e / (kPjRows * kPjWarps), c = e % (kPjRows * kPjWarps);
+            ts[l][c] = (l < nl && i0 + c < r) ? tr[static_cast<size_t>(l0 + l) * r + i0 + c] : 0.0;
+        }
+        __syncthreads();
+        for (int l = 0; l < nl; ++l) {
+            const double dv = ds[l][lane];
+#pragma unroll
+            for (int k = 0; k < kPjRows; ++k) acc[k] = fma(ts[l][wg * kPjRows + k], dv, acc[k]);
+        }
+        __syncthreads();
     }
-    qhat[static_cast<size_t>(i0) * K + j] = acc0;
-    if (two) qhat[static_cast<size_t>(i0 + 1) * K + j] = acc1;
+    if (j < K) {
+#pragma unroll
+        for (int k = 0; k < kPjRows; ++k) {
+            const int i = i0 + wg * kPjRows + k;
+            if (i < r) qhat[static_cast<size_t>(i) * K + j] = acc[k];
+        }
+    }
 }
 
 __global__ void basis_rows_kernel(const double* __restrict__ q, size_t ld, int K,
@@ -64,18 +82,26 @@ __global__ void basis_rows_kernel(const double* __restrict__ q, size_t ld, int K
 }
 
 // ---- Φ_r = Q · T_r on DMMA ---------------------------------------------------
-constexpr int BM = 128;     // rows of Q per CTA tile
+// Warp grid WM × WN (8 consumer warps); warp tile 32 rows × 8·NT columns.
+// CTA tile BM = 32·WM rows × BN = 8·NT·WN columns.
 constexpr int BKB = 16;     // snapshots per stage (128 B rows → 128B swizzle)
-constexpr int STAGES = 6;
-constexpr int CONSUMERS = 8;  // 4 (m) × 2 (n) warps; warp tile 32 × 8·NT
+constexpr int CONSUMERS = 8;
 constexpr int THREADS = (CONSUMERS + 1) * 32;
 
-template <int NT>
+template <int WM, int WN, int NT>
+struct Cfg {
+    static constexpr int BM = 32 * WM;
+    static constexpr int BN = 8 * NT * WN;
+    static constexpr int STAGES = (BM + BN) * BKB * 8 * 6 <= 200 * 1024 ? 6 : 5;
+};
+
+template <int WM, int WN, int NT>
 struct __align__(1024) BasisSmem {
-    double a[STAGES][BM * BKB];            // 16 KiB per stage
-    double b[STAGES][16 * NT * BKB];       // T_rᵀ slab, BN = 16·NT rows
-    uint64_t full[STAGES];
-    uint64_t empty[STAGES];
+    using C = Cfg<WM, WN, NT>;
+    double a[C::STAGES][C::BM * BKB];
+    double b[C::STAGES][((C::BN * BKB + 127) / 128) * 128];  // 1 KiB-aligned slabs
+    uint64_t full[C::STAGES];
+    uint64_t empty[C::STAGES];
 };
 
 // (row, chunk) of a [rows][16 doubles] tile written by TMA with 128B swizzle.
@@ -83,14 +109,15 @@ __device__ __forceinline__ const double* swz(const double* base, int row, int ch
     return base + row * BKB + ((chunk ^ (row & 7)) << 1);
 }
 
-template <int NT>
+template <int WM, int WN, int NT>
 __global__ void __launch_bounds__(THREADS, 1)
     basis_dmma_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap tmap,
                       long long rows, int K, double* __restrict__ phi, int ldp) {
+    using C = Cfg<WM, WN, NT>;
+    constexpr int BM = C::BM, BN = C::BN, STAGES = C::STAGES;
     extern __shared__ unsigned char smem_raw[];
-    BasisSmem<NT>& s = *reinterpret_cast<BasisSmem<NT>*>(
+    BasisSmem<WM, WN, NT>& s = *reinterpret_cast<BasisSmem<WM, WN, NT>*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    constexpr int BN = 16 * NT;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const long long n_rb = (rows + BM - 1) / BM;
     const int nkb = (K + BKB - 1) / BKB;
@@ -127,7 +154,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else {
         const int g = lane >> 2, t = lane & 3;
-        const int wm = warp & 3, wn = warp >> 2;
+        const int wm = warp % WM, wn = warp / WM;
         int stage = 0;
         uint32_t phase = 0;
         for (long long rb = blockIdx.x; rb < n_rb; rb += gridDim.x) {
@@ -209,37 +236,41 @@ cudaError_t map_2d(CUtensorMap* map, const double* base, long long rows, int col
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int NT>
-cudaError_t launch_basis_nt(const double* q, size_t ld, long long rows, int K, const double* trt,
-                            size_t ldt, int col_blocks, double* phi, int ldp, int num_sms,
-                            cudaStream_t stream) {
+template <int WM, int WN, int NT>
+cudaError_t launch_basis_cfg(const double* q, size_t ld, long long rows, int K, const double* trt,
+                             size_t ldt, int col_blocks, double* phi, int ldp, int num_sms,
+                             cudaStream_t stream) {
+    using Cf = Cfg<WM, WN, NT>;
     CUtensorMap qmap, tmap;
-    cudaError_t e = map_2d(&qmap, q, rows, K, ld, BM);
+    cudaError_t e = map_2d(&qmap, q, rows, K, ld, Cf::BM);
     if (e != cudaSuccess) return e;
-    e = map_2d(&tmap, trt, static_cast<long long>(col_blocks) * 16 * NT, K, ldt, 16 * NT);
+    e = map_2d(&tmap, trt, static_cast<long long>(col_blocks) * Cf::BN, K, ldt, Cf::BN);
     if (e != cudaSuccess) return e;
-    const size_t smem = sizeof(BasisSmem<NT>) + 1024;
-    e = set_smem_attr_once(reinterpret_cast<const void*>(basis_dmma_kernel<NT>), static_cast<int>(smem));
+    const size_t smem = sizeof(BasisSmem<WM, WN, NT>) + 1024;
+    e = set_smem_attr_once(reinterpret_cast<const void*>(basis_dmma_kernel<WM, WN, NT>), static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    const long long n_rb = (rows + BM - 1) / BM;
+    const long long n_rb = (rows + Cf::BM - 1) / Cf::BM;
     const int gx = static_cast<int>(std::max<long long>(
         1, std::min<long long>(n_rb, std::max(1, num_sms / col_blocks))));
-    basis_dmma_kernel<NT><<<dim3(gx, col_blocks), THREADS, smem, stream>>>(qmap, tmap, rows, K, phi, ldp);
+    basis_dmma_kernel<WM, WN, NT><<<dim3(gx, col_blocks), THREADS, smem, stream>>>(qmap, tmap, rows, K, phi, ldp);
     note_launch();
     return cudaGetLastError();
 }
 
 }  // namespace
 
+// Padded Φ_r width: a multiple of 8 up to 48 (one warp column, 256-row CTA
+// tiles), else a multiple of 16 up to 128 (two warp columns), else of 128.
 int basis_cols_pad(int r) {
-    if (r <= 128) return std::max(16, (r + 15) / 16 * 16);
+    if (r <= 48) return std::max(8, (r + 7) / 8 * 8);
+    if (r <= 128) return (r + 15) / 16 * 16;
     return (r + 127) / 128 * 128;
 }
 
 cudaError_t launch_project(const double* tr, const double* d, int K, int r, double* qhat,
                            cudaStream_t stream) {
-    dim3 grid((K + kProjThreads - 1) / kProjThreads, (r + kProjRowsPerThread - 1) / kProjRowsPerThread);
-    project_kernel<<<grid, kProjThreads, 0, stream>>>(tr, d, K, r, qhat);
+    dim3 grid((K + kPjCols - 1) / kPjCols, (r + kPjRows * kPjWarps - 1) / (kPjRows * kPjWarps));
+    project_kernel<<<grid, kPjCols * kPjWarps, 0, stream>>>(tr, d, K, r, qhat);
     note_launch();
     return cudaGetLastError();
 }
@@ -256,19 +287,27 @@ cudaError_t launch_basis_rows(const double* q, size_t ld, int K, const double* t
 
 cudaError_t launch_basis(const double* q, size_t ld, long long rows, int K, const double* trt,
                          size_t ldt, int r_pad, double* phi, int num_sms, cudaStream_t stream) {
-    if (r_pad > 128) {
-        return launch_basis_nt<8>(q, ld, rows, K, trt, ldt, r_pad / 128, phi, r_pad, num_sms, stream);
+#define DOPINF_BASIS(WM, WN, NT, CB) \
+    return launch_basis_cfg<WM, WN, NT>(q, ld, rows, K, trt, ldt, CB, phi, r_pad, num_sms, stream)
+    if (r_pad > 128) DOPINF_BASIS(4, 2, 8, r_pad / 128);
+    if (r_pad > 48) {
+        switch (r_pad / 16) {
+            case 4: DOPINF_BASIS(4, 2, 4, 1);
+            case 5: DOPINF_BASIS(4, 2, 5, 1);
+            case 6: DOPINF_BASIS(4, 2, 6, 1);
+            case 7: DOPINF_BASIS(4, 2, 7, 1);
+            default: DOPINF_BASIS(4, 2, 8, 1);
+        }
     }
-    switch (r_pad / 16) {
-        case 1: return launch_basis_nt<1>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
-        case 2: return launch_basis_nt<2>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
-        case 3: return launch_basis_nt<3>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
-        case 4: return launch_basis_nt<4>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
-        case 5: return launch_basis_nt<5>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
-        case 6: return launch_basis_nt<6>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
-        case 7: return launch_basis_nt<7>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
-        default: return launch_basis_nt<8>(q, ld, rows, K, trt, ldt, 1, phi, r_pad, num_sms, stream);
+    switch (r_pad / 8) {
+        case 1: DOPINF_BASIS(8, 1, 1, 1);
+        case 2: DOPINF_BASIS(8, 1, 2, 1);
+        case 3: DOPINF_BASIS(8, 1, 3, 1);
+        case 4: DOPINF_BASIS(8, 1, 4, 1);
+        case 5: DOPINF_BASIS(8, 1, 5, 1);
+        default: DOPINF_BASIS(8, 1, 6, 1);
     }
+#undef DOPINF_BASIS
 }
 
 }  // namespace project

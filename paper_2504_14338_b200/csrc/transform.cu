@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(256)
     for (long long row = warp0; row < rows; row += nwarps) {
         const double neg = means ? -means[row] : -0.0;
         const double s = kScale ? scales[row / nx_i] : 1.0;
+        if (kScale && s == 0.0) continue;  // degenerate variable: left centered, host raises
         double2* p = reinterpret_cast<double2*>(q + static_cast<size_t>(row) * ld);
         for (int c = lane; c < pairs; c += 32 * kApplyBatch) {
             double2 v[kApplyBatch];

@@ -75,8 +75,10 @@ def main():
             q = ref.matmul(allv[: m * rk].reshape(m, rk), allv[m * rk:].reshape(rk, nt))
         d1 = ref.global_gram(q, 1)
         d7 = ref.global_gram(q, 7)
-        lam, _ = ref.eig_reduced_map(d1, 0)
-        numerical_rank = int(np.sum(np.sqrt(np.maximum(lam, 0)) > 1e-8 * np.sqrt(lam[0])))
+        # numerical rank from the singular values of q (acceptance.cpp:218-222 uses thin_svd);
+        # the Gram's round-off eigenvalues (~1e-16 λ1) would over-count it.
+        sigma = np.linalg.svd(q, compute_uv=False)
+        numerical_rank = int(np.sum(sigma > 1e-8 * sigma[0]))
         r = min(max(numerical_rank, 1), 10)
         lam, tr = ref.eig_reduced_map(d1, r)
         out[f"sweep_{i}_gram_p1"] = d1

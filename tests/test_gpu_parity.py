@@ -226,3 +226,75 @@ def test_config1_pass_against_oracle(ctx, oracle):
     assert np.array_equal(b.values, oq)
     ref = oracle.gram(oq)
     assert rel_frob(d, ref) <= GRAM_TOL
+
+
+# ---- streamed pass from host memory (dopinf_b200_snapshot_pass_host) ----------------------------
+@pytest.mark.parametrize("nv,nx,nt,scaling", [(2, 40000, 64, True), (3, 33000, 37, True), (1, 70000, 129, False),
+                                              (4, 100, 9, True), (2, 65536, 200, True)])
+def test_streamed_pass_matches_resident(ctx, oracle, nv, nx, nt, scaling):
+    a = api()
+    rng = np.random.default_rng(nx + nt)
+    q = rng.standard_normal((nv * nx, nt)) * np.repeat(10.0 ** np.arange(nv), nx)[:, None] + 3.0
+    b1 = make_block(ctx, q, nv)
+    p1, d1 = a.snapshot_pass(b1, scaling=scaling)
+    v1 = b1.values
+    b2 = a.LocalBlock(ctx, nv, a.RowRange(0, nx), nt)
+    p2, d2 = a.snapshot_pass_host(b2, q, scaling=scaling)
+    assert np.array_equal(p1.local_means, p2.local_means)
+    if scaling:
+        assert np.array_equal(p1.scales, p2.scales)
+    assert np.array_equal(b2.values, v1)          # bit-identical transformed block
+    oq, _ = oracle.center(q)
+    if scaling:
+        oq = oracle.scale(oq, nv, nx, p1.scales)
+    assert rel_frob(d2, oracle.gram(oq)) <= GRAM_TOL
+    assert np.array_equal(d2, d2.T)
+    _, d3 = a.snapshot_pass_host(b2, q, scaling=scaling)
+    assert np.array_equal(d2, d3)                 # deterministic
+
+
+def test_streamed_pass_degenerate_variable(ctx):
+    a = api()
+    q = np.vstack([np.full((50, 6), 2.5), np.random.default_rng(0).standard_normal((50, 6))])
+    b = a.LocalBlock(ctx, 2, a.RowRange(0, 50), 6)
+    with pytest.raises(a.DegenerateVariableError):
+        a.snapshot_pass_host(b, q, scaling=True)
+
+
+# ---- against the reference's own outputs (tests/golden, made by the unmodified reference) ------------
+def _golden():
+    from pathlib import Path
+
+    return np.load(Path(__file__).parent / "golden" / "reference_vectors.npz")
+
+
+@pytest.mark.parametrize("i", list(range(20)))
+def test_sweep_against_reference_golden(ctx, oracle, i):
+    a = api()
+    g = _golden()
+    m, nt, rk = (int(v) for v in g["sweep_meta"][i])
+    rng = oracle.rng(1000 + i)
+    q = rng.matrix(m, nt) if rk == 0 else oracle.matmul(rng.matrix(m, rk), rng.matrix(rk, nt))
+    b = make_block(ctx, q)
+    d = a.local_gram(b)
+    assert rel_frob(d, g[f"sweep_{i}_gram_p1"]) <= GRAM_TOL
+    tr = g[f"sweep_{i}_tr"]
+    assert np.array_equal(a.project(tr, g[f"sweep_{i}_gram_p1"], ctx), g[f"sweep_{i}_qhat"])
+    assert np.array_equal(a.basis_rows(b, tr, g[f"sweep_{i}_basis_sel"]), g[f"sweep_{i}_basis_rows"])
+    phi = a.basis(b, tr)
+    assert rel_frob(phi, oracle.matmul(q, tr)) <= BASIS_TOL
+
+
+@pytest.mark.parametrize("tag", ["t12", "t8", "t21", "t77"])
+def test_transform_against_reference_golden(ctx, oracle, tag):
+    a = api()
+    g = _golden()
+    nv, nx, nt, seed = next((int(x) for x in row) for row in g["transform_meta"]
+                            if {12: "t12", 8: "t8", 21: "t21", 77: "t77"}[int(row[3])] == tag)
+    q = oracle.rng(seed).matrix(nv * nx, nt)
+    b = make_block(ctx, q, nv)
+    params, d = a.snapshot_pass(b, scaling=True)
+    assert np.array_equal(b.values, g[f"transform_{tag}_p1_q"])
+    assert np.array_equal(params.local_means, g[f"transform_{tag}_p1_means"])
+    assert np.array_equal(params.scales, g[f"transform_{tag}_p1_scales"])
+    assert rel_frob(d, g[f"transform_{tag}_p1_gram"]) <= GRAM_TOL
