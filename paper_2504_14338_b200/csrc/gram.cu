@@ -41,8 +41,8 @@ namespace {
 constexpr int BT = kTileEdge;         // 128 columns per block
 constexpr int BK = kRowsPerStage;     // 16 rows per stage
 constexpr int STAGES = 6;
-constexpr int CONSUMERS = kConsumerWarps;  // 16
-constexpr int THREADS = (CONSUMERS + 1) * kWarp;
+constexpr int CONSUMERS = kConsumerWarps;  // 16 = 4 consumer warpgroups
+constexpr int THREADS = (CONSUMERS + 1) * kWarp;  // + one TMA producer warp
 constexpr int FLAG_FIRST = 1, FLAG_LAST = 2, FLAG_DONE = 4;
 
 struct __align__(1024) Smem {
@@ -98,7 +98,8 @@ __device__ __forceinline__ void stage_mma(double (&acc)[16][2], const double* __
 
 __global__ void __launch_bounds__(THREADS, 1)
     gram_dmma_kernel(const __grid_constant__ CUtensorMap tmap, const TileInfo* __restrict__ tiles,
-                     int n_tiles, int n_items, long long n_rows, int chunk_rows,
+                     int n_tiles, int n_items, long long n_rows, int chunk_rows, int big_splits,
+                     int small_rows,
                      double* __restrict__ work, int* __restrict__ counters, int accumulate) {
     extern __shared__ unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(
@@ -132,8 +133,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int tile = item % n_tiles;
                 const int split = item / n_tiles;
                 const int I = tiles[tile].I, J = tiles[tile].J;
-                const long long row0 = static_cast<long long>(split) * chunk_rows;
-                const long long rows = min(static_cast<long long>(chunk_rows), n_rows - row0);
+                // Guided split sizes: big_splits chunks of chunk_rows, then short
+                // chunks of small_rows so the last wave of items ends together.
+                const long long row0 = split < big_splits
+                                           ? static_cast<long long>(split) * chunk_rows
+                                           : static_cast<long long>(big_splits) * chunk_rows +
+                                                 static_cast<long long>(split - big_splits) * small_rows;
+                const long long rows =
+                    min(static_cast<long long>(split < big_splits ? chunk_rows : small_rows), n_rows - row0);
                 const int nkb = static_cast<int>((rows + BK - 1) / BK);
                 const bool diag = (I == J);
                 const uint32_t bytes = (diag ? 1u : 2u) * BK * BT * sizeof(double);
@@ -393,8 +400,20 @@ Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes)
     }
     chunk = std::max<long long>(BK, (chunk + BK - 1) / BK * BK);
     S = std::max<long long>(1, (n_rows + chunk - 1) / chunk);
-    p.n_splits = static_cast<int>(S);
+    // Guided tail: the last T big splits (about two waves of items) become 4T
+    // quarter-size splits so the final items finish close together.
+    const long long T = (2LL * num_sms + p.n_tiles - 1) / p.n_tiles;
+    long long big = S, small = chunk, n_small = 0;
+    if (S > 2 * T && chunk >= 4 * BK) {
+        big = S - T;
+        const long long rest = n_rows - big * chunk;
+        small = std::max<long long>(BK, ((rest + 4 * T - 1) / (4 * T) + BK - 1) / BK * BK);
+        n_small = (rest + small - 1) / small;
+    }
+    p.n_splits = static_cast<int>(big + n_small);
     p.chunk_rows = static_cast<int>(chunk);
+    p.big_splits = static_cast<int>(big);
+    p.small_rows = static_cast<int>(small);
     p.n_items = p.n_splits * p.n_tiles;
     p.grid = std::min(num_sms, p.n_items);
     p.workspace_doubles = static_cast<size_t>(p.n_items) * kItemDoubles;
@@ -423,8 +442,8 @@ cudaError_t launch_gram(const Plan& plan, const CUtensorMap& map, const TileInfo
                                              static_cast<int>(smem_bytes()));
     if (e != cudaSuccess) return e;
     gram_dmma_kernel<<<plan.grid, THREADS, smem_bytes(), stream>>>(
-        map, d_tiles, plan.n_tiles, plan.n_items, plan.n_rows, plan.chunk_rows, work, counters,
-        accumulate ? 1 : 0);
+        map, d_tiles, plan.n_tiles, plan.n_items, plan.n_rows, plan.chunk_rows, plan.big_splits, plan.small_rows,
+        work, counters, accumulate ? 1 : 0);
     note_launch();
     return cudaGetLastError();
 }
@@ -437,6 +456,8 @@ Plan make_stream_plan(long long chunk_rows, int K, int num_sms, long long split_
     const long long split = std::max<long long>(BK, (split_rows + BK - 1) / BK * BK);
     p.chunk_rows = static_cast<int>(split);
     p.n_splits = static_cast<int>(std::max<long long>(1, (chunk_rows + split - 1) / split));
+    p.big_splits = p.n_splits;
+    p.small_rows = p.chunk_rows;
     p.n_items = p.n_splits * p.n_tiles;
     p.grid = std::min(num_sms, p.n_items);
     p.workspace_doubles = static_cast<size_t>(p.n_items) * kItemDoubles;

@@ -31,7 +31,9 @@ struct Plan {
     long long n_rows = 0;
     int n_tiles = 0;
     int n_splits = 0;
-    int chunk_rows = 0;
+    int chunk_rows = 0;   // rows of the first big_splits splits
+    int big_splits = 0;
+    int small_rows = 0;   // rows of the remaining (tail) splits
     int n_items = 0;
     int grid = 0;
     size_t workspace_doubles = 0;
