@@ -84,7 +84,8 @@ typedef enum dopinf_b200_stage {
     DOPINF_B200_STAGE_BASIS = 9,      /* Φ_r = Q T_r                            */
     DOPINF_B200_STAGE_DOWNLOAD = 10,
     DOPINF_B200_STAGE_STREAM = 11,    /* whole streamed pass (first H2D -> D ready) */
-    DOPINF_B200_STAGE_COUNT = 12
+    DOPINF_B200_STAGE_STREAM_GRAM = 12,/* sum of the streamed pass's Gram launches */
+    DOPINF_B200_STAGE_COUNT = 13
 } dopinf_b200_stage;
 
 typedef struct dopinf_b200_ctx dopinf_b200_ctx;
@@ -200,6 +201,17 @@ int dopinf_b200_snapshot_pass(dopinf_b200_block* block, int scaling, double* mea
  * the degenerate one are left scaled. */
 int dopinf_b200_snapshot_pass_host(dopinf_b200_block* block, const double* host, size_t host_ld,
                                    int scaling, double* means, double* scales, double* d);
+/* Steps II-III for a block too large to hold (BASELINE config 4: 8 vars ×
+ * 4,194,304 points × K=1500 is 403 GB per GPU): the rows are generated on the
+ * device chunk by chunk (the seeded oscillator of
+ * dopinf_b200_block_synth_oscillator, same bytes) into a two-slot ring and
+ * streamed through stats, centering and the per-variable Gram; the block is
+ * never resident, so only the means (rows), scales (n_vars) and D (nt x nt)
+ * come back. Ranks pass their own (nx_i, row_begin). */
+int dopinf_b200_stream_pass_synth(dopinf_b200_ctx* ctx, size_t n_vars, size_t nx_i, size_t row_begin,
+                                  size_t nt, uint64_t seed, int n_modes, double dt, double noise,
+                                  const double* amps, int scaling, double* means, double* scales,
+                                  double* d);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ SUM, MAX, MIN = 0, 1, 2
 GRAM_REDUCE_ORDERED, GRAM_REDUCE_NCCL = 0, 1
 
 STAGES = ["upload", "stats", "scales", "apply", "gram", "gram_reduce", "allreduce", "unpack",
-          "project", "basis", "download", "stream"]
+          "project", "basis", "download", "stream", "stream_gram"]
 UNIQUE_ID_BYTES = 128
 
 _dp = C.POINTER(C.c_double)
@@ -69,6 +69,8 @@ SIGNATURES = {
     "dopinf_b200_basis_rows": (C.c_int, [_vp, _dp, C.c_size_t, _sp, C.c_size_t, _dp]),
     "dopinf_b200_snapshot_pass": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp]),
     "dopinf_b200_snapshot_pass_host": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int, _dp, _dp, _dp]),
+    "dopinf_b200_stream_pass_synth": (C.c_int, [_vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64,
+                                                 C.c_int, C.c_double, C.c_double, _dp, C.c_int, _dp, _dp, _dp]),
 }
 
 _lib = None

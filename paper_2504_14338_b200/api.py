@@ -408,3 +408,19 @@ def snapshot_pass_host(block: LocalBlock, host_values, scaling: bool, out: dict 
 
 def kernel_launches() -> int:
     return int(_lib.load().dopinf_b200_kernel_launches())
+
+
+def stream_pass_synth(ctx: DeviceContext, n_vars: int, row_range: RowRange, nt: int, seed: int, n_modes: int,
+                      dt: float = 1e-3, noise: float = 1e-4, amps=None, scaling: bool = True):
+    """Steps II-III over device-generated rows that are never resident (config 4:
+    403 GB per GPU): returns (TransformParams, D) — means, scales and the Gram."""
+    nx_i = row_range.count()
+    means = np.empty(max(n_vars * nx_i, 1), dtype=np.float64)
+    scales = np.empty(n_vars, dtype=np.float64)
+    d = np.empty((nt, nt), dtype=np.float64)
+    a = None if amps is None else _f64(amps, (n_vars,))
+    rc = _lib.load().dopinf_b200_stream_pass_synth(ctx._h, n_vars, nx_i, row_range.begin, nt, seed, n_modes, dt,
+                                                   noise, _lib.dptr(a), 1 if scaling else 0, _lib.dptr(means),
+                                                   _lib.dptr(scales), _lib.dptr(d))
+    _check(rc, ctx, "stream_pass_synth")
+    return TransformParams(means[: n_vars * nx_i], scales if scaling else np.zeros(0), scaling), d

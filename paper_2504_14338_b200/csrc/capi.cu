@@ -141,6 +141,36 @@ struct dopinf_b200_ctx {
     cudaStream_t copy_stream = nullptr;    // streamed pass: H2D of chunk c+1 overlaps chunk c
     std::vector<cudaEvent_t> chunk_events;  // one per streamed chunk (grow-only)
     DBuf gv;                                // per-variable packed Grams of the streamed pass
+    DBuf ring;                              // synth stream: two chunk slots
+    std::vector<cudaEvent_t> timing_events; // streamed Gram launches: start/end pairs
+    size_t stream_gram_ms_events_used = 0;
+    struct EvList {
+        std::vector<cudaEvent_t>* pool;
+        size_t* used;
+        void clear() { *used = 0; }
+    } stream_gram_ms_events{&timing_events, &stream_gram_ms_events_used};
+
+    // Record one timing event on the compute stream (pairs bracket Gram launches).
+    void gram_event_pair() {
+        if (stream_gram_ms_events_used == timing_events.size()) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "cudaEventCreate");
+            timing_events.push_back(e);
+        }
+        ck(cudaEventRecord(timing_events[stream_gram_ms_events_used++], stream), "event");
+    }
+    // Sum of the bracketed Gram launch times of the last streamed pass (ms).
+    double stream_gram_ms() const {
+        double total = 0.0;
+        for (size_t i = 0; i + 1 < stream_gram_ms_events_used; i += 2) {
+            float f = 0.0f;
+            if (cudaEventSynchronize(timing_events[i + 1]) == cudaSuccess &&
+                cudaEventElapsedTime(&f, timing_events[i], timing_events[i + 1]) == cudaSuccess) {
+                total += f;
+            }
+        }
+        return total;
+    }
     ncclComm_t comm = nullptr;
     int gram_reduce = DOPINF_B200_GRAM_REDUCE_ORDERED;
     std::string err;
@@ -398,9 +428,15 @@ void do_global_gram(dopinf_b200_ctx* c, double* d_host) {
     copy_d_out(c, d_host);
 }
 
-// ---- streamed Steps II-III (dopinf_b200_snapshot_pass_host) ------------------------
-constexpr long long kStreamChunkRows = 32768;  // rows per H2D chunk (315 MB at K = 1200)
-constexpr long long kStreamSplitRows = 2048;   // rows per Gram item inside a chunk
+// ---- streamed Steps II-III ----------------------------------------------------------
+// dopinf_b200_snapshot_pass_host: rows arrive from host memory into the
+// resident block (H2D on the copy stream overlaps the compute stream).
+// dopinf_b200_stream_pass_synth: rows are generated on the device chunk by chunk
+// into a two-slot ring — the block is never resident (config 4: 403 GB/GPU).
+constexpr long long kStreamChunkRows = 32768;   // rows per H2D chunk (315 MB at K = 1200)
+constexpr long long kStreamSplitRows = 2048;    // rows per Gram item inside a host chunk
+constexpr long long kSynthChunkRows = 262144;   // rows per generated chunk (3.1 GB at K = 1500)
+constexpr long long kSynthSplitRows = 8192;
 
 struct StreamChunk {
     int var;
@@ -408,34 +444,46 @@ struct StreamChunk {
     bool first_of_var, last_of_var;
 };
 
-std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b) {
+struct StreamSource {
+    const double* host = nullptr;  // host rows (pitch host_ld) → resident block
+    size_t host_ld = 0;
+    bool synth = false;            // device-generated rows → ring buffer, block not resident
+    uint64_t seed = 0;
+    int n_modes = 0;
+    double dt = 0.0, noise = 0.0;
+    const double* amps = nullptr;  // host [n_vars] or null
+};
+
+std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b, long long chunk_rows) {
     std::vector<StreamChunk> out;
     for (size_t v = 0; v < b->n_vars; ++v) {
         const long long v0 = static_cast<long long>(v * b->nx_i), v1 = v0 + static_cast<long long>(b->nx_i);
-        for (long long r0 = v0; r0 < v1; r0 += kStreamChunkRows) {
-            const long long rows = std::min(kStreamChunkRows, v1 - r0);
+        for (long long r0 = v0; r0 < v1; r0 += chunk_rows) {
+            const long long rows = std::min(chunk_rows, v1 - r0);
             out.push_back({static_cast<int>(v), r0, rows, r0 == v0, r0 + rows == v1});
         }
     }
     return out;
 }
 
-// Chunks of rows land on the copy stream; on the compute stream each landed
-// chunk gets its row means / max-abs (stats pass), is centered in place, and
-// its Gram items accumulate (chunk order) into the split slots of its
-// variable. When a variable's last chunk is done its slots are reduced into
-// G_v, its MAX goes over the ranks, and its rows are scaled. D = Σ_v G_v/s_v².
-void do_stream_pass(dopinf_b200_block* b, const double* host, size_t host_ld, bool scaling, double* means_host,
+// On the compute stream each landed chunk gets its row means / max-abs (stats
+// pass), is centered in place, and its Gram items accumulate (chunk order)
+// into the split slots of its variable. When a variable's last chunk is done
+// its slots are reduced into G_v, its MAX goes over the ranks and (resident
+// block) its rows are scaled. D = Σ_v G_v / s_v².
+void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling, double* means_host,
                     double* scales_host) {
     auto* c = b->ctx;
     const int K = static_cast<int>(b->nt);
     const size_t count = gram::packed_count(K);
+    const long long chunk_rows = src.synth ? kSynthChunkRows : kStreamChunkRows;
+    const long long split_rows = src.synth ? kSynthSplitRows : kStreamSplitRows;
     b->pending_center = false;
     b->stats_valid = false;
     c->have_gram = false;
     c->K = K;
-    const std::vector<StreamChunk> chunks = stream_chunks(b);
-    while (c->chunk_events.size() < chunks.size()) {
+    const std::vector<StreamChunk> chunks = stream_chunks(b, chunk_rows);
+    while (c->chunk_events.size() < chunks.size() + 1) {
         cudaEvent_t e;
         ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
         c->chunk_events.push_back(e);
@@ -443,36 +491,53 @@ void do_stream_pass(dopinf_b200_block* b, const double* host, size_t host_ld, bo
     ensure_tiles(c, K);
     int* counters = ensure_counters(c);
     const auto* tiles = c->tiles.get<gram::TileInfo>(gram::plan_tiles(K).size(), "tiles");
-    const long long first_rows = std::min<long long>(kStreamChunkRows, static_cast<long long>(b->nx_i));
-    const gram::Plan full = gram::make_stream_plan(std::max<long long>(first_rows, 1), K, c->num_sms,
-                                                   kStreamSplitRows);
+    const long long first_rows = std::min<long long>(chunk_rows, static_cast<long long>(b->nx_i));
+    const gram::Plan full =
+        gram::make_stream_plan(std::max<long long>(first_rows, 1), K, c->num_sms, split_rows);
     double* work = c->work.get<double>(full.workspace_doubles, "workspace");
     double* gv = c->gv.get<double>(count * b->n_vars, "per-variable Grams");
     double* vm = b->varmax.get<double>(b->n_vars, "varmax");
     double* ds = c->scales.get<double>(b->n_vars, "scales");
     double* mn = b->means.get<double>(std::max<size_t>(b->rows, 1), "means");
     double* packed = c->packed.get<double>(count, "packed");
+    double* ring = src.synth ? c->ring.get<double>(2 * static_cast<size_t>(first_rows) * b->ld, "chunk ring")
+                             : nullptr;
+    std::vector<double> amps_v;  // per-variable amplitude slice for the generator
+    if (src.synth && src.amps) amps_v.assign(src.amps, src.amps + b->n_vars);
+    c->stream_gram_ms_events.clear();
 
     c->record(DOPINF_B200_STAGE_STREAM, 0);
     ck(cudaMemsetAsync(vm, 0, b->n_vars * sizeof(double), c->stream), "memset");
     ck(cudaMemsetAsync(gv, 0, count * b->n_vars * sizeof(double), c->stream), "memset");
-    // The copy stream must not overwrite the block before earlier work on it is done.
-    cudaEvent_t ready = c->chunk_events[0];
-    ck(cudaEventRecord(ready, c->stream), "event");
-    ck(cudaStreamWaitEvent(c->copy_stream, ready, 0), "event wait");
-    for (size_t k = 0; k < chunks.size(); ++k) {
-        const StreamChunk& ch = chunks[k];
-        ck(cudaMemcpy2DAsync(b->q + ch.r0 * b->ld, b->ld * sizeof(double), host + ch.r0 * host_ld,
-                             host_ld * sizeof(double), b->nt * sizeof(double), ch.rows, cudaMemcpyHostToDevice,
-                             c->copy_stream),
-           "chunk H2D");
-        ck(cudaEventRecord(c->chunk_events[k], c->copy_stream), "event");
+    if (!src.synth) {
+        // The copy stream must not overwrite the block before earlier work on it is done.
+        cudaEvent_t ready = c->chunk_events[chunks.size()];
+        ck(cudaEventRecord(ready, c->stream), "event");
+        ck(cudaStreamWaitEvent(c->copy_stream, ready, 0), "event wait");
+        for (size_t k = 0; k < chunks.size(); ++k) {
+            const StreamChunk& ch = chunks[k];
+            ck(cudaMemcpy2DAsync(b->q + ch.r0 * b->ld, b->ld * sizeof(double), src.host + ch.r0 * src.host_ld,
+                                 src.host_ld * sizeof(double), b->nt * sizeof(double), ch.rows,
+                                 cudaMemcpyHostToDevice, c->copy_stream),
+               "chunk H2D");
+            ck(cudaEventRecord(c->chunk_events[k], c->copy_stream), "event");
+        }
     }
     gram::Plan first_plan = full;
     for (size_t k = 0; k < chunks.size(); ++k) {
         const StreamChunk& ch = chunks[k];
-        ck(cudaStreamWaitEvent(c->stream, c->chunk_events[k], 0), "event wait");
-        double* qk = b->q + ch.r0 * b->ld;
+        double* qk;
+        if (src.synth) {
+            qk = ring + (k % 2) * static_cast<size_t>(first_rows) * b->ld;
+            const long long local0 = ch.r0 - static_cast<long long>(ch.var) * static_cast<long long>(b->nx_i);
+            ck(synth::oscillator(qk, b->ld, ch.rows, K, ch.rows, static_cast<long long>(b->row_begin) + local0, 1,
+                                 src.seed, src.n_modes, src.dt, src.noise, src.amps ? &amps_v[ch.var] : nullptr,
+                                 c->num_sms, c->stream, ch.var),
+               "synth chunk");
+        } else {
+            ck(cudaStreamWaitEvent(c->stream, c->chunk_events[k], 0), "event wait");
+            qk = b->q + ch.r0 * b->ld;
+        }
         // chunk = one variable's rows: present it to the kernels as a 1-variable block
         ck(transform::launch_stats(qk, b->ld, ch.rows, K, ch.rows, 1, true, mn + ch.r0, vm + ch.var, c->num_sms,
                                    c->stream),
@@ -481,9 +546,11 @@ void do_stream_pass(dopinf_b200_block* b, const double* host, size_t host_ld, bo
            "center");
         CUtensorMap map;
         ck(gram::make_tensor_map(&map, qk, ch.rows, K, b->ld), "tensor map");
-        const gram::Plan plan = gram::make_stream_plan(ch.rows, K, c->num_sms, kStreamSplitRows);
+        const gram::Plan plan = gram::make_stream_plan(ch.rows, K, c->num_sms, split_rows);
         if (ch.first_of_var) first_plan = plan;
+        c->gram_event_pair();
         ck(gram::launch_gram(plan, map, tiles, work, counters, c->stream, !ch.first_of_var), "gram");
+        c->gram_event_pair();
         if (ch.last_of_var) {
             ck(gram::launch_reduce(first_plan, tiles, work, gv + static_cast<size_t>(ch.var) * count, c->stream),
                "gram reduce");
@@ -496,11 +563,13 @@ void do_stream_pass(dopinf_b200_block* b, const double* host, size_t host_ld, bo
                                        c->stream),
                        "copy");
                 }
-                const long long v0 = static_cast<long long>(ch.var) * static_cast<long long>(b->nx_i);
-                ck(transform::launch_apply(b->q + v0 * b->ld, b->ld, static_cast<long long>(b->nx_i), K,
-                                           static_cast<long long>(b->nx_i), nullptr, ds + ch.var, c->num_sms,
-                                           c->stream),
-                   "scale");
+                if (!src.synth) {
+                    const long long v0 = static_cast<long long>(ch.var) * static_cast<long long>(b->nx_i);
+                    ck(transform::launch_apply(b->q + v0 * b->ld, b->ld, static_cast<long long>(b->nx_i), K,
+                                               static_cast<long long>(b->nx_i), nullptr, ds + ch.var, c->num_sms,
+                                               c->stream),
+                       "scale");
+                }
             }
         }
     }
@@ -639,7 +708,9 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
     }
     c->staging.release();
     c->gv.release();
+    c->ring.release();
     for (cudaEvent_t e : c->chunk_events) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->timing_events) cudaEventDestroy(e);
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);
         cudaStreamDestroy(c->copy_stream);
@@ -692,6 +763,10 @@ int dopinf_b200_barrier(dopinf_b200_ctx* c) {
 int dopinf_b200_stage_ms(const dopinf_b200_ctx* c, int stage, double* ms) {
     if (!c || !ms || stage < 0 || stage >= DOPINF_B200_STAGE_COUNT) return DOPINF_B200_ERR_INVALID_ARGUMENT;
     *ms = 0.0;
+    if (stage == DOPINF_B200_STAGE_STREAM_GRAM) {
+        *ms = c->stream_gram_ms();
+        return DOPINF_B200_OK;
+    }
     if (!c->ev_done[stage]) return DOPINF_B200_OK;
     float f = 0.0f;
     if (cudaEventSynchronize(c->ev[stage][1]) != cudaSuccess ||
@@ -1003,10 +1078,50 @@ int dopinf_b200_snapshot_pass_host(dopinf_b200_block* b, const double* host, siz
     auto* c = b->ctx;
     return guarded(c, [&] {
         require(host_ld >= b->nt && (b->rows == 0 || host), "snapshot_pass_host: bad host buffer");
-        do_stream_pass(b, host, host_ld, scaling != 0, means, scales);
+        StreamSource src;
+        src.host = host;
+        src.host_ld = host_ld;
+        do_stream_pass(b, src, scaling != 0, means, scales);
         unpack(c);
         do_global_gram(c, d);
         c->sync("snapshot_pass_host");
+    });
+}
+
+int dopinf_b200_stream_pass_synth(dopinf_b200_ctx* c, size_t n_vars, size_t nx_i, size_t row_begin, size_t nt,
+                                  uint64_t seed, int n_modes, double dt, double noise, const double* amps,
+                                  int scaling, double* means, double* scales, double* d) {
+    return guarded(c, [&] {
+        require(n_vars >= 1 && nt >= 1 && nt <= (1u << 20), "stream_pass_synth: bad shape");
+        require(n_modes >= 1 && n_modes <= 128, "stream_pass_synth: n_modes must lie in [1, 128]");
+        // A block that is never resident: means/varmax live on the device, values stream through a ring.
+        dopinf_b200_block view;
+        view.ctx = c;
+        view.n_vars = n_vars;
+        view.nx_i = nx_i;
+        view.row_begin = row_begin;
+        view.nt = nt;
+        view.ld = (nt + 1) / 2 * 2;
+        view.rows = n_vars * nx_i;
+        struct Release {
+            dopinf_b200_block& b;
+            ~Release() {
+                cudaStreamSynchronize(b.ctx->stream);
+                b.means.release();
+                b.varmax.release();
+            }
+        } release{view};
+        StreamSource src;
+        src.synth = true;
+        src.seed = seed;
+        src.n_modes = n_modes;
+        src.dt = dt;
+        src.noise = noise;
+        src.amps = amps;
+        do_stream_pass(&view, src, scaling != 0, means, scales);
+        unpack(c);
+        do_global_gram(c, d);
+        c->sync("stream_pass_synth");
     });
 }
 

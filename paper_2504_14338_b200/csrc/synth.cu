@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256)
     fill_kernel(double* __restrict__ q, size_t ld, long long rows, int K, long long nx_i,
                 long long row_begin, int m, const double* __restrict__ modes,
                 const double* __restrict__ amps, const double* __restrict__ table, uint64_t seed,
-                double noise, double amp) {
+                double noise, double amp, int var0) {
     __shared__ double fac[8][kMaxModes];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const long long nwarps = static_cast<long long>(gridDim.x) * 8;
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256)
         for (int k = lane; k < K; k += 32) {
             double acc = 0.0;
             for (int j = 0; j < m; ++j) acc = fma(fac[warp][j], tab[static_cast<size_t>(j) * K + k], acc);
-            if (noise != 0.0) acc += noise * normal(key4(seed, 0x5EED0004ULL + v, p, k));
+            if (noise != 0.0) acc += noise * normal(key4(seed, 0x5EED0004ULL + var0 + v, p, k));
             dst[k] = acc;
         }
         __syncwarp();
@@ -107,11 +107,11 @@ __global__ void __launch_bounds__(256)
 
 cudaError_t oscillator(double* q, size_t ld, long long rows, int K, long long nx_i,
                        long long row_begin, int n_vars, uint64_t seed, int n_modes, double dt,
-                       double noise, const double* amps_host, int num_sms, cudaStream_t stream) {
+                       double noise, const double* amps_host, int num_sms, cudaStream_t stream, int var0) {
     if (n_modes < 1 || n_modes > kMaxModes) return cudaErrorInvalidValue;
     std::vector<double> modes(static_cast<size_t>(n_vars) * n_modes * 4);
     for (int v = 0; v < n_vars; ++v) {
-        std::mt19937_64 gen(seed * 1000003ULL + static_cast<uint64_t>(v));
+        std::mt19937_64 gen(seed * 1000003ULL + static_cast<uint64_t>(var0 + v));
         auto uni = [&](double lo, double hi) {
             return lo + (hi - lo) * (static_cast<double>(gen() >> 11) * 0x1.0p-53);
         };
@@ -137,7 +137,7 @@ cudaError_t oscillator(double* q, size_t ld, long long rows, int K, long long nx
         osc_table_kernel<<<num_sms * 4, 256, 0, stream>>>(d_modes, n_vars, n_modes, K, dt, d_table);
         note_launch();
         fill_kernel<true><<<num_sms * 8, 256, 0, stream>>>(q, ld, rows, K, nx_i, row_begin, n_modes,
-                                                          d_modes, d_amps, d_table, seed, noise, 1.0);
+                                                          d_modes, d_amps, d_table, seed, noise, 1.0, var0);
         note_launch();
         e = cudaGetLastError();
         // Host vectors must outlive the async copies.
@@ -160,7 +160,7 @@ cudaError_t lowrank(double* q, size_t ld, long long rows, int K, long long nx_i,
         note_launch();
         fill_kernel<false><<<num_sms * 8, 256, 0, stream>>>(q, ld, rows, K, nx_i, row_begin, rank,
                                                            nullptr, nullptr, d_table, seed, 1.0,
-                                                           amplitude);
+                                                           amplitude, 0);
         note_launch();
         e = cudaGetLastError();
     }

@@ -298,3 +298,21 @@ def test_transform_against_reference_golden(ctx, oracle, tag):
     assert np.array_equal(params.local_means, g[f"transform_{tag}_p1_means"])
     assert np.array_equal(params.scales, g[f"transform_{tag}_p1_scales"])
     assert rel_frob(d, g[f"transform_{tag}_p1_gram"]) <= GRAM_TOL
+
+
+def test_synth_stream_pass_matches_resident(ctx, oracle):
+    """Config-4 path: device-generated, never-resident rows (two 262,144-row ring
+    chunks per variable here) give the resident pass's means and scales bit for
+    bit and its Gram within tolerance."""
+    a = api()
+    nv, nx, nt = 2, 300000, 24
+    amps = np.array([1e-2, 1e5])
+    b = a.LocalBlock(ctx, nv, a.RowRange(5, 5 + nx), nt)
+    b.synth_oscillator(seed=7, n_modes=12, dt=1e-3, noise=1e-4, amps=amps)
+    p1, d1 = a.snapshot_pass(b, scaling=True)
+    p2, d2 = a.stream_pass_synth(ctx, nv, a.RowRange(5, 5 + nx), nt, seed=7, n_modes=12, dt=1e-3, noise=1e-4,
+                                 amps=amps, scaling=True)
+    assert np.array_equal(p1.local_means, p2.local_means)
+    assert np.array_equal(p1.scales, p2.scales)
+    assert rel_frob(d2, d1) <= GRAM_TOL
+    assert ctx.stage_ms("stream_gram") > 0.0
