@@ -49,7 +49,10 @@ typedef enum dopinf_b200_status {
     DOPINF_B200_ERR_COLLECTIVE = 3,         /* CollectiveError        (errors.hpp:28-31) */
     DOPINF_B200_ERR_DEGENERATE_VARIABLE = 4,/* DegenerateVariableError(errors.hpp:34-37) */
     DOPINF_B200_ERR_DEVICE = 5,             /* CUDA / NCCL failure (surfaced as dopinf::Error) */
-    DOPINF_B200_ERR_OUT_OF_MEMORY = 6       /* device allocation failure (dopinf::Error)      */
+    DOPINF_B200_ERR_OUT_OF_MEMORY = 6,      /* device allocation failure (dopinf::Error)      */
+    DOPINF_B200_ERR_NOT_PSD = 7,            /* NotPsdError            (errors.hpp:40-43) */
+    DOPINF_B200_ERR_RANK_DEFICIENCY = 8,    /* RankDeficiencyError    (errors.hpp:46-49) */
+    DOPINF_B200_ERR_SOLVE = 9               /* SolveError             (errors.hpp:52-55) */
 } dopinf_b200_status;
 
 /* Collective ops, same order as comm::ReduceOp (comm.hpp:9). */
@@ -168,16 +171,32 @@ int dopinf_b200_local_gram(dopinf_b200_block* block, double* d);
  * ranks (identical on every rank) and optionally writes it to the host. */
 int dopinf_b200_global_gram(dopinf_b200_ctx* ctx, double* d);
 /* project (pod.cpp:103-105): Q̂ = T_rᵀ D with the context's device D;
- * tr is host nt x r, qhat host r x nt. */
+ * tr is host nt x r (NULL: the device T_r of dopinf_b200_reduced_map),
+ * qhat host r x nt. */
 int dopinf_b200_project(dopinf_b200_ctx* ctx, const double* tr, size_t nt, size_t r,
                         double* qhat);
+/* §8(f) next-row 1 — the eigensolve on the device. eig_sym_desc
+ * (pod.cpp:20-65): cuSOLVER dsyevd of the context's device D; eigenvalues
+ * descending, negatives within −1e-10·λ1 clamped to 0 (NOT_PSD below that),
+ * each eigenvector flipped so its largest-magnitude entry (lowest index on
+ * ties) is positive. lambda: host [nt]; vectors: host nt x nt row-major,
+ * column k ↔ lambda[k]; either may be NULL. */
+int dopinf_b200_eig_sym_desc(dopinf_b200_ctx* ctx, double* lambda, double* vectors);
+/* Make a host nt x nt symmetric D the context's device Gram (for
+ * eig_sym_desc(const Matrix& d) callers that hold D on the host). */
+int dopinf_b200_set_gram(dopinf_b200_ctx* ctx, const double* d, size_t nt);
+/* reduced_map (pod.cpp:84-101): T_r = U_r · (1/√λ_k) from the context's
+ * eigendecomposition, kept on the device (project / basis with tr == NULL use
+ * it); RANK_DEFICIENCY when λ_r is 0. tr: host nt x r, may be NULL. */
+int dopinf_b200_reduced_map(dopinf_b200_ctx* ctx, size_t r, double* tr);
 /* project with a caller-provided host D (nt x nt). */
 int dopinf_b200_project_host(dopinf_b200_ctx* ctx, const double* tr, const double* d, size_t nt,
                              size_t r, double* qhat);
 
 /* ---- Step V products (postprocess.cpp) --------------------------------- */
-/* Φ_r = Q T_r over the (transformed) block: rows x r. phi (host) may be NULL
- * to keep the result on the device only (dopinf_b200_basis_device). */
+/* Φ_r = Q T_r over the (transformed) block: rows x r. tr: host nt x r, or
+ * NULL for the context's device T_r. phi (host) may be NULL to keep the
+ * result on the device only (dopinf_b200_basis_device). */
 int dopinf_b200_basis(dopinf_b200_block* block, const double* tr, size_t r, double* phi);
 int dopinf_b200_basis_device(dopinf_b200_block* block, double** phi, size_t* ld);
 /* basis_rows (postprocess.cpp:12-34): out[k] = Q[rows[k]] T_r. */

@@ -19,6 +19,9 @@ ERR_COLLECTIVE = 3
 ERR_DEGENERATE_VARIABLE = 4
 ERR_DEVICE = 5
 ERR_OUT_OF_MEMORY = 6
+ERR_NOT_PSD = 7
+ERR_RANK_DEFICIENCY = 8
+ERR_SOLVE = 9
 
 SUM, MAX, MIN = 0, 1, 2
 GRAM_REDUCE_ORDERED, GRAM_REDUCE_NCCL = 0, 1
@@ -64,6 +67,9 @@ SIGNATURES = {
     "dopinf_b200_global_gram": (C.c_int, [_vp, _dp]),
     "dopinf_b200_project": (C.c_int, [_vp, _dp, C.c_size_t, C.c_size_t, _dp]),
     "dopinf_b200_project_host": (C.c_int, [_vp, _dp, _dp, C.c_size_t, C.c_size_t, _dp]),
+    "dopinf_b200_eig_sym_desc": (C.c_int, [_vp, _dp, _dp]),
+    "dopinf_b200_set_gram": (C.c_int, [_vp, _dp, C.c_size_t]),
+    "dopinf_b200_reduced_map": (C.c_int, [_vp, C.c_size_t, _dp]),
     "dopinf_b200_basis": (C.c_int, [_vp, _dp, C.c_size_t, _dp]),
     "dopinf_b200_basis_device": (C.c_int, [_vp, C.POINTER(_dp), _sp]),
     "dopinf_b200_basis_rows": (C.c_int, [_vp, _dp, C.c_size_t, _sp, C.c_size_t, _dp]),

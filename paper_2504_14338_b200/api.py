@@ -75,6 +75,9 @@ _STATUS = {
     _lib.ERR_DEGENERATE_VARIABLE: DegenerateVariableError,
     _lib.ERR_DEVICE: DeviceError,
     _lib.ERR_OUT_OF_MEMORY: DeviceError,
+    _lib.ERR_NOT_PSD: NotPsdError,
+    _lib.ERR_RANK_DEFICIENCY: RankDeficiencyError,
+    _lib.ERR_SOLVE: SolveError,
 }
 
 
@@ -311,6 +314,7 @@ def local_gram(block: LocalBlock) -> np.ndarray:
     """pod.cpp:11-13: D_i = Q_iᵀ Q_i (full symmetric nt × nt)."""
     d = np.empty((block.nt, block.nt), dtype=np.float64)
     _check(_lib.load().dopinf_b200_local_gram(block._h, _lib.dptr(d)), block.ctx, "local_gram")
+    block.ctx._gram_nt = block.nt
     return d
 
 
@@ -336,9 +340,57 @@ def project(tr, d, ctx: DeviceContext) -> np.ndarray:
     return out
 
 
-def project_resident(ctx: DeviceContext, tr, out: np.ndarray | None = None) -> np.ndarray:
-    """Q̂ = T_rᵀ D with the context's device-resident (global) Gram. `out`
-    (r × nt float64, e.g. pinned) is filled when given."""
+@dataclass
+class EigenSpectrum:
+    """pod::EigenSpectrum (pod.hpp:18-21)."""
+    eigenvalues: np.ndarray
+    eigenvectors: np.ndarray
+
+
+def eig_sym_desc(ctx: DeviceContext, vectors: bool = True) -> EigenSpectrum:
+    """pod::eig_sym_desc (pod.cpp:20-65) of the context's device Gram, on the
+    device (cuSOLVER): descending, clamped, sign-normalised."""
+    n = _device_gram_size(ctx)
+    lam = np.empty(n, dtype=np.float64)
+    vec = np.empty((n, n), dtype=np.float64) if vectors else None
+    _check(_lib.load().dopinf_b200_eig_sym_desc(ctx._h, _lib.dptr(lam), _lib.dptr(vec)), ctx, "eig_sym_desc")
+    return EigenSpectrum(lam, vec)
+
+
+def set_gram(ctx: DeviceContext, d) -> None:
+    """Make a host D (nt × nt, symmetric) the context's device Gram."""
+    d = _f64(d)
+    if d.ndim != 2 or d.shape[0] != d.shape[1]:
+        raise InvalidArgumentError("set_gram: D must be square")
+    _check(_lib.load().dopinf_b200_set_gram(ctx._h, _lib.dptr(d), d.shape[0]), ctx, "set_gram")
+    ctx._gram_nt = d.shape[0]
+
+
+def reduced_map(ctx: DeviceContext, r: int, download: bool = True):
+    """pod::reduced_map (pod.cpp:84-101) on the device; the T_r stays on the
+    context for project_resident(ctx, None) and basis(block, None, r)."""
+    n = _device_gram_size(ctx)
+    tr = np.empty((n, r), dtype=np.float64) if download else None
+    _check(_lib.load().dopinf_b200_reduced_map(ctx._h, r, _lib.dptr(tr)), ctx, "reduced_map")
+    return tr
+
+
+def _device_gram_size(ctx: DeviceContext) -> int:
+    n = getattr(ctx, "_gram_nt", None)
+    if n is None:
+        raise InvalidArgumentError("no Gram on this context")
+    return n
+
+
+def project_resident(ctx: DeviceContext, tr, out: np.ndarray | None = None, r: int | None = None) -> np.ndarray:
+    """Q̂ = T_rᵀ D with the context's device-resident (global) Gram. `tr` may be
+    None to use the device T_r of reduced_map (then pass r). `out` (r × nt
+    float64, e.g. pinned) is filled when given."""
+    if tr is None:
+        nt = _device_gram_size(ctx)
+        out = np.empty((r, nt), dtype=np.float64) if out is None else _out(out, (r, nt))
+        _check(_lib.load().dopinf_b200_project(ctx._h, None, nt, r, _lib.dptr(out)), ctx, "project")
+        return out
     tr = _f64(tr)
     nt, r = tr.shape
     out = np.empty((r, nt), dtype=np.float64) if out is None else _out(out, (r, nt))
@@ -360,12 +412,14 @@ def basis_rows(block: LocalBlock, tr, local_rows) -> np.ndarray:
     return out
 
 
-def basis(block: LocalBlock, tr, download: bool = True):
-    """Φ_r = Q·T_r over the whole block (postprocess.cpp:66), rows × r."""
-    tr = _f64(tr)
-    if tr.shape[0] != block.nt:
-        raise InvalidArgumentError("basis: block and map disagree on nt")
-    r = tr.shape[1]
+def basis(block: LocalBlock, tr, download: bool = True, r: int | None = None):
+    """Φ_r = Q·T_r over the whole block (postprocess.cpp:66), rows × r. `tr`
+    None uses the context's device T_r from reduced_map (pass r)."""
+    if tr is not None:
+        tr = _f64(tr)
+        if tr.shape[0] != block.nt:
+            raise InvalidArgumentError("basis: block and map disagree on nt")
+        r = tr.shape[1]
     out = np.empty((block.rows, r), dtype=np.float64) if download else None
     _check(_lib.load().dopinf_b200_basis(block._h, _lib.dptr(tr), r, _lib.dptr(out)), block.ctx, "basis")
     return out
@@ -381,6 +435,7 @@ def snapshot_pass(block: LocalBlock, scaling: bool, out: dict | None = None):
     d = _out(out["d"], (block.nt, block.nt)) if "d" in out else np.empty((block.nt, block.nt), dtype=np.float64)
     _check(_lib.load().dopinf_b200_snapshot_pass(block._h, 1 if scaling else 0, _lib.dptr(means),
                                                  _lib.dptr(scales), _lib.dptr(d)), block.ctx, "snapshot_pass")
+    block.ctx._gram_nt = block.nt
     params = TransformParams(means, scales if scaling else np.zeros(0), scaling)
     return params, d
 
@@ -403,6 +458,7 @@ def snapshot_pass_host(block: LocalBlock, host_values, scaling: bool, out: dict 
     rc = _lib.load().dopinf_b200_snapshot_pass_host(block._h, ptr, ld, 1 if scaling else 0, _lib.dptr(means),
                                                     _lib.dptr(scales), _lib.dptr(d))
     _check(rc, block.ctx, "snapshot_pass_host")
+    block.ctx._gram_nt = block.nt
     return TransformParams(means, scales if scaling else np.zeros(0), scaling), d
 
 
@@ -423,4 +479,5 @@ def stream_pass_synth(ctx: DeviceContext, n_vars: int, row_range: RowRange, nt: 
                                                    noise, _lib.dptr(a), 1 if scaling else 0, _lib.dptr(means),
                                                    _lib.dptr(scales), _lib.dptr(d))
     _check(rc, ctx, "stream_pass_synth")
+    ctx._gram_nt = nt
     return TransformParams(means[: n_vars * nx_i], scales if scaling else np.zeros(0), scaling), d

@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = PKG / "libdopinf_b200.so"
-SOURCES = ["capi.cu", "gram.cu", "transform.cu", "project.cu", "synth.cu"]
+SOURCES = ["capi.cu", "gram.cu", "transform.cu", "project.cu", "synth.cu", "eig.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -79,6 +79,7 @@ def build_extension(force: bool = False, verbose: bool = False) -> Path:
             cmd += [f"-L{nccl / 'lib'}", "-l:libnccl.so.2", f"-Xlinker=-rpath,{nccl / 'lib'}"]
         else:
             cmd += ["-lnccl"]
+        cmd += ["-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")

@@ -18,6 +18,7 @@
 
 #include "../../include/dopinf_b200.h"
 #include "common.cuh"
+#include "eig.h"
 #include "gram.h"
 #include "project.h"
 #include "synth.h"
@@ -187,6 +188,11 @@ struct dopinf_b200_ctx {
     // scratch
     DBuf scales, tr, trt, qhat, sel, rows_out, span;
     PinnedBuf staging;
+    // device eigensolve (dopinf_b200_eig_sym_desc / dopinf_b200_reduced_map)
+    eig::Solver solver;
+    DBuf eig_a, eig_w, eig_work, eig_info, eig_v, eig_lambda, tr_dev;
+    int eig_K = 0;      // size of the held eigendecomposition (0: none)
+    size_t tr_dev_r = 0;
 
     // Device → host copy that completes before returning (callers sync anyway).
     void d2h(void* dst, const void* src, size_t bytes, const char* what) {
@@ -601,12 +607,24 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
     }
 }
 
+// T_r operand: the caller's host T_r (uploaded) or, for tr_host == nullptr,
+// the context's device T_r from dopinf_b200_reduced_map.
+const double* tr_operand(dopinf_b200_ctx* c, const double* tr_host, size_t nt, size_t r) {
+    if (!tr_host) {
+        require(c->tr_dev_r > 0 && c->tr_dev_r == r && static_cast<size_t>(c->K) == nt,
+                "no device T_r of this shape on the context (call dopinf_b200_reduced_map)");
+        return c->tr_dev.get<double>(nt * r, "tr");
+    }
+    double* dtr = c->tr.get<double>(nt * r, "tr");
+    ck(cudaMemcpyAsync(dtr, tr_host, nt * r * sizeof(double), cudaMemcpyHostToDevice, c->stream), "tr H2D");
+    return dtr;
+}
+
 void do_project(dopinf_b200_ctx* c, const double* tr_host, const double* d_dev, size_t nt, size_t r,
                 double* qhat_host) {
     require(r >= 1 && r <= nt, "project: r must lie in [1, nt]");
-    double* dtr = c->tr.get<double>(nt * r, "tr");
+    const double* dtr = tr_operand(c, tr_host, nt, r);
     double* dq = c->qhat.get<double>(nt * r, "qhat");
-    ck(cudaMemcpyAsync(dtr, tr_host, nt * r * sizeof(double), cudaMemcpyHostToDevice, c->stream), "tr H2D");
     c->record(DOPINF_B200_STAGE_PROJECT, 0);
     ck(project::launch_project(dtr, d_dev, static_cast<int>(nt), static_cast<int>(r), dq, c->stream),
        "project");
@@ -631,6 +649,9 @@ const char* dopinf_b200_status_string(int status) {
         case DOPINF_B200_ERR_DEGENERATE_VARIABLE: return "DegenerateVariableError";
         case DOPINF_B200_ERR_DEVICE: return "DeviceError";
         case DOPINF_B200_ERR_OUT_OF_MEMORY: return "OutOfMemoryError";
+        case DOPINF_B200_ERR_NOT_PSD: return "NotPsdError";
+        case DOPINF_B200_ERR_RANK_DEFICIENCY: return "RankDeficiencyError";
+        case DOPINF_B200_ERR_SOLVE: return "SolveError";
         default: return "unknown status";
     }
 }
@@ -961,7 +982,7 @@ int dopinf_b200_global_gram(dopinf_b200_ctx* c, double* d) {
 
 int dopinf_b200_project(dopinf_b200_ctx* c, const double* tr, size_t nt, size_t r, double* qhat) {
     return guarded(c, [&] {
-        require(tr && qhat, "project: null buffers");
+        require(qhat != nullptr, "project: null buffers");
         require(c->have_gram && static_cast<size_t>(c->K) == nt,
                 "project: no Gram of matching size on this context");
         do_project(c, tr, c->dmat.get<double>(nt * nt, "D"), nt, r, qhat);
@@ -980,20 +1001,108 @@ int dopinf_b200_project_host(dopinf_b200_ctx* c, const double* tr, const double*
     });
 }
 
+int dopinf_b200_set_gram(dopinf_b200_ctx* c, const double* d, size_t nt) {
+    return guarded(c, [&] {
+        require(d != nullptr && nt >= 1 && nt <= (1u << 16), "set_gram: bad matrix");
+        const size_t nn = nt * nt;
+        ck(cudaMemcpyAsync(c->dmat.get<double>(nn, "D"), d, nn * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+           "D H2D");
+        c->K = static_cast<int>(nt);
+        c->have_gram = true;
+        c->eig_K = 0;
+        c->tr_dev_r = 0;
+        c->sync("set_gram");
+    });
+}
+
+int dopinf_b200_eig_sym_desc(dopinf_b200_ctx* c, double* lambda, double* vectors) {
+    return guarded(c, [&] {
+        require(c->have_gram && c->K > 0, "eig_sym_desc: no Gram on this context");
+        const int n = c->K;
+        const size_t nn = static_cast<size_t>(n) * n;
+        std::string err;
+        const size_t lwork = c->solver.workspace_doubles(n, &err);
+        if (!err.empty()) fail(DOPINF_B200_ERR_DEVICE, "eig_sym_desc: " + err);
+        double* a = c->eig_a.get<double>(nn, "eig scratch");
+        double* w = c->eig_w.get<double>(n, "eig w");
+        double* work = c->eig_work.get<double>(std::max<size_t>(lwork, 1), "eig work");
+        int* info = c->eig_info.get<int>(1, "eig info");
+        double* v = c->eig_v.get<double>(nn, "eig vectors");
+        double* lam = c->eig_lambda.get<double>(n, "eig lambda");
+        c->eig_K = 0;
+        c->tr_dev_r = 0;
+        if (c->solver.run(c->dmat.get<double>(nn, "D"), n, a, w, work, lwork, info, v, lam, c->stream, &err) !=
+            cudaSuccess) {
+            fail(DOPINF_B200_ERR_DEVICE, "eig_sym_desc: " + (err.empty() ? std::string("cuSOLVER failure") : err));
+        }
+        int hinfo = 0;
+        std::vector<double> hl(n);
+        c->d2h(&hinfo, info, sizeof(int), "info D2H");
+        c->d2h(hl.data(), lam, n * sizeof(double), "lambda D2H");
+        if (hinfo != 0) fail(DOPINF_B200_ERR_SOLVE, "symmetric eigendecomposition failed (dsyevd info=" +
+                                                         std::to_string(hinfo) + ")");
+        // pod.cpp:35-48: clamp round-off negatives, reject real ones.
+        const double lambda1 = hl.empty() ? 0.0 : hl.front();
+        if (lambda1 < 0.0) {
+            fail(DOPINF_B200_ERR_NOT_PSD, "Gram matrix is not positive semidefinite (largest eigenvalue is negative)");
+        }
+        const double clamp = 1e-10 * lambda1;
+        bool changed = false;
+        for (double& l : hl) {
+            if (l < -clamp) {
+                fail(DOPINF_B200_ERR_NOT_PSD, "Gram matrix has eigenvalue " + std::to_string(l) +
+                                                  " below the round-off clamp; data is corrupted");
+            }
+            if (l < 0.0) {
+                l = 0.0;
+                changed = true;
+            }
+        }
+        if (changed) {
+            ck(cudaMemcpyAsync(lam, hl.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "lambda H2D");
+        }
+        if (lambda) std::memcpy(lambda, hl.data(), n * sizeof(double));
+        if (vectors) c->d2h(vectors, v, nn * sizeof(double), "vectors D2H");
+        c->sync("eig_sym_desc");
+        c->eig_K = n;
+    });
+}
+
+int dopinf_b200_reduced_map(dopinf_b200_ctx* c, size_t r, double* tr) {
+    return guarded(c, [&] {
+        require(c->eig_K > 0 && c->eig_K == c->K, "reduced_map: no eigendecomposition on this context");
+        const size_t n = static_cast<size_t>(c->eig_K);
+        require(r >= 1 && r <= n, "reduced_map: r must lie in [1, nt]");
+        double lam_r = 0.0;
+        c->d2h(&lam_r, c->eig_lambda.get<double>(n, "eig lambda") + (r - 1), sizeof(double), "lambda D2H");
+        if (!(lam_r > 0.0)) {
+            fail(DOPINF_B200_ERR_RANK_DEFICIENCY,
+                 "reduced dimension " + std::to_string(r) + " exceeds the numerical rank of the data");
+        }
+        double* dtr = c->tr_dev.get<double>(n * r, "device T_r");
+        ck(eig::launch_reduced_map(c->eig_v.get<double>(n * n, "eig vectors"), c->eig_lambda.get<double>(n, "lambda"),
+                                   static_cast<int>(n), static_cast<int>(r), dtr, c->stream),
+           "reduced_map");
+        c->tr_dev_r = r;
+        if (tr) c->d2h(tr, dtr, n * r * sizeof(double), "T_r D2H");
+        c->sync("reduced_map");
+    });
+}
+
 int dopinf_b200_basis(dopinf_b200_block* b, const double* tr, size_t r, double* phi) {
     if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
     auto* c = b->ctx;
     return guarded(c, [&] {
-        require(tr != nullptr && r >= 1, "basis: bad map");
+        require(r >= 1, "basis: bad map");
         materialize(b);
         const int r_pad = project::basis_cols_pad(static_cast<int>(r));
-        // T_rᵀ, zero padded to r_pad rows, pitch = block pitch.
-        std::vector<double> trt(static_cast<size_t>(r_pad) * b->ld, 0.0);
-        for (size_t k = 0; k < b->nt; ++k)
-            for (size_t j = 0; j < r; ++j) trt[j * b->ld + k] = tr[k * r + j];
-        double* dtrt = c->trt.get<double>(trt.size(), "trt");
-        ck(cudaMemcpyAsync(dtrt, trt.data(), trt.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream),
-           "trt H2D");
+        // T_rᵀ, zero padded to r_pad rows, pitch = block pitch (host T_r, or the
+        // context's device T_r when tr == nullptr).
+        const double* dtr = tr_operand(c, tr, b->nt, r);
+        double* dtrt = c->trt.get<double>(static_cast<size_t>(r_pad) * b->ld, "trt");
+        ck(eig::launch_transpose_pad(dtr, static_cast<int>(b->nt), static_cast<int>(r), r_pad, b->ld, dtrt,
+                                     c->stream),
+           "T_r transpose");
         double* dphi = b->phi.get<double>(std::max<size_t>(b->rows, 1) * r_pad, "phi");
         b->phi_ld = r_pad;
         c->record(DOPINF_B200_STAGE_BASIS, 0);

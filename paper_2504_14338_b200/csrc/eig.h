@@ -1,0 +1,33 @@
+// eig.h — device eigensolve of the Gram (eig.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include <string>
+
+namespace dopinf_b200 {
+namespace eig {
+
+// nullptr when cuSOLVER can be loaded, else why not.
+const char* unavailable_reason();
+
+class Solver {
+public:
+    ~Solver();
+    size_t workspace_doubles(int n, std::string* err);
+    // v_out (n×n row-major, column k ↔ lambda_out[k]) and lambda_out (n,
+    // descending, unclamped) from the symmetric n×n d; a_scratch n×n, w n.
+    cudaError_t run(const double* d, int n, double* a_scratch, double* w, double* work_dev, size_t work_doubles,
+                    int* info_dev, double* v_out, double* lambda_out, cudaStream_t stream, std::string* err);
+
+private:
+    void* handle_ = nullptr;
+};
+
+cudaError_t launch_reduced_map(const double* v, const double* lambda, int n, int r, double* tr, cudaStream_t stream);
+cudaError_t launch_transpose_pad(const double* tr, int n, int r, int r_pad, size_t ld, double* trt,
+                                 cudaStream_t stream);
+
+}  // namespace eig
+}  // namespace dopinf_b200
