@@ -43,6 +43,9 @@ using InvalidArgumentError = ::dopinf::InvalidArgumentError;
 using PartitionError = ::dopinf::PartitionError;
 using CollectiveError = ::dopinf::CollectiveError;
 using DegenerateVariableError = ::dopinf::DegenerateVariableError;
+using NotPsdError = ::dopinf::NotPsdError;
+using RankDeficiencyError = ::dopinf::RankDeficiencyError;
+using SolveError = ::dopinf::SolveError;
 #else
 struct Error : std::runtime_error {
     explicit Error(const std::string& m) : std::runtime_error(m) {}
@@ -59,6 +62,15 @@ struct CollectiveError : Error {
 struct DegenerateVariableError : Error {
     using Error::Error;
 };
+struct NotPsdError : Error {
+    using Error::Error;
+};
+struct RankDeficiencyError : Error {
+    using Error::Error;
+};
+struct SolveError : Error {
+    using Error::Error;
+};
 #endif
 
 [[noreturn]] inline void raise(int status, const std::string& msg) {
@@ -67,6 +79,9 @@ struct DegenerateVariableError : Error {
         case DOPINF_B200_ERR_PARTITION: throw PartitionError(msg);
         case DOPINF_B200_ERR_COLLECTIVE: throw CollectiveError(msg);
         case DOPINF_B200_ERR_DEGENERATE_VARIABLE: throw DegenerateVariableError(msg);
+        case DOPINF_B200_ERR_NOT_PSD: throw NotPsdError(msg);
+        case DOPINF_B200_ERR_RANK_DEFICIENCY: throw RankDeficiencyError(msg);
+        case DOPINF_B200_ERR_SOLVE: throw SolveError(msg);
         default: throw Error(msg);
     }
 }
@@ -255,6 +270,34 @@ MatrixT global_gram(MatrixT local, CommT& comm) {
     Context::check(dopinf_b200_global_gram(detail::ctx().handle(), local.data()), detail::ctx().handle(),
                    "global_gram");
     return local;
+}
+
+// pod.cpp:20-65 on the device (cuSOLVER dsyevd + the reference's descending
+// order, clamp and sign convention). SpectrumT is the caller's
+// pod::EigenSpectrum-like type {std::vector<double> eigenvalues; MatrixT eigenvectors;}.
+template <class SpectrumT, class MatrixT>
+SpectrumT eig_sym_desc(const MatrixT& d) {
+    if (d.rows() != d.cols()) throw InvalidArgumentError("symmetric_eig: matrix is not square");
+    Context& c = detail::ctx();
+    Context::check(dopinf_b200_set_gram(c.handle(), d.data(), d.rows()), c.handle(), "eig_sym_desc");
+    SpectrumT out;
+    out.eigenvalues.resize(d.rows());
+    out.eigenvectors = MatrixT(d.rows(), d.cols());
+    const int rc = dopinf_b200_eig_sym_desc(c.handle(), out.eigenvalues.data(), out.eigenvectors.data());
+    if (rc == DOPINF_B200_ERR_NOT_PSD) throw NotPsdError(dopinf_b200_last_error(c.handle()));
+    Context::check(rc, c.handle(), "eig_sym_desc");
+    return out;
+}
+
+// pod.cpp:84-101 on the device from the last eig_sym_desc of this thread's context.
+template <class MatrixT>
+MatrixT reduced_map_device(std::size_t nt, std::size_t r) {
+    Context& c = detail::ctx();
+    MatrixT tr(nt, r);
+    const int rc = dopinf_b200_reduced_map(c.handle(), r, tr.data());
+    if (rc == DOPINF_B200_ERR_RANK_DEFICIENCY) throw RankDeficiencyError(dopinf_b200_last_error(c.handle()));
+    Context::check(rc, c.handle(), "reduced_map");
+    return tr;
 }
 
 // pod.cpp:103-105: Q̂ = T_rᵀ D, the reference's FMA order (bit-identical).

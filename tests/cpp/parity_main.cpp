@@ -195,6 +195,7 @@ int main() {
             {480, 36, 0}, {33, 20, 0}, {100, 12, 0}, {450, 48, 0}, {77, 31, 0}, {500, 50, 5}, {300, 30, 3},
             {120, 40, 10}, {64, 16, 1}, {500, 24, 8}, {90, 45, 12}, {250, 50, 2}, {48, 12, 4}};
         double gram_gap = 0, lam_gap = 0, qhat_gap = 0, rows_gap = 0, phi_gap = 0;
+        double deig_gap = 0, deig_resid = 0;  // device eig_sym_desc vs the reference's
         bool bitwise_proj = true;
         for (std::size_t i = 0; i < shapes.size(); ++i) {
             synth::Rng rng(1000 + i);
@@ -225,6 +226,20 @@ int main() {
             const Matrix dref = linalg::gram(q);
             const auto sg = pod::eig_sym_desc(dg);
             const auto sr = pod::eig_sym_desc(dref);
+            {
+                // §8(f) next row 1: the eigensolve on the device, same D
+                const auto sd = dopinf_b200::pod::eig_sym_desc<pod::EigenSpectrum>(dref);
+                const double l1 = sr.eigenvalues[0];
+                for (std::size_t k = 0; k < sr.eigenvalues.size(); ++k) {
+                    deig_gap = std::max(deig_gap, std::abs(sd.eigenvalues[k] - sr.eigenvalues[k]) / l1);
+                    // residual |D v_k - λ_k v_k|∞ / λ1 (well defined even for clustered λ)
+                    for (std::size_t i = 0; i < s.nt; ++i) {
+                        double dv = 0.0;
+                        for (std::size_t j = 0; j < s.nt; ++j) dv += dref(i, j) * sd.eigenvectors(j, k);
+                        deig_resid = std::max(deig_resid, std::abs(dv - sd.eigenvalues[k] * sd.eigenvectors(i, k)) / l1);
+                    }
+                }
+            }
             for (std::size_t k = 0; k < sr.eigenvalues.size(); ++k)
                 lam_gap = std::max(lam_gap, std::abs(sg.eigenvalues[k] - sr.eigenvalues[k]) / sr.eigenvalues[0]);
             // numerical rank from q's singular values, as acceptance.cpp:218-222
@@ -253,6 +268,8 @@ int main() {
         report(qhat_gap <= 1e-9, "sweep Q-hat end to end, sign-folded", fmt(qhat_gap) + " rel sigma1 <= 1e-9");
         report(rows_gap == 0.0, "basis_rows bit-identical to postprocess::basis_rows", "20 shapes");
         report(phi_gap <= 1e-9, "Phi_r = Q T_r vs linalg::matmul", "rel Frobenius " + fmt(phi_gap) + " <= 1e-9");
+        report(deig_gap <= 1e-10 && deig_resid <= 1e-12, "device eig_sym_desc vs pod::eig_sym_desc",
+               "eigenvalues " + fmt(deig_gap) + " rel lambda1 <= 1e-10; residual " + fmt(deig_resid) + " <= 1e-12");
     }
 
     // 4. Steps II-IV: B200 Steps II-III + reference eig/project/grid_search vs the
