@@ -23,6 +23,10 @@
  *   postprocess::reconstruct_field's Φ_r = Q·T_r (postprocess.cpp:66)
  *                                                            dopinf_b200_basis
  *   postprocess::basis_rows (postprocess.hpp:25-26)          dopinf_b200_basis_rows
+ *   data::read_header (data.hpp:52, data.cpp:133-162)        dopinf_b200_snp1_header
+ *   data::read_block (data.hpp:54, data.cpp:164-202)         dopinf_b200_block_read
+ *   pipeline::run_rank read + Steps II-III (pipeline.cpp:254-280)
+ *                                                            dopinf_b200_snapshot_pass_file
  *
  * The eigensolve (pod::eig_sym_desc), rank selection, reduced_map, the OpInf
  * solve and the ROM search stay on the reference code path: the host D
@@ -52,7 +56,8 @@ typedef enum dopinf_b200_status {
     DOPINF_B200_ERR_OUT_OF_MEMORY = 6,      /* device allocation failure (dopinf::Error)      */
     DOPINF_B200_ERR_NOT_PSD = 7,            /* NotPsdError            (errors.hpp:40-43) */
     DOPINF_B200_ERR_RANK_DEFICIENCY = 8,    /* RankDeficiencyError    (errors.hpp:46-49) */
-    DOPINF_B200_ERR_SOLVE = 9               /* SolveError             (errors.hpp:52-55) */
+    DOPINF_B200_ERR_SOLVE = 9,              /* SolveError             (errors.hpp:52-55) */
+    DOPINF_B200_ERR_DATA_FORMAT = 10        /* DataFormatError        (errors.hpp:15-18) */
 } dopinf_b200_status;
 
 /* Collective ops, same order as comm::ReduceOp (comm.hpp:9). */
@@ -231,6 +236,33 @@ int dopinf_b200_stream_pass_synth(dopinf_b200_ctx* ctx, size_t n_vars, size_t nx
                                   size_t nt, uint64_t seed, int n_modes, double dt, double noise,
                                   const double* amps, int scaling, double* means, double* scales,
                                   double* d);
+
+/* ---- SNP1 snapshot files (data.hpp:11-15) --------------------------------- */
+/* data::read_header (data.cpp:133-162): parse and validate the header of the
+ * SNP1 file at `path` (magic, n_vars/nx/nt, names, payload size) with the
+ * reference's checks and DataFormatError messages. dims receives
+ * {n_vars, nx, nt, data_offset}; `names` (capacity names_cap, may be NULL)
+ * receives the variable names NUL-terminated back to back; *names_len (may be
+ * NULL) the bytes they need. Context-free: the message of a failed call is
+ * dopinf_b200_last_error(NULL) on the calling thread. */
+int dopinf_b200_snp1_header(const char* path, uint64_t* dims, char* names, size_t names_cap,
+                            size_t* names_len);
+/* data::read_block (data.cpp:164-202): rows [row_begin, row_end) of every
+ * variable (the rank's plan entry; the C++ mirror checks the plan itself)
+ * into a new device block, each variable's slice one contiguous byte range of
+ * the file, read through a pinned two-slot ring whose H2D copies overlap the
+ * next read. */
+int dopinf_b200_block_read(dopinf_b200_ctx* ctx, const char* path, size_t row_begin, size_t row_end,
+                           dopinf_b200_block** out);
+/* Read + Steps II-III in one streamed call (pipeline.cpp:254-280): the rank's
+ * slice is read chunk by chunk into the pinned ring; while chunk c+1 is read
+ * and copied, chunk c is centered and its Gram accumulated on the device
+ * (as dopinf_b200_snapshot_pass_host). *out receives the resident, transformed
+ * block; means [n_vars*(row_end-row_begin)], scales [n_vars], d [nt x nt] as
+ * in dopinf_b200_snapshot_pass. On any error *out stays NULL. */
+int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* ctx, const char* path, size_t row_begin,
+                                   size_t row_end, int scaling, dopinf_b200_block** out, double* means,
+                                   double* scales, double* d);
 
 #ifdef __cplusplus
 }

@@ -11,6 +11,7 @@ legs import this module.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import subprocess
 from pathlib import Path
 
@@ -199,6 +200,14 @@ class _Rng:
             pass
 
 
+class RefError(RuntimeError):
+    """A reference exception: `code` as ref_bench.cpp's fail(), `msg` = what()."""
+
+    def __init__(self, code, msg):
+        super().__init__(f"reference error {code}: {msg}")
+        self.code, self.msg = code, msg
+
+
 class Reference:
     """The unmodified reference (oracle/_ref), or unavailable."""
 
@@ -229,12 +238,15 @@ class Reference:
             lib.ref_eig_reduced_map.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, _dp]
             lib.ref_grid_search.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp, C.c_size_t,
                                             C.c_double, C.c_size_t, _dp, _dp]
+            lib.ref_write_snapshots.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_char_p, _dp]
+            lib.ref_read_header.argtypes = [C.c_char_p, _sp, C.c_char_p, C.c_size_t]
+            lib.ref_read_block.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
             Reference._lib = lib
         self.lib = Reference._lib
 
     def _ok(self, rc):
         if rc != 0:
-            raise RuntimeError(f"reference error {rc}: {self.lib.ref_last_error().decode()}")
+            raise RefError(rc, self.lib.ref_last_error().decode())
 
     def backend(self) -> str:
         return self.lib.ref_backend().decode()
@@ -317,3 +329,28 @@ class Reference:
         self._ok(self.lib.ref_grid_search(_d(qhat), r, nt, _d(b1), b1.size, _d(b2), b2.size, max_growth, nt_p,
                                           _d(traj), _d(pe)))
         return traj, (pe[0], pe[1]), pe[2]
+
+    # ---- data.cpp: SNP1 container ---------------------------------------------------
+    def write_snapshots(self, path, names, variables):
+        """data::write_snapshots (data.cpp:105-131)."""
+        full = _f(np.concatenate([np.asarray(v, dtype=np.float64) for v in variables], axis=0))
+        nx, nt = np.asarray(variables[0]).shape
+        blob = b"".join(n.encode() + b"\0" for n in names)
+        self._ok(self.lib.ref_write_snapshots(os.fsencode(str(path)), len(names), nx, nt, blob, _d(full)))
+
+    def read_header(self, path):
+        """data::read_header (data.cpp:133-162) -> (n_vars, nx, nt, names)."""
+        dims = np.zeros(3, dtype=np.uintp)
+        buf = C.create_string_buffer(1 << 16)
+        self._ok(self.lib.ref_read_header(os.fsencode(str(path)), dims.ctypes.data_as(_sp), buf, len(buf)))
+        n_vars = int(dims[0])
+        names = [n.decode() for n in buf.raw.split(b"\0")[:n_vars]]
+        return n_vars, int(dims[1]), int(dims[2]), names
+
+    def read_block(self, path, p, rank):
+        """data::read_block (data.cpp:164-202) of rank `rank` of partition_rows(nx, p)."""
+        n_vars, nx, nt, _ = self.read_header(path)
+        nx_i = nx // p if rank + 1 < p else nx - (p - 1) * (nx // p)
+        out = np.empty((n_vars * nx_i, nt))
+        self._ok(self.lib.ref_read_block(os.fsencode(str(path)), p, rank, _d(out)))
+        return out

@@ -37,6 +37,7 @@ int fail(const std::exception& e) {
     if (dynamic_cast<const InvalidArgumentError*>(&e)) return 1;
     if (dynamic_cast<const NotPsdError*>(&e)) return 7;
     if (dynamic_cast<const RankDeficiencyError*>(&e)) return 8;
+    if (dynamic_cast<const DataFormatError*>(&e)) return 10;
     return 99;
 }
 
@@ -279,6 +280,61 @@ int ref_grid_search(const double* qhat, std::size_t r, std::size_t nt, const dou
             pair_err[1] = out.pair_opt.beta2;
             pair_err[2] = out.train_err;
         });
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// data::write_snapshots (data.cpp:105-131): `names` holds n_vars NUL-terminated
+// names back to back; `full` is the stacked (n_vars*nx) x nt matrix.
+int ref_write_snapshots(const char* path, std::size_t n_vars, std::size_t nx, std::size_t nt,
+                        const char* names, const double* full) {
+    try {
+        data::SnapshotHeader h;
+        h.n_vars = n_vars;
+        h.nx = nx;
+        h.nt = nt;
+        const char* p = names;
+        for (std::size_t j = 0; j < n_vars; ++j) {
+            h.var_names.emplace_back(p);
+            p += h.var_names.back().size() + 1;
+        }
+        std::vector<Matrix> vars;
+        for (std::size_t j = 0; j < n_vars; ++j) vars.push_back(to_matrix(full + j * nx * nt, nx, nt));
+        data::write_snapshots(path, h, vars);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// data::read_header (data.cpp:133-162): dims out, names back to back.
+int ref_read_header(const char* path, std::size_t* dims, char* names, std::size_t names_cap) {
+    try {
+        const data::SnapshotHeader h = data::read_header(path);
+        dims[0] = h.n_vars;
+        dims[1] = h.nx;
+        dims[2] = h.nt;
+        std::size_t at = 0;
+        for (const auto& n : h.var_names) {
+            if (at + n.size() + 1 > names_cap) return 1;
+            std::memcpy(names + at, n.c_str(), n.size() + 1);
+            at += n.size() + 1;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// data::read_block (data.cpp:164-202) for rank `rank` of partition_rows(nx, p).
+int ref_read_block(const char* path, int p, int rank, double* out) {
+    try {
+        const data::SnapshotHeader h = data::read_header(path);
+        const data::PartitionPlan plan = data::partition_rows(h.nx, p);
+        const data::LocalBlock b = data::read_block(path, plan, rank, h);
+        from_matrix(b.values, out);
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

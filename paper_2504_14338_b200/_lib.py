@@ -22,6 +22,7 @@ ERR_OUT_OF_MEMORY = 6
 ERR_NOT_PSD = 7
 ERR_RANK_DEFICIENCY = 8
 ERR_SOLVE = 9
+ERR_DATA_FORMAT = 10
 
 SUM, MAX, MIN = 0, 1, 2
 GRAM_REDUCE_ORDERED, GRAM_REDUCE_NCCL = 0, 1
@@ -77,6 +78,11 @@ SIGNATURES = {
     "dopinf_b200_snapshot_pass_host": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int, _dp, _dp, _dp]),
     "dopinf_b200_stream_pass_synth": (C.c_int, [_vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64,
                                                  C.c_int, C.c_double, C.c_double, _dp, C.c_int, _dp, _dp, _dp]),
+    "dopinf_b200_snp1_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t,
+                                          C.POINTER(C.c_size_t)]),
+    "dopinf_b200_block_read": (C.c_int, [_vp, C.c_char_p, C.c_size_t, C.c_size_t, C.POINTER(_vp)]),
+    "dopinf_b200_snapshot_pass_file": (C.c_int, [_vp, C.c_char_p, C.c_size_t, C.c_size_t, C.c_int, C.POINTER(_vp),
+                                                 _dp, _dp, _dp]),
 }
 
 _lib = None

@@ -20,6 +20,7 @@ C++ callers is include/dopinf_b200.hpp.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -78,6 +79,7 @@ _STATUS = {
     _lib.ERR_NOT_PSD: NotPsdError,
     _lib.ERR_RANK_DEFICIENCY: RankDeficiencyError,
     _lib.ERR_SOLVE: SolveError,
+    _lib.ERR_DATA_FORMAT: DataFormatError,
 }
 
 
@@ -85,7 +87,8 @@ def _check(rc: int, ctx=None, what: str = ""):
     if rc == _lib.OK:
         return
     lib = _lib.load()
-    msg = lib.dopinf_b200_last_error(ctx._h).decode() if ctx is not None else ""
+    # ctx None: context-free call, its message is thread-local in the library
+    msg = lib.dopinf_b200_last_error(ctx._h if ctx is not None else None).decode()
     raise _STATUS.get(rc, Error)(f"{what}: {msg}" if what else msg)
 
 
@@ -208,6 +211,110 @@ class DeviceContext:
         self.close()
 
 
+# ---- SNP1 snapshot files (data.hpp:11-15) -------------------------------------------
+_MAGIC = b"SNP1"
+
+
+def write_snapshots(path: str, header: SnapshotHeader, variables) -> None:
+    """data::write_snapshots (data.cpp:105-131): host-side writer of the SNP1
+    container (magic, u64 n_vars/nx/nt, u32-length names, per-variable row-major
+    nx × nt float64). Same checks and messages as the reference."""
+    _validate_header(header)
+    if len(variables) != header.n_vars:
+        raise InvalidArgumentError("write_snapshots: variable count mismatch")
+    arrs = [np.ascontiguousarray(v, dtype=np.float64) for v in variables]
+    if any(a.shape != (header.nx, header.nt) for a in arrs):
+        raise InvalidArgumentError("write_snapshots: variable shape mismatch")
+    try:
+        with open(path, "wb") as f:
+            f.write(_MAGIC)
+            f.write(np.array([header.n_vars, header.nx, header.nt], dtype="<u8").tobytes())
+            for name in header.var_names:
+                b = name.encode()
+                f.write(np.array([len(b)], dtype="<u4").tobytes())
+                f.write(b)
+            for a in arrs:
+                a.tofile(f)
+    except OSError as e:
+        raise DataFormatError(f"cannot create snapshot file: {path}") from e
+
+
+def _validate_header(h: SnapshotHeader) -> None:
+    """data.cpp:35-48."""
+    if h.n_vars < 1:
+        raise DataFormatError("snapshot header: n_vars must be >= 1")
+    if h.nx < 1:
+        raise DataFormatError("snapshot header: nx must be >= 1")
+    if h.nt < 2:
+        raise DataFormatError("snapshot header: nt must be >= 2")
+    if len(h.var_names) != h.n_vars:
+        raise DataFormatError("snapshot header: name count does not match n_vars")
+    seen = set()
+    for name in h.var_names:
+        if not name:
+            raise DataFormatError("snapshot header: empty variable name")
+        if name in seen:
+            raise DataFormatError(f"snapshot header: duplicate variable name '{name}'")
+        seen.add(name)
+
+
+def read_header(path: str) -> SnapshotHeader:
+    """data::read_header (data.cpp:133-162) through dopinf_b200_snp1_header."""
+    lib = _lib.load()
+    dims = (C.c_uint64 * 4)()
+    need = C.c_size_t()
+    bpath = os.fsencode(path)
+    _check(lib.dopinf_b200_snp1_header(bpath, dims, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(max(need.value, 1))
+    _check(lib.dopinf_b200_snp1_header(bpath, dims, buf, need.value, None))
+    names = [n.decode() for n in buf.raw[: need.value].split(b"\0")[:-1]]
+    return SnapshotHeader(int(dims[0]), int(dims[1]), int(dims[2]), names)
+
+
+def _check_plan(plan, rank: int, header: SnapshotHeader) -> RowRange:
+    """data.cpp:166-177: the plan covers [0, nx) contiguously and rank is in it."""
+    if not plan or plan[0].begin != 0 or plan[-1].end != header.nx:
+        raise PartitionError("read_block: plan does not cover the file's rows")
+    for a, b in zip(plan, plan[1:]):
+        if b.begin != a.end:
+            raise PartitionError("read_block: plan intervals are not contiguous")
+    if rank < 0 or rank >= len(plan):
+        raise PartitionError(f"read_block: rank {rank} outside plan of size {len(plan)}")
+    return plan[rank]
+
+
+def read_block(path: str, plan, rank: int, header: SnapshotHeader, ctx: DeviceContext) -> "LocalBlock":
+    """data::read_block (data.cpp:164-202) into a device-resident LocalBlock:
+    each variable's slice is one contiguous byte range of the file, read into a
+    pinned two-slot ring with the H2D of one chunk overlapping the next read."""
+    rr = _check_plan(plan, rank, header)
+    h = C.c_void_p()
+    _check(_lib.load().dopinf_b200_block_read(ctx._h, os.fsencode(path), rr.begin, rr.end, C.byref(h)), ctx,
+           "read_block")
+    return LocalBlock._adopt(ctx, h, header.n_vars, rr, header.nt, rank)
+
+
+def snapshot_pass_file(path: str, plan, rank: int, header: SnapshotHeader, ctx: DeviceContext, scaling: bool,
+                       out: dict | None = None):
+    """read_block + Steps II-III (pipeline.cpp:254-280) streamed: chunk c+1 is
+    read and copied while chunk c is centered and its Gram accumulated.
+    Returns (LocalBlock resident and transformed, TransformParams, D)."""
+    rr = _check_plan(plan, rank, header)
+    rows, nt = header.n_vars * rr.count(), header.nt
+    out = out or {}
+    means = _out(out["means"], (rows,)) if "means" in out else np.empty(max(rows, 1), dtype=np.float64)
+    scales = _out(out["scales"], (header.n_vars,)) if "scales" in out else np.empty(header.n_vars, dtype=np.float64)
+    d = _out(out["d"], (nt, nt)) if "d" in out else np.empty((nt, nt), dtype=np.float64)
+    h = C.c_void_p()
+    rc = _lib.load().dopinf_b200_snapshot_pass_file(ctx._h, os.fsencode(path), rr.begin, rr.end,
+                                                    1 if scaling else 0, C.byref(h), _lib.dptr(means),
+                                                    _lib.dptr(scales), _lib.dptr(d))
+    _check(rc, ctx, "snapshot_pass_file")
+    ctx._gram_nt = nt
+    block = LocalBlock._adopt(ctx, h, header.n_vars, rr, nt, rank)
+    return block, TransformParams(means[:rows], scales if scaling else np.zeros(0), scaling), d
+
+
 # ---- device-resident data::LocalBlock ----------------------------------------------
 class LocalBlock:
     """data::LocalBlock (data.hpp:38-42) held on the device: (n_vars·nx_i) × nt fp64,
@@ -228,6 +335,20 @@ class LocalBlock:
         self._h = h
         if values is not None:
             self.upload(values)
+
+    @classmethod
+    def _adopt(cls, ctx: DeviceContext, handle: C.c_void_p, n_vars: int, row_range: RowRange, nt: int,
+               rank: int | None = None) -> "LocalBlock":
+        """Wrap a block the library created (block_read / snapshot_pass_file)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.rank = ctx.rank() if rank is None else rank
+        self.row_range = row_range
+        self.n_vars, self.nt = n_vars, nt
+        self.nx_i = row_range.count()
+        self.rows = n_vars * self.nx_i
+        self._h = handle
+        return self
 
     def upload(self, values) -> None:
         v = _f64(values, (self.rows, self.nt))

@@ -5,6 +5,11 @@
 // and maps failures onto the reference's exception classes by status code.
 #include <nccl.h>
 
+#include <errno.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -13,6 +18,7 @@
 #include <new>
 #include <set>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -55,6 +61,9 @@ struct Fail {
 };
 
 [[noreturn]] void fail(int status, std::string msg) { throw Fail{status, std::move(msg)}; }
+
+// Message of the last failed context-free call (or null-context call) on this thread.
+thread_local std::string g_thread_err = "null context";
 
 void ck(cudaError_t e, const char* what) {
     if (e == cudaErrorMemoryAllocation) {
@@ -143,6 +152,7 @@ struct dopinf_b200_ctx {
     std::vector<cudaEvent_t> chunk_events;  // one per streamed chunk (grow-only)
     DBuf gv;                                // per-variable packed Grams of the streamed pass
     DBuf ring;                              // synth stream: two chunk slots
+    PinnedBuf file_ring;                    // SNP1 reads: two pinned chunk slots
     std::vector<cudaEvent_t> timing_events; // streamed Gram launches: start/end pairs
     size_t stream_gram_ms_events_used = 0;
     struct EvList {
@@ -231,9 +241,30 @@ struct dopinf_b200_block {
 
 namespace {
 
+// Context-free entry points: status + message on the calling thread.
+template <class F>
+int guarded_free(F&& fn) {
+    try {
+        fn();
+        return DOPINF_B200_OK;
+    } catch (const Fail& f) {
+        g_thread_err = f.msg;
+        return f.status;
+    } catch (const std::bad_alloc&) {
+        g_thread_err = "host allocation failed";
+        return DOPINF_B200_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        g_thread_err = "unexpected failure";
+        return DOPINF_B200_ERR_DEVICE;
+    }
+}
+
 template <class F>
 int guarded(dopinf_b200_ctx* ctx, F&& fn) {
-    if (!ctx) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    if (!ctx) {
+        g_thread_err = "null context";
+        return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    }
     try {
         DeviceGuard dg(ctx->device);
         fn();
@@ -444,6 +475,138 @@ constexpr long long kStreamSplitRows = 2048;    // rows per Gram item inside a h
 constexpr long long kSynthChunkRows = 262144;   // rows per generated chunk (3.1 GB at K = 1500)
 constexpr long long kSynthSplitRows = 8192;
 
+// ---- SNP1 snapshot files (reference data.hpp:11-15, data.cpp) ----------------
+// "SNP1", little-endian u64 n_vars / nx / nt, names as u32 length + bytes,
+// then per variable an nx x nt row-major fp64 matrix: a rank's rows of one
+// variable are one contiguous byte range.
+struct Snp1 {
+    uint64_t n_vars = 0, nx = 0, nt = 0, data_offset = 0, file_bytes = 0;
+    std::vector<std::string> names;
+};
+
+[[noreturn]] void format_fail(const std::string& msg) { fail(DOPINF_B200_ERR_DATA_FORMAT, msg); }
+
+struct Fd {
+    int fd = -1;
+    Fd() = default;
+    Fd(const Fd&) = delete;
+    Fd& operator=(const Fd&) = delete;
+    ~Fd() {
+        if (fd >= 0) close(fd);
+    }
+};
+
+// Exactly `bytes` at `off`, or false (EOF / error).
+bool pread_all(int fd, void* dst, size_t bytes, uint64_t off) {
+    auto* p = static_cast<char*>(dst);
+    while (bytes > 0) {
+        const ssize_t n = pread(fd, p, bytes, static_cast<off_t>(off));
+        if (n < 0 && errno == EINTR) continue;
+        if (n <= 0) return false;
+        p += n;
+        bytes -= static_cast<size_t>(n);
+        off += static_cast<uint64_t>(n);
+    }
+    return true;
+}
+
+void open_snp1(Fd& f, const std::string& path) {
+    f.fd = open(path.c_str(), O_RDONLY | O_CLOEXEC);
+    if (f.fd < 0) format_fail("cannot open snapshot file: " + path);  // data.cpp:61-65
+}
+
+// data.cpp:35-48 (same checks, same order, same messages).
+void validate_snp1(const Snp1& h) {
+    if (h.n_vars < 1) format_fail("snapshot header: n_vars must be >= 1");
+    if (h.nx < 1) format_fail("snapshot header: nx must be >= 1");
+    if (h.nt < 2) format_fail("snapshot header: nt must be >= 2");
+    if (h.names.size() != h.n_vars) format_fail("snapshot header: name count does not match n_vars");
+    std::set<std::string> seen;
+    for (const auto& name : h.names) {
+        if (name.empty()) format_fail("snapshot header: empty variable name");
+        if (!seen.insert(name).second) format_fail("snapshot header: duplicate variable name '" + name + "'");
+    }
+}
+
+// data.cpp:69-82: a payload shorter than the header promises names the
+// variable the missing bytes belong to.
+void check_snp1_payload(const Snp1& h, const std::string& path) {
+    const unsigned __int128 per_var = static_cast<unsigned __int128>(h.nx) * h.nt * sizeof(double);
+    const unsigned __int128 expected = h.data_offset + h.n_vars * per_var;
+    if (h.file_bytes < expected) {
+        const uint64_t have = h.file_bytes - std::min(h.file_bytes, h.data_offset);
+        const uint64_t var =
+            static_cast<uint64_t>(std::min<unsigned __int128>(have / per_var, h.n_vars - 1));
+        format_fail("snapshot file truncated in variable '" + h.names[var] + "': " + path);
+    }
+}
+
+// data::read_header (data.cpp:133-162).
+Snp1 read_snp1_header(int fd, const std::string& path) {
+    struct stat st;
+    if (fstat(fd, &st) != 0) format_fail("cannot open snapshot file: " + path);
+    Snp1 h;
+    h.file_bytes = static_cast<uint64_t>(st.st_size);
+    char magic[4] = {};
+    if (!pread_all(fd, magic, 4, 0) || std::memcmp(magic, "SNP1", 4) != 0) {
+        format_fail("not a snapshot file (bad magic): " + path);
+    }
+    uint64_t off = 4;
+    auto u64 = [&](const char* field) {
+        uint64_t v = 0;
+        if (!pread_all(fd, &v, sizeof v, off)) format_fail(std::string("snapshot file truncated in ") + field);
+        off += sizeof v;
+        return v;
+    };
+    h.n_vars = u64("n_vars");
+    h.nx = u64("nx");
+    h.nt = u64("nt");
+    if (h.n_vars > (1u << 20)) format_fail("snapshot header: implausible n_vars");
+    for (uint64_t j = 0; j < h.n_vars; ++j) {
+        const std::string where = "snapshot file truncated in name of variable " + std::to_string(j);
+        uint32_t len = 0;
+        if (!pread_all(fd, &len, sizeof len, off)) format_fail(where);
+        off += sizeof len;
+        if (off + len > h.file_bytes) format_fail(where);  // before allocating `len` bytes
+        std::string name(len, '\0');
+        if (!pread_all(fd, name.data(), len, off)) format_fail(where);
+        off += len;
+        h.names.push_back(std::move(name));
+    }
+    h.data_offset = off;  // data.cpp:51-58: 4 + 3*8 + sum(4 + len)
+    validate_snp1(h);
+    check_snp1_payload(h, path);
+    return h;
+}
+
+// Reader threads per chunk: a page-cache or NVMe read of a few hundred MB is
+// bound by one core's memcpy, so the byte range is split over several.
+int file_reader_threads() {
+    static const int n = [] {
+        const unsigned hw = std::thread::hardware_concurrency();
+        return static_cast<int>(std::max(1u, std::min(16u, hw / 2)));
+    }();
+    return n;
+}
+
+// pread `bytes` at `off` into `dst` on up to file_reader_threads() threads.
+bool pread_parallel(int fd, void* dst, size_t bytes, uint64_t off) {
+    constexpr size_t kPiece = size_t(8) << 20;
+    const int n = static_cast<int>(std::min<size_t>(file_reader_threads(), (bytes + kPiece - 1) / kPiece));
+    if (n <= 1) return pread_all(fd, dst, bytes, off);
+    const size_t per = (bytes / n + 4095) / 4096 * 4096;
+    std::vector<std::thread> threads;
+    std::vector<char> ok(n, 0);
+    for (int i = 0; i < n; ++i) {
+        const size_t b0 = std::min(bytes, per * i), b1 = std::min(bytes, per * (i + 1));
+        threads.emplace_back([&, i, b0, b1] {
+            ok[i] = pread_all(fd, static_cast<char*>(dst) + b0, b1 - b0, off + b0) ? 1 : 0;
+        });
+    }
+    for (auto& t : threads) t.join();
+    return std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
+}
+
 struct StreamChunk {
     int var;
     long long r0, rows;
@@ -458,7 +621,32 @@ struct StreamSource {
     int n_modes = 0;
     double dt = 0.0, noise = 0.0;
     const double* amps = nullptr;  // host [n_vars] or null
+    int fd = -1;                   // SNP1 file rows → pinned ring → resident block
+    const Snp1* file = nullptr;
+    const std::string* path = nullptr;
 };
+
+// File source: read chunk k of the block's rows into pinned ring slot k % 2
+// and enqueue its H2D on the copy stream; chunk_events[k] marks the copy done
+// (the compute stream waits on it; the read of chunk k + 2 into the same slot
+// waits on it from the host).
+void file_chunk_h2d(dopinf_b200_block* b, const StreamSource& src, const std::vector<StreamChunk>& chunks,
+                    size_t k, double* ring, size_t slot_doubles) {
+    auto* c = b->ctx;
+    const StreamChunk& ch = chunks[k];
+    if (k >= 2) ck(cudaEventSynchronize(c->chunk_events[k - 2]), "ring slot");
+    double* slot = ring + (k % 2) * slot_doubles;
+    const uint64_t local0 = static_cast<uint64_t>(ch.r0) - static_cast<uint64_t>(ch.var) * b->nx_i;
+    const uint64_t first = static_cast<uint64_t>(ch.var) * src.file->nx + b->row_begin + local0;
+    const size_t bytes = static_cast<size_t>(ch.rows) * b->nt * sizeof(double);
+    if (!pread_parallel(src.fd, slot, bytes, src.file->data_offset + first * b->nt * sizeof(double))) {
+        format_fail("snapshot file truncated in variable '" + src.file->names[ch.var] + "': " + *src.path);
+    }
+    ck(cudaMemcpy2DAsync(b->q + ch.r0 * b->ld, b->ld * sizeof(double), slot, b->nt * sizeof(double),
+                         b->nt * sizeof(double), ch.rows, cudaMemcpyHostToDevice, c->copy_stream),
+       "chunk H2D");
+    ck(cudaEventRecord(c->chunk_events[k], c->copy_stream), "event");
+}
 
 std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b, long long chunk_rows) {
     std::vector<StreamChunk> out;
@@ -508,6 +696,11 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
     double* packed = c->packed.get<double>(count, "packed");
     double* ring = src.synth ? c->ring.get<double>(2 * static_cast<size_t>(first_rows) * b->ld, "chunk ring")
                              : nullptr;
+    const bool from_file = src.fd >= 0;
+    const size_t slot_doubles = static_cast<size_t>(first_rows) * b->nt;
+    double* fring = from_file && !chunks.empty()
+                        ? static_cast<double*>(c->file_ring.get(2 * slot_doubles * sizeof(double)))
+                        : nullptr;
     std::vector<double> amps_v;  // per-variable amplitude slice for the generator
     if (src.synth && src.amps) amps_v.assign(src.amps, src.amps + b->n_vars);
     c->stream_gram_ms_events.clear();
@@ -520,7 +713,8 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
         cudaEvent_t ready = c->chunk_events[chunks.size()];
         ck(cudaEventRecord(ready, c->stream), "event");
         ck(cudaStreamWaitEvent(c->copy_stream, ready, 0), "event wait");
-        for (size_t k = 0; k < chunks.size(); ++k) {
+        if (from_file && !chunks.empty()) file_chunk_h2d(b, src, chunks, 0, fring, slot_doubles);
+        for (size_t k = 0; !from_file && k < chunks.size(); ++k) {
             const StreamChunk& ch = chunks[k];
             ck(cudaMemcpy2DAsync(b->q + ch.r0 * b->ld, b->ld * sizeof(double), src.host + ch.r0 * src.host_ld,
                                  src.host_ld * sizeof(double), b->nt * sizeof(double), ch.rows,
@@ -578,7 +772,11 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
                 }
             }
         }
+        // the host reads chunk k + 1 while the device copies and reduces chunk k
+        if (from_file && k + 1 < chunks.size()) file_chunk_h2d(b, src, chunks, k + 1, fring, slot_doubles);
     }
+    // the pinned ring is free for the next call once the last copy has landed
+    if (from_file && !chunks.empty()) ck(cudaEventSynchronize(c->chunk_events[chunks.size() - 1]), "ring");
     if (b->rows == 0 && scaling) {  // an empty rank still joins the MAX collectives
         for (size_t v = 0; v < b->n_vars; ++v) {
             if (c->size > 1) {
@@ -605,6 +803,31 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
             }
         }
     }
+}
+
+// data::read_block (data.cpp:164-202) into the device block: the file rows go
+// through the pinned ring, each H2D overlapping the next chunk's read.
+void do_block_read(dopinf_b200_block* b, const StreamSource& src) {
+    auto* c = b->ctx;
+    b->pending_center = false;
+    b->stats_valid = false;
+    const std::vector<StreamChunk> chunks = stream_chunks(b, kStreamChunkRows);
+    if (chunks.empty()) return;
+    while (c->chunk_events.size() < chunks.size() + 1) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        c->chunk_events.push_back(e);
+    }
+    const size_t slot_doubles = static_cast<size_t>(std::min<long long>(kStreamChunkRows, b->nx_i)) * b->nt;
+    auto* fring = static_cast<double*>(c->file_ring.get(2 * slot_doubles * sizeof(double)));
+    c->record(DOPINF_B200_STAGE_UPLOAD, 0);
+    cudaEvent_t ready = c->chunk_events[chunks.size()];
+    ck(cudaEventRecord(ready, c->stream), "event");
+    ck(cudaStreamWaitEvent(c->copy_stream, ready, 0), "event wait");
+    for (size_t k = 0; k < chunks.size(); ++k) file_chunk_h2d(b, src, chunks, k, fring, slot_doubles);
+    ck(cudaStreamWaitEvent(c->stream, c->chunk_events[chunks.size() - 1], 0), "event wait");
+    c->record(DOPINF_B200_STAGE_UPLOAD, 1);
+    ck(cudaEventSynchronize(c->chunk_events[chunks.size() - 1]), "ring");
 }
 
 // T_r operand: the caller's host T_r (uploaded) or, for tr_host == nullptr,
@@ -652,6 +875,7 @@ const char* dopinf_b200_status_string(int status) {
         case DOPINF_B200_ERR_NOT_PSD: return "NotPsdError";
         case DOPINF_B200_ERR_RANK_DEFICIENCY: return "RankDeficiencyError";
         case DOPINF_B200_ERR_SOLVE: return "SolveError";
+        case DOPINF_B200_ERR_DATA_FORMAT: return "DataFormatError";
         default: return "unknown status";
     }
 }
@@ -728,6 +952,7 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
         b->release();
     }
     c->staging.release();
+    c->file_ring.release();
     c->gv.release();
     c->ring.release();
     for (cudaEvent_t e : c->chunk_events) cudaEventDestroy(e);
@@ -743,7 +968,7 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
 
 int dopinf_b200_ctx_rank(const dopinf_b200_ctx* c) { return c ? c->rank : -1; }
 int dopinf_b200_ctx_size(const dopinf_b200_ctx* c) { return c ? c->size : -1; }
-const char* dopinf_b200_last_error(const dopinf_b200_ctx* c) { return c ? c->err.c_str() : "null context"; }
+const char* dopinf_b200_last_error(const dopinf_b200_ctx* c) { return c ? c->err.c_str() : g_thread_err.c_str(); }
 void* dopinf_b200_ctx_stream(dopinf_b200_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
 int dopinf_b200_set_gram_reduce(dopinf_b200_ctx* c, int mode) {
@@ -1195,6 +1420,111 @@ int dopinf_b200_snapshot_pass_host(dopinf_b200_block* b, const double* host, siz
         do_global_gram(c, d);
         c->sync("snapshot_pass_host");
     });
+}
+
+int dopinf_b200_snp1_header(const char* path, uint64_t* dims, char* names, size_t names_cap,
+                            size_t* names_len) {
+    return guarded_free([&] {
+        require(path && dims, "snp1_header: null path or dims");
+        Fd f;
+        open_snp1(f, path);
+        const Snp1 h = read_snp1_header(f.fd, path);
+        dims[0] = h.n_vars;
+        dims[1] = h.nx;
+        dims[2] = h.nt;
+        dims[3] = h.data_offset;
+        size_t need = 0;
+        for (const auto& n : h.names) need += n.size() + 1;
+        if (names_len) *names_len = need;
+        if (names) {
+            require(names_cap >= need, "snp1_header: names buffer too small");
+            size_t at = 0;
+            for (const auto& n : h.names) {
+                std::memcpy(names + at, n.c_str(), n.size() + 1);
+                at += n.size() + 1;
+            }
+        }
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Open + validate the file and create the device block of rows
+// [row_begin, row_end) of every variable (pipeline.cpp:254-258).
+dopinf_b200_block* open_file_block(dopinf_b200_ctx* c, const char* path, size_t row_begin, size_t row_end,
+                                   Fd& f, Snp1& h) {
+    require(path != nullptr, "null path");
+    open_snp1(f, path);
+    h = read_snp1_header(f.fd, path);
+    if (row_begin > row_end || row_end > h.nx) {
+        fail(DOPINF_B200_ERR_PARTITION, "read_block: rows [" + std::to_string(row_begin) + ", " +
+                                            std::to_string(row_end) + ") outside the file's " +
+                                            std::to_string(h.nx) + " rows");
+    }
+    require(h.nt <= (1u << 20), "snapshot file: nt too large");
+    dopinf_b200_block* b = nullptr;
+    const int rc = dopinf_b200_block_create(c, h.n_vars, row_end - row_begin, row_begin, h.nt, &b);
+    if (rc != DOPINF_B200_OK) fail(rc, c->err);
+    return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dopinf_b200_block_read(dopinf_b200_ctx* c, const char* path, size_t row_begin, size_t row_end,
+                           dopinf_b200_block** out) {
+    if (!out) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    dopinf_b200_block* b = nullptr;
+    const int rc = guarded(c, [&] {
+        Fd f;
+        Snp1 h;
+        b = open_file_block(c, path, row_begin, row_end, f, h);
+        StreamSource src;
+        src.fd = f.fd;
+        src.file = &h;
+        const std::string p(path);
+        src.path = &p;
+        do_block_read(b, src);
+        c->sync("block_read");
+    });
+    if (rc != DOPINF_B200_OK) {
+        dopinf_b200_block_destroy(b);
+        return rc;
+    }
+    *out = b;
+    return DOPINF_B200_OK;
+}
+
+int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* c, const char* path, size_t row_begin, size_t row_end,
+                                   int scaling, dopinf_b200_block** out, double* means, double* scales,
+                                   double* d) {
+    if (!out) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    dopinf_b200_block* b = nullptr;
+    const int rc = guarded(c, [&] {
+        Fd f;
+        Snp1 h;
+        b = open_file_block(c, path, row_begin, row_end, f, h);
+        StreamSource src;
+        src.fd = f.fd;
+        src.file = &h;
+        const std::string p(path);
+        src.path = &p;
+        do_stream_pass(b, src, scaling != 0, means, scales);
+        unpack(c);
+        do_global_gram(c, d);
+        c->sync("snapshot_pass_file");
+    });
+    if (rc != DOPINF_B200_OK) {
+        dopinf_b200_block_destroy(b);
+        return rc;
+    }
+    *out = b;
+    return DOPINF_B200_OK;
 }
 
 int dopinf_b200_stream_pass_synth(dopinf_b200_ctx* c, size_t n_vars, size_t nx_i, size_t row_begin, size_t nt,
