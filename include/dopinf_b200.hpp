@@ -11,6 +11,9 @@
 //   dopinf_b200::postprocess::basis_rows(block, tr, rows)        postprocess.hpp:25-26
 //   dopinf_b200::postprocess::basis(block, tr)  (Φ_r of reconstruct_field, postprocess.cpp:66)
 //   dopinf_b200::data::partition_rows(nx, p)                     data.hpp:47
+//   dopinf_b200::data::read_header<HeaderT>(path)                data.hpp:52
+//   dopinf_b200::data::read_block<LocalBlockT>(path, plan, rank, header)  data.hpp:54
+//   dopinf_b200::data::read_block_device(path, plan, rank, header)  (the same rows, left on the device)
 //
 // The functions are templates over the caller's block / matrix / header types
 // (duck-typed on the members the reference's data::LocalBlock, Matrix and
@@ -27,6 +30,7 @@
 #pragma once
 
 #include <cstddef>
+#include <cstdint>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -46,6 +50,7 @@ using DegenerateVariableError = ::dopinf::DegenerateVariableError;
 using NotPsdError = ::dopinf::NotPsdError;
 using RankDeficiencyError = ::dopinf::RankDeficiencyError;
 using SolveError = ::dopinf::SolveError;
+using DataFormatError = ::dopinf::DataFormatError;
 #else
 struct Error : std::runtime_error {
     explicit Error(const std::string& m) : std::runtime_error(m) {}
@@ -71,6 +76,9 @@ struct RankDeficiencyError : Error {
 struct SolveError : Error {
     using Error::Error;
 };
+struct DataFormatError : Error {
+    using Error::Error;
+};
 #endif
 
 [[noreturn]] inline void raise(int status, const std::string& msg) {
@@ -82,6 +90,7 @@ struct SolveError : Error {
         case DOPINF_B200_ERR_NOT_PSD: throw NotPsdError(msg);
         case DOPINF_B200_ERR_RANK_DEFICIENCY: throw RankDeficiencyError(msg);
         case DOPINF_B200_ERR_SOLVE: throw SolveError(msg);
+        case DOPINF_B200_ERR_DATA_FORMAT: throw DataFormatError(msg);
         default: throw Error(msg);
     }
 }
@@ -119,9 +128,11 @@ public:
     }
 
     static void check(int rc, const dopinf_b200_ctx* c, const char* what) {
-        if (rc != DOPINF_B200_OK) {
-            raise(rc, std::string(what) + ": " + (c ? dopinf_b200_last_error(c) : dopinf_b200_status_string(rc)));
-        }
+        if (rc != DOPINF_B200_OK) raise(rc, std::string(what) + ": " + dopinf_b200_last_error(c));
+    }
+    // The library's message unchanged (the reference's own text for data::).
+    static void check_exact(int rc, const dopinf_b200_ctx* c) {
+        if (rc != DOPINF_B200_OK) raise(rc, dopinf_b200_last_error(c));
     }
 
 private:
@@ -161,6 +172,8 @@ public:
     DeviceBlock(const DeviceBlock&) = delete;
     DeviceBlock& operator=(const DeviceBlock&) = delete;
     DeviceBlock(DeviceBlock&& o) noexcept : ctx_(o.ctx_), b_(o.b_) { o.b_ = nullptr; }
+    // Take ownership of a block the library created (dopinf_b200_block_read).
+    DeviceBlock(Context& c, dopinf_b200_block* owned) : ctx_(c), b_(owned) {}
 
     void upload(const double* host, std::size_t ld) {
         Context::check(dopinf_b200_block_upload(b_, host, ld), ctx_.handle(), "upload");
@@ -209,6 +222,64 @@ std::vector<RowRangeT> partition_rows(std::size_t nx, int p) {
         plan[r].end = e[r];
     }
     return plan;
+}
+
+// data::read_header (data.cpp:133-162): same checks, same DataFormatError text.
+template <class HeaderT>
+HeaderT read_header(const std::string& path) {
+    std::uint64_t dims[4] = {};
+    std::size_t need = 0;
+    Context::check_exact(dopinf_b200_snp1_header(path.c_str(), dims, nullptr, 0, &need), nullptr);
+    std::vector<char> names(need + 1);
+    Context::check_exact(dopinf_b200_snp1_header(path.c_str(), dims, names.data(), names.size(), nullptr), nullptr);
+    HeaderT h;
+    h.n_vars = dims[0];
+    h.nx = dims[1];
+    h.nt = dims[2];
+    h.var_names.clear();
+    for (std::size_t at = 0; at < need; at += h.var_names.back().size() + 1) h.var_names.emplace_back(&names[at]);
+    return h;
+}
+
+namespace detail {
+// data.cpp:166-177: the plan covers [0, nx) contiguously and rank lies in it.
+template <class PlanT, class HeaderT>
+void check_plan(const PlanT& plan, int rank, const HeaderT& header) {
+    if (plan.empty() || plan.front().begin != 0 || plan.back().end != header.nx) {
+        throw PartitionError("read_block: plan does not cover the file's rows");
+    }
+    for (std::size_t r = 1; r < plan.size(); ++r) {
+        if (plan[r].begin != plan[r - 1].end) throw PartitionError("read_block: plan intervals are not contiguous");
+    }
+    if (rank < 0 || static_cast<std::size_t>(rank) >= plan.size()) {
+        throw PartitionError("read_block: rank " + std::to_string(rank) + " outside plan of size " +
+                             std::to_string(plan.size()));
+    }
+}
+}  // namespace detail
+
+// The rank's rows of every variable, read through the pinned ring straight
+// into a device block (no host Matrix).
+template <class PlanT, class HeaderT>
+DeviceBlock read_block_device(const std::string& path, const PlanT& plan, int rank, const HeaderT& header) {
+    detail::check_plan(plan, rank, header);
+    Context& c = ::dopinf_b200::detail::ctx();
+    dopinf_b200_block* b = nullptr;
+    const auto& range = plan[static_cast<std::size_t>(rank)];
+    Context::check_exact(dopinf_b200_block_read(c.handle(), path.c_str(), range.begin, range.end, &b), c.handle());
+    return DeviceBlock(c, b);
+}
+
+// data::read_block (data.cpp:164-202) with the reference's return type.
+template <class LocalBlockT, class PlanT, class HeaderT>
+LocalBlockT read_block(const std::string& path, const PlanT& plan, int rank, const HeaderT& header) {
+    DeviceBlock d = read_block_device(path, plan, rank, header);
+    LocalBlockT block;
+    block.rank = rank;
+    block.row_range = plan[static_cast<std::size_t>(rank)];
+    block.values = decltype(block.values)(header.n_vars * block.row_range.count(), header.nt);
+    d.download(block.values.data(), header.nt);
+    return block;
 }
 }  // namespace data
 
@@ -278,7 +349,7 @@ MatrixT global_gram(MatrixT local, CommT& comm) {
 template <class SpectrumT, class MatrixT>
 SpectrumT eig_sym_desc(const MatrixT& d) {
     if (d.rows() != d.cols()) throw InvalidArgumentError("symmetric_eig: matrix is not square");
-    Context& c = detail::ctx();
+    Context& c = ::dopinf_b200::detail::ctx();
     Context::check(dopinf_b200_set_gram(c.handle(), d.data(), d.rows()), c.handle(), "eig_sym_desc");
     SpectrumT out;
     out.eigenvalues.resize(d.rows());
@@ -292,7 +363,7 @@ SpectrumT eig_sym_desc(const MatrixT& d) {
 // pod.cpp:84-101 on the device from the last eig_sym_desc of this thread's context.
 template <class MatrixT>
 MatrixT reduced_map_device(std::size_t nt, std::size_t r) {
-    Context& c = detail::ctx();
+    Context& c = ::dopinf_b200::detail::ctx();
     MatrixT tr(nt, r);
     const int rc = dopinf_b200_reduced_map(c.handle(), r, tr.data());
     if (rc == DOPINF_B200_ERR_RANK_DEFICIENCY) throw RankDeficiencyError(dopinf_b200_last_error(c.handle()));

@@ -6,7 +6,10 @@
 // for the B200 ones and checks them against the unmodified reference on the
 // same bytes, printing one PASS/FAIL line per check like
 // tests/acceptance.cpp. Exit status 0 iff all pass. Needs one B200.
+#include <unistd.h>
+
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -182,6 +185,55 @@ int main() {
             }
         });
         report(thrown, "DegenerateVariableError names the variable", "dopinf::DegenerateVariableError");
+    }
+
+    // 2b. SNP1 files (test_data.cpp's round trip): the reference writes, both read.
+    //     read_header identical, read_block bitwise for every rank, and a
+    //     truncated file throws DataFormatError with the reference's text.
+    {
+        const std::string path = "/tmp/dopinf_b200_parity.snp";
+        synth::Rng rng(31);
+        data::SnapshotHeader h;
+        h.n_vars = 3;
+        h.nx = 70001;
+        h.nt = 5;
+        h.var_names = {"rho", "u", "energy"};
+        std::vector<Matrix> vars;
+        for (int j = 0; j < 3; ++j) vars.push_back(random_matrix(rng, h.nx, h.nt));
+        data::write_snapshots(path, h, vars);
+        const data::SnapshotHeader hr = data::read_header(path);
+        const auto hg = dopinf_b200::data::read_header<data::SnapshotHeader>(path);
+        bool ok = hr.n_vars == hg.n_vars && hr.nx == hg.nx && hr.nt == hg.nt && hr.var_names == hg.var_names;
+        for (int p : {1, 3, 8}) {
+            const data::PartitionPlan plan = data::partition_rows(h.nx, p);
+            for (int rank = 0; rank < p; ++rank) {
+                const data::LocalBlock r = data::read_block(path, plan, rank, hr);
+                const auto g = dopinf_b200::data::read_block<data::LocalBlock>(path, plan, rank, hg);
+                ok = ok && g.values == r.values && g.row_range == r.row_range && g.rank == r.rank;
+            }
+        }
+        std::string ref_msg, b200_msg;
+        {
+            // cut the file inside variable 'u'
+            std::FILE* f = std::fopen(path.c_str(), "r+b");
+            const long cut = 4 + 24 + (4 + 3) + (4 + 1) + (4 + 6) + static_cast<long>(h.nx * h.nt * 8) + 800;
+            ok = ok && f != nullptr && ftruncate(fileno(f), cut) == 0;
+            if (f) std::fclose(f);
+            try {
+                (void)data::read_header(path);
+            } catch (const DataFormatError& e) {
+                ref_msg = e.what();
+            }
+            try {
+                (void)dopinf_b200::data::read_header<data::SnapshotHeader>(path);
+            } catch (const DataFormatError& e) {
+                b200_msg = e.what();
+            }
+        }
+        std::remove(path.c_str());
+        ok = ok && !ref_msg.empty() && ref_msg == b200_msg;
+        report(ok, "SNP1 read_header / read_block identical to data.cpp",
+               "p in {1,3,8} bitwise; truncated: \"" + b200_msg + "\"");
     }
 
     // 3. acceptance.cpp sweep (20 shapes, seeds 1000+i): Gram vs the reference at
