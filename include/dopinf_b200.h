@@ -27,6 +27,8 @@
  *   data::read_block (data.hpp:54, data.cpp:164-202)         dopinf_b200_block_read
  *   pipeline::run_rank read + Steps II-III (pipeline.cpp:254-280)
  *                                                            dopinf_b200_snapshot_pass_file
+ *   postprocess::reconstruct_field (postprocess.cpp:63-70)   dopinf_b200_reconstruct_field
+ *   Step V field_rank<r>.snp1 output (pipeline.cpp:330-350) dopinf_b200_write_field
  *
  * The eigensolve (pod::eig_sym_desc), rank selection, reduced_map, the OpInf
  * solve and the ROM search stay on the reference code path: the host D
@@ -93,7 +95,8 @@ typedef enum dopinf_b200_stage {
     DOPINF_B200_STAGE_DOWNLOAD = 10,
     DOPINF_B200_STAGE_STREAM = 11,    /* whole streamed pass (first H2D -> D ready) */
     DOPINF_B200_STAGE_STREAM_GRAM = 12,/* sum of the streamed pass's Gram launches */
-    DOPINF_B200_STAGE_COUNT = 13
+    DOPINF_B200_STAGE_FIELD = 13,     /* Φ_r·Q̃ᵀ + inverse transform (reconstruct_field) */
+    DOPINF_B200_STAGE_COUNT = 14
 } dopinf_b200_stage;
 
 typedef struct dopinf_b200_ctx dopinf_b200_ctx;
@@ -263,6 +266,32 @@ int dopinf_b200_block_read(dopinf_b200_ctx* ctx, const char* path, size_t row_be
 int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* ctx, const char* path, size_t row_begin,
                                    size_t row_end, int scaling, dopinf_b200_block** out, double* means,
                                    double* scales, double* d);
+
+/* ---- Step V: field reconstruction (postprocess.hpp:40-45) ----------------- */
+/* postprocess::reconstruct_field (postprocess.cpp:63-70): this rank's field
+ * (n_vars*nx_i) x nt_p in original coordinates,
+ *   field = inverse_transform_block(matmul_nt(Q·T_r, Q̃))  (transform.cpp:62-72),
+ * i.e. X[row][t] = s_row · (Φ_r[row]·Q̃[t]) + mean_row with one FMA. The block
+ * must hold the transformed values (after a snapshot pass). tr: host K x r, or
+ * NULL for the context's device T_r (dopinf_b200_reduced_map). qtilde: host
+ * nt_p x r (the ROM trajectory, rows = time). means [rows] and scales [n_vars]
+ * are the TransformParams (scales ignored unless scaling). field: host
+ * (rows x nt_p) or NULL to keep it on the device (dopinf_b200_field_device).
+ * Φ_r is left on the device as after dopinf_b200_basis. */
+int dopinf_b200_reconstruct_field(dopinf_b200_block* block, const double* tr, size_t r, const double* qtilde,
+                                  size_t nt_p, const double* means, const double* scales, int scaling,
+                                  double* field);
+/* Device pointer and pitch (elements) of the last reconstructed field. */
+int dopinf_b200_field_device(dopinf_b200_block* block, double** field, size_t* ld);
+/* Step V field output (pipeline.cpp:330-350): reconstruct_field + write_snapshots
+ * of the SNP1 file `path` (n_vars, nx = nx_i, nt = nt_p; `names` = n_vars
+ * NUL-terminated names back to back), streamed: row chunks of the field are
+ * computed on the device, copied into a pinned ring and written while the next
+ * chunk computes — the whole field is never resident. Header checks and
+ * messages as data::write_snapshots (DataFormatError). */
+int dopinf_b200_write_field(dopinf_b200_block* block, const double* tr, size_t r, const double* qtilde,
+                            size_t nt_p, const double* means, const double* scales, int scaling, const char* names,
+                            const char* path);
 
 #ifdef __cplusplus
 }

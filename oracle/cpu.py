@@ -72,6 +72,7 @@ class Oracle:
             lib.oracle_allreduce_sum.argtypes = [_dp, C.c_int, C.c_size_t, _dp]
             lib.oracle_matmul_tn.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
             lib.oracle_matmul.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
+            lib.oracle_matmul_nt.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
             lib.oracle_basis_rows.restype = C.c_long
             lib.oracle_basis_rows.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _sp, C.c_size_t, _dp]
             lib.oracle_partition_rows.restype = C.c_int
@@ -158,6 +159,16 @@ class Oracle:
         self.lib.oracle_matmul(_d(a), a.shape[0], a.shape[1], _d(b), b.shape[1], _d(out))
         return out
 
+    def matmul_nt(self, a, b):
+        a, b = _f(a), _f(b)
+        out = np.empty((a.shape[0], b.shape[0]))
+        self.lib.oracle_matmul_nt(_d(a), a.shape[0], a.shape[1], _d(b), b.shape[0], _d(out))
+        return out
+
+    def reconstruct_field(self, q, tr, qtilde, means, scales, nx_i, scaling):
+        """postprocess.cpp:63-70: inverse_transform_block(matmul_nt(matmul(q, tr), qtilde))."""
+        return self.inverse_transform(self.matmul_nt(self.matmul(q, tr), qtilde), nx_i, means, scales, scaling)
+
     def basis_rows(self, q, tr, rows):
         q, tr = _f(q), _f(tr)
         sel = np.ascontiguousarray(rows, dtype=np.uintp)
@@ -241,6 +252,8 @@ class Reference:
             lib.ref_write_snapshots.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_char_p, _dp]
             lib.ref_read_header.argtypes = [C.c_char_p, _sp, C.c_char_p, C.c_size_t]
             lib.ref_read_block.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
+            lib.ref_reconstruct_field.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp,
+                                                  C.c_size_t, _dp, _dp, C.c_int, _dp]
             Reference._lib = lib
         self.lib = Reference._lib
 
@@ -353,4 +366,14 @@ class Reference:
         nx_i = nx // p if rank + 1 < p else nx - (p - 1) * (nx // p)
         out = np.empty((n_vars * nx_i, nt))
         self._ok(self.lib.ref_read_block(os.fsencode(str(path)), p, rank, _d(out)))
+        return out
+
+    def reconstruct_field(self, q, n_vars, tr, qtilde, means, scales, scaling):
+        """postprocess::reconstruct_field (postprocess.cpp:63-70) on one rank's block."""
+        q, tr, qt = _f(q), _f(tr), _f(qtilde)
+        rows, nt = q.shape
+        out = np.empty((rows, qt.shape[0]))
+        sc = _f(scales) if scaling else np.zeros(max(n_vars, 1))
+        self._ok(self.lib.ref_reconstruct_field(_d(q), n_vars, rows // n_vars, nt, _d(tr), tr.shape[1], _d(qt),
+                                                qt.shape[0], _d(_f(means)), _d(sc), 1 if scaling else 0, _d(out)))
         return out

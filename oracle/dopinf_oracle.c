@@ -135,7 +135,10 @@ void oracle_k_axpy(double a, const double* x, double* y, size_t n) {
 }
 
 /* kernels_avx2.cpp:32-46 dot_avx2: two 4-lane FMA accumulators over blocks
- * of 8, one over a trailing block of 4, hsum(acc0 + acc1), scalar tail. */
+ * of 8, one over a trailing block of 4, hsum(acc0 + acc1), scalar tail. The
+ * tail `acc += a[i] * b[i]` is NOT contracted by the reference's compiler
+ * (vmulsd + vaddsd in the compiled kernels_avx2.o, unlike the axpy and
+ * scale_shift tails): rounded product, then the add. */
 double oracle_k_dot(const double* a, const double* b, size_t n) {
     double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
     size_t i = 0;
@@ -151,7 +154,7 @@ double oracle_k_dot(const double* a, const double* b, size_t n) {
     double v[4];
     for (int l = 0; l < 4; ++l) v[l] = c0[l] + c1[l];
     double acc = (v[0] + v[2]) + (v[1] + v[3]);
-    for (; i < n; ++i) acc = fma(a[i], b[i], acc);
+    for (; i < n; ++i) acc = acc + a[i] * b[i];
     return acc;
 }
 
@@ -256,6 +259,14 @@ void oracle_matmul(const double* a, size_t m, size_t k, const double* b, size_t 
     memset(c, 0, m * nb * sizeof(double));
     for (size_t i = 0; i < m; ++i) {
         for (size_t l = 0; l < k; ++l) oracle_k_axpy(a[i * k + l], b + l * nb, c + i * nb, nb);
+    }
+}
+
+/* linalg.cpp:39-48 matmul_nt (postprocess::reconstruct_field, postprocess.cpp:67):
+ * c(i, j) = kernels::dot(a.row(i), b.row(j)); a is m x k, b is n x k. */
+void oracle_matmul_nt(const double* a, size_t m, size_t k, const double* b, size_t n, double* c) {
+    for (size_t i = 0; i < m; ++i) {
+        for (size_t j = 0; j < n; ++j) c[i * n + j] = oracle_k_dot(a + i * k, b + j * k, k);
     }
 }
 

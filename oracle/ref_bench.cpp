@@ -341,4 +341,25 @@ int ref_read_block(const char* path, int p, int rank, double* out) {
     }
 }
 
+// postprocess::reconstruct_field (postprocess.cpp:63-70) on one rank's
+// transformed block q ((n_vars*nx_i) x nt) with T_r (nt x r), Q̃ (nt_p x r).
+int ref_reconstruct_field(const double* q, std::size_t n_vars, std::size_t nx_i, std::size_t nt, const double* tr,
+                          std::size_t r, const double* qtilde, std::size_t nt_p, const double* means,
+                          const double* scales, int scaling, double* out) {
+    try {
+        data::LocalBlock block;
+        block.row_range = {0, nx_i};
+        block.values = to_matrix(q, n_vars * nx_i, nt);
+        transform::TransformParams params;
+        params.local_means.assign(means, means + n_vars * nx_i);
+        if (scaling) params.scales.assign(scales, scales + n_vars);
+        params.scaling_enabled = scaling != 0;
+        from_matrix(postprocess::reconstruct_field(block, to_matrix(tr, nt, r), to_matrix(qtilde, nt_p, r), params),
+                    out);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 }  // extern "C"

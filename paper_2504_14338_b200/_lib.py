@@ -28,7 +28,7 @@ SUM, MAX, MIN = 0, 1, 2
 GRAM_REDUCE_ORDERED, GRAM_REDUCE_NCCL = 0, 1
 
 STAGES = ["upload", "stats", "scales", "apply", "gram", "gram_reduce", "allreduce", "unpack",
-          "project", "basis", "download", "stream", "stream_gram"]
+          "project", "basis", "download", "stream", "stream_gram", "field"]
 UNIQUE_ID_BYTES = 128
 
 _dp = C.POINTER(C.c_double)
@@ -80,6 +80,10 @@ SIGNATURES = {
                                                  C.c_int, C.c_double, C.c_double, _dp, C.c_int, _dp, _dp, _dp]),
     "dopinf_b200_snp1_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t,
                                           C.POINTER(C.c_size_t)]),
+    "dopinf_b200_reconstruct_field": (C.c_int, [_vp, _dp, C.c_size_t, _dp, C.c_size_t, _dp, _dp, C.c_int, _dp]),
+    "dopinf_b200_field_device": (C.c_int, [_vp, C.POINTER(_dp), C.POINTER(C.c_size_t)]),
+    "dopinf_b200_write_field": (C.c_int, [_vp, _dp, C.c_size_t, _dp, C.c_size_t, _dp, _dp, C.c_int, C.c_char_p,
+                                          C.c_char_p]),
     "dopinf_b200_block_read": (C.c_int, [_vp, C.c_char_p, C.c_size_t, C.c_size_t, C.POINTER(_vp)]),
     "dopinf_b200_snapshot_pass_file": (C.c_int, [_vp, C.c_char_p, C.c_size_t, C.c_size_t, C.c_int, C.POINTER(_vp),
                                                  _dp, _dp, _dp]),

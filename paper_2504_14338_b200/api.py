@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -164,6 +165,7 @@ class DeviceContext:
                                          f"{lib.dopinf_b200_status_string(rc).decode()}")
         self._h = h
         self._rank, self._size, self.device = rank, size, device
+        self._blocks = weakref.WeakSet()  # destroyed before the context
         self.set_gram_reduce(gram_reduce)
 
     @staticmethod
@@ -201,6 +203,8 @@ class DeviceContext:
 
     def close(self):
         if getattr(self, "_h", None):
+            for b in list(getattr(self, "_blocks", ())):
+                b.close()
             _lib.load().dopinf_b200_ctx_destroy(self._h)
             self._h = None
 
@@ -333,6 +337,7 @@ class LocalBlock:
         _check(lib.dopinf_b200_block_create(ctx._h, n_vars, self.nx_i, row_range.begin, nt, C.byref(h)), ctx,
                "block_create")
         self._h = h
+        ctx._blocks.add(self)
         if values is not None:
             self.upload(values)
 
@@ -348,6 +353,7 @@ class LocalBlock:
         self.nx_i = row_range.count()
         self.rows = n_vars * self.nx_i
         self._h = handle
+        ctx._blocks.add(self)
         return self
 
     def upload(self, values) -> None:
@@ -544,6 +550,62 @@ def basis(block: LocalBlock, tr, download: bool = True, r: int | None = None):
     out = np.empty((block.rows, r), dtype=np.float64) if download else None
     _check(_lib.load().dopinf_b200_basis(block._h, _lib.dptr(tr), r, _lib.dptr(out)), block.ctx, "basis")
     return out
+
+
+def _field_args(block: LocalBlock, tr, qtilde, params: TransformParams, r: int | None, what: str):
+    if tr is not None:
+        tr = _f64(tr)
+        if tr.shape[0] != block.nt:
+            raise InvalidArgumentError(f"{what}: block and map disagree on nt")
+        r = tr.shape[1]
+    qt = _f64(qtilde)
+    if qt.ndim != 2 or qt.shape[1] != r:
+        raise InvalidArgumentError(f"{what}: trajectory must be nt_p x r")
+    means = _f64(params.local_means, (block.rows,))
+    scales = _f64(params.scales, (block.n_vars,)) if params.scaling_enabled else None
+    return tr, r, qt, means, scales
+
+
+def reconstruct_field(block: LocalBlock, tr, qtilde, params: TransformParams, download: bool = True,
+                      r: int | None = None, out: np.ndarray | None = None):
+    """postprocess::reconstruct_field (postprocess.cpp:63-70): this rank's field
+    (n_vars·nx_i) × nt_p in original coordinates, X = s·(Q·T_r)·Q̃ᵀ + mean, on
+    the device (DMMA, inverse transform fused). `tr` None uses the context's
+    device T_r (pass r). download=False keeps the field on the device
+    (`field_device`)."""
+    tr, r, qt, means, scales = _field_args(block, tr, qtilde, params, r, "reconstruct_field")
+    nt_p = qt.shape[0]
+    if download:
+        out = _out(out, (block.rows, nt_p)) if out is not None else np.empty((block.rows, nt_p), dtype=np.float64)
+    else:
+        out = None
+    rc = _lib.load().dopinf_b200_reconstruct_field(block._h, _lib.dptr(tr), r, _lib.dptr(qt), nt_p,
+                                                   _lib.dptr(means), _lib.dptr(scales),
+                                                   1 if params.scaling_enabled else 0, _lib.dptr(out))
+    _check(rc, block.ctx, "reconstruct_field")
+    return out
+
+
+def field_device(block: LocalBlock):
+    """(device pointer, pitch in elements) of the last reconstructed field."""
+    p = _lib._dp()
+    ld = C.c_size_t()
+    _check(_lib.load().dopinf_b200_field_device(block._h, C.byref(p), C.byref(ld)), block.ctx, "field_device")
+    return C.cast(p, C.c_void_p).value, ld.value
+
+
+def write_field(block: LocalBlock, tr, qtilde, params: TransformParams, var_names, path: str,
+                r: int | None = None) -> None:
+    """Step V field output (pipeline.cpp:330-350): reconstruct_field streamed
+    straight into the SNP1 file `path` (n_vars, nx = nx_i, nt = nt_p)."""
+    tr, r, qt, means, scales = _field_args(block, tr, qtilde, params, r, "write_field")
+    if len(var_names) != block.n_vars:
+        raise DataFormatError("snapshot header: name count does not match n_vars")
+    names = b"".join(n.encode() + b"\0" for n in var_names)
+    rc = _lib.load().dopinf_b200_write_field(block._h, _lib.dptr(tr), r, _lib.dptr(qt), qt.shape[0],
+                                             _lib.dptr(means), _lib.dptr(scales),
+                                             1 if params.scaling_enabled else 0, names, os.fsencode(path))
+    _check(rc, block.ctx, "write_field")
 
 
 def snapshot_pass(block: LocalBlock, scaling: bool, out: dict | None = None):

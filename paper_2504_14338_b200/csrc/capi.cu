@@ -25,6 +25,7 @@
 #include "../../include/dopinf_b200.h"
 #include "common.cuh"
 #include "eig.h"
+#include "field.h"
 #include "gram.h"
 #include "project.h"
 #include "synth.h"
@@ -153,6 +154,8 @@ struct dopinf_b200_ctx {
     DBuf gv;                                // per-variable packed Grams of the streamed pass
     DBuf ring;                              // synth stream: two chunk slots
     PinnedBuf file_ring;                    // SNP1 reads: two pinned chunk slots
+    std::vector<cudaEvent_t> chunk_events2; // field writer: compute-done events
+    DBuf field_qt, field_means, field_scales, field_ring;
     std::vector<cudaEvent_t> timing_events; // streamed Gram launches: start/end pairs
     size_t stream_gram_ms_events_used = 0;
     struct EvList {
@@ -231,8 +234,9 @@ struct dopinf_b200_block {
     dopinf_b200_ctx* ctx = nullptr;
     size_t n_vars = 0, nx_i = 0, row_begin = 0, nt = 0, ld = 0, rows = 0;
     double* q = nullptr;
-    DBuf means, varmax, phi;
+    DBuf means, varmax, phi, field;
     int phi_ld = 0;
+    size_t field_ld = 0;  // pitch of the last reconstructed field (0: none)
     bool pending_center = false;  // means computed, subtraction not yet applied
     bool stats_valid = false;     // varmax describes the current (logical) values
     CUtensorMap gram_map{};
@@ -855,6 +859,221 @@ void do_project(dopinf_b200_ctx* c, const double* tr_host, const double* d_dev, 
     if (qhat_host) c->d2h(qhat_host, dq, nt * r * sizeof(double), "qhat D2H");
 }
 
+// Φ_r = Q·T_r into b->phi (pitch basis_cols_pad(r), columns ≥ r zero);
+// returns the pitch. T_r from the host, or the context's device T_r (NULL).
+int do_basis(dopinf_b200_block* b, const double* tr, size_t r) {
+    auto* c = b->ctx;
+    require(r >= 1, "basis: bad map");
+    materialize(b);
+    const int r_pad = project::basis_cols_pad(static_cast<int>(r));
+    // T_rᵀ, zero padded to r_pad rows, pitch = block pitch
+    const double* dtr = tr_operand(c, tr, b->nt, r);
+    double* dtrt = c->trt.get<double>(static_cast<size_t>(r_pad) * b->ld, "trt");
+    ck(eig::launch_transpose_pad(dtr, static_cast<int>(b->nt), static_cast<int>(r), r_pad, b->ld, dtrt,
+                                 c->stream),
+       "T_r transpose");
+    double* dphi = b->phi.get<double>(std::max<size_t>(b->rows, 1) * r_pad, "phi");
+    b->phi_ld = r_pad;
+    c->record(DOPINF_B200_STAGE_BASIS, 0);
+    if (b->rows > 0) {
+        ck(project::launch_basis(b->q, b->ld, static_cast<long long>(b->rows), static_cast<int>(b->nt), dtrt,
+                                 b->ld, r_pad, dphi, c->num_sms, c->stream),
+           "basis");
+    }
+    c->record(DOPINF_B200_STAGE_BASIS, 1);
+    return r_pad;
+}
+
+// Field operands on the device: Q̃ (nt_p × r) padded to the Φ_r pitch with
+// zeros, the means and (scaling) the scales of the transform.
+struct FieldOperands {
+    const double* qt = nullptr;
+    const double* means = nullptr;
+    const double* scales = nullptr;
+    size_t nt_p = 0;
+    int r_pad = 0;
+};
+
+FieldOperands field_operands(dopinf_b200_block* b, const double* qtilde, size_t r, size_t nt_p, int r_pad,
+                             const double* means, const double* scales, bool scaling) {
+    auto* c = b->ctx;
+    FieldOperands f;
+    f.nt_p = nt_p;
+    f.r_pad = r_pad;
+    double* dqt = c->field_qt.get<double>(nt_p * r_pad, "qtilde");
+    ck(cudaMemsetAsync(dqt, 0, nt_p * r_pad * sizeof(double), c->stream), "memset");
+    ck(cudaMemcpy2DAsync(dqt, r_pad * sizeof(double), qtilde, r * sizeof(double), r * sizeof(double), nt_p,
+                         cudaMemcpyHostToDevice, c->stream),
+       "qtilde H2D");
+    f.qt = dqt;
+    if (b->rows > 0) {
+        double* dm = c->field_means.get<double>(b->rows, "field means");
+        ck(cudaMemcpyAsync(dm, means, b->rows * sizeof(double), cudaMemcpyHostToDevice, c->stream), "means H2D");
+        f.means = dm;
+    }
+    if (scaling) {
+        double* ds = c->field_scales.get<double>(b->n_vars, "field scales");
+        ck(cudaMemcpyAsync(ds, scales, b->n_vars * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+           "scales H2D");
+        f.scales = ds;
+    }
+    return f;
+}
+
+// Field rows [row0, row0 + nrows) → out (pitch ldo). Widths beyond the
+// kernel's resident Φ_r tile run as k-slabs accumulated in `out`, the inverse
+// transform applied with the last one.
+void do_field_rows(dopinf_b200_block* b, const FieldOperands& f, long long row0, long long nrows, double* out,
+                   size_t ldo) {
+    auto* c = b->ctx;
+    const int slab = field::max_r_pad();
+    const double* phi = static_cast<const double*>(b->phi.p) + static_cast<size_t>(row0) * f.r_pad;
+    for (int k0 = 0; k0 < f.r_pad; k0 += slab) {
+        const int w = std::min(slab, f.r_pad - k0);
+        const bool last = k0 + w == f.r_pad;
+        ck(field::launch_field(phi + k0, f.r_pad, f.qt + k0, f.r_pad, nrows, static_cast<int>(f.nt_p), w,
+                               last && f.means ? f.means + row0 : nullptr, last ? f.scales : nullptr,
+                               static_cast<long long>(b->nx_i), row0, out, ldo, k0 > 0 ? 1 : 0, c->num_sms,
+                               c->stream),
+           "field");
+    }
+}
+
+void ensure_events(std::vector<cudaEvent_t>& v, size_t n) {
+    while (v.size() < n) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        v.push_back(e);
+    }
+}
+
+// rows × cols doubles, device pitch dev_ld → host pitch host_ld. Pinned
+// destinations take one copy; pageable ones go through two pinned slots, the
+// host copy of one slot overlapping the D2H of the next. Synchronous.
+void d2h_2d(dopinf_b200_ctx* c, double* host, size_t host_ld, const double* dev, size_t dev_ld, size_t rows,
+            size_t cols, const char* what) {
+    if (rows == 0) return;
+    if (is_pinned(host)) {
+        ck(cudaMemcpy2DAsync(host, host_ld * sizeof(double), dev, dev_ld * sizeof(double), cols * sizeof(double),
+                             rows, cudaMemcpyDeviceToHost, c->stream),
+           what);
+        ck(cudaStreamSynchronize(c->stream), what);
+        return;
+    }
+    const size_t slot_rows = std::max<size_t>(1, (size_t(64) << 20) / (cols * sizeof(double)));
+    auto* st = static_cast<double*>(c->staging.get(2 * slot_rows * cols * sizeof(double)));
+    const size_t n = (rows + slot_rows - 1) / slot_rows;
+    ensure_events(c->chunk_events2, 2);
+    auto drain = [&](size_t k) {
+        const size_t r0 = k * slot_rows, nr = std::min(slot_rows, rows - r0);
+        ck(cudaEventSynchronize(c->chunk_events2[k % 2]), what);
+        const double* src = st + (k % 2) * slot_rows * cols;
+        if (host_ld == cols) {
+            std::memcpy(host + r0 * cols, src, nr * cols * sizeof(double));
+        } else {
+            for (size_t i = 0; i < nr; ++i) std::memcpy(host + (r0 + i) * host_ld, src + i * cols, cols * sizeof(double));
+        }
+    };
+    for (size_t k = 0; k < n; ++k) {
+        const size_t r0 = k * slot_rows, nr = std::min(slot_rows, rows - r0);
+        ck(cudaMemcpy2DAsync(st + (k % 2) * slot_rows * cols, cols * sizeof(double), dev + r0 * dev_ld,
+                             dev_ld * sizeof(double), cols * sizeof(double), nr, cudaMemcpyDeviceToHost, c->stream),
+           what);
+        ck(cudaEventRecord(c->chunk_events2[k % 2], c->stream), "event");
+        if (k > 0) drain(k - 1);
+    }
+    drain(n - 1);
+}
+
+// pwrite `bytes` at `off` from `src` on up to file_reader_threads() threads.
+bool pwrite_parallel(int fd, const void* src, size_t bytes, uint64_t off) {
+    auto write_all = [fd](const char* p, size_t n, uint64_t o) {
+        while (n > 0) {
+            const ssize_t w = pwrite(fd, p, n, static_cast<off_t>(o));
+            if (w < 0 && errno == EINTR) continue;
+            if (w <= 0) return false;
+            p += w;
+            n -= static_cast<size_t>(w);
+            o += static_cast<uint64_t>(w);
+        }
+        return true;
+    };
+    constexpr size_t kPiece = size_t(8) << 20;
+    const int n = static_cast<int>(std::min<size_t>(file_reader_threads(), (bytes + kPiece - 1) / kPiece));
+    if (n <= 1) return write_all(static_cast<const char*>(src), bytes, off);
+    const size_t per = (bytes / n + 4095) / 4096 * 4096;
+    std::vector<std::thread> threads;
+    std::vector<char> ok(n, 0);
+    for (int i = 0; i < n; ++i) {
+        const size_t b0 = std::min(bytes, per * i), b1 = std::min(bytes, per * (i + 1));
+        threads.emplace_back([&, i, b0, b1] {
+            ok[i] = write_all(static_cast<const char*>(src) + b0, b1 - b0, off + b0) ? 1 : 0;
+        });
+    }
+    for (auto& t : threads) t.join();
+    return std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
+}
+
+// Stream the field into an SNP1 file: chunk k is computed into device slot
+// k % 2, copied (copy stream) into pinned slot k % 2, and written by the host
+// while chunk k + 1 computes. Layout = data::write_snapshots (data.cpp:118-129):
+// the field's rows are the variables' rows in order.
+void write_field_file(dopinf_b200_block* b, const FieldOperands& f, const Snp1& h, const std::string& path) {
+    auto* c = b->ctx;
+    Fd fd;
+    fd.fd = open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+    if (fd.fd < 0) format_fail("cannot create snapshot file: " + path);
+    std::string head("SNP1");
+    for (uint64_t v : {h.n_vars, h.nx, h.nt}) head.append(reinterpret_cast<const char*>(&v), sizeof v);
+    for (const auto& n : h.names) {
+        const uint32_t len = static_cast<uint32_t>(n.size());
+        head.append(reinterpret_cast<const char*>(&len), sizeof len);
+        head += n;
+    }
+    if (!pwrite_parallel(fd.fd, head.data(), head.size(), 0)) format_fail("write failed: " + path);
+    const uint64_t data_off = head.size();
+    const size_t nt_p = f.nt_p, ldo = (nt_p + 1) / 2 * 2, rows = b->rows;
+    size_t ch = std::max<size_t>(128, (size_t(256) << 20) / (nt_p * sizeof(double))) / 128 * 128;
+    ch = std::min(ch, (rows + 127) / 128 * 128);
+    const size_t n = (rows + ch - 1) / ch;
+    double* dring = c->field_ring.get<double>(2 * ch * ldo, "field ring");
+    auto* hring = static_cast<double*>(c->file_ring.get(2 * ch * nt_p * sizeof(double)));
+    ensure_events(c->chunk_events, n + 1);
+    ensure_events(c->chunk_events2, n + 1);
+    cudaEvent_t* computed = c->chunk_events2.data();
+    cudaEvent_t* copied = c->chunk_events.data();
+    auto flush = [&](size_t k) {  // host: write chunk k from pinned slot k % 2
+        const size_t r0 = k * ch, nr = std::min(ch, rows - r0);
+        ck(cudaEventSynchronize(copied[k]), "field D2H");
+        if (!pwrite_parallel(fd.fd, hring + (k % 2) * ch * nt_p, nr * nt_p * sizeof(double),
+                             data_off + r0 * nt_p * sizeof(double))) {
+            format_fail("write failed: " + path);
+        }
+    };
+    c->record(DOPINF_B200_STAGE_FIELD, 0);
+    for (size_t k = 0; k < n; ++k) {
+        const size_t r0 = k * ch, nr = std::min(ch, rows - r0);
+        double* dslot = dring + (k % 2) * ch * ldo;
+        if (k >= 2) ck(cudaStreamWaitEvent(c->stream, copied[k - 2], 0), "event wait");  // slot drained
+        do_field_rows(b, f, static_cast<long long>(r0), static_cast<long long>(nr), dslot, ldo);
+        ck(cudaEventRecord(computed[k], c->stream), "event");
+        ck(cudaStreamWaitEvent(c->copy_stream, computed[k], 0), "event wait");
+        ck(cudaMemcpy2DAsync(hring + (k % 2) * ch * nt_p, nt_p * sizeof(double), dslot, ldo * sizeof(double),
+                             nt_p * sizeof(double), nr, cudaMemcpyDeviceToHost, c->copy_stream),
+           "field D2H");
+        ck(cudaEventRecord(copied[k], c->copy_stream), "event");
+        if (k > 0) flush(k - 1);  // pinned slot (k-1) % 2 is reused by chunk k + 1
+    }
+    if (n > 0) flush(n - 1);
+    c->record(DOPINF_B200_STAGE_FIELD, 1);
+    if (close(fd.fd) != 0) {
+        fd.fd = -1;
+        format_fail("write failed: " + path);
+    }
+    fd.fd = -1;
+}
+
+
 }  // namespace
 
 extern "C" {
@@ -948,7 +1167,9 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
         if (pair[1]) cudaEventDestroy(pair[1]);
     }
     for (DBuf* b : {&c->tiles, &c->work, &c->counters, &c->packed, &c->gather, &c->dmat, &c->dhost_in,
-                    &c->scales, &c->tr, &c->trt, &c->qhat, &c->sel, &c->rows_out, &c->span}) {
+                    &c->scales, &c->tr, &c->trt, &c->qhat, &c->sel, &c->rows_out, &c->span, &c->eig_a,
+                    &c->eig_w, &c->eig_work, &c->eig_info, &c->eig_v, &c->eig_lambda, &c->tr_dev, &c->field_qt,
+                    &c->field_means, &c->field_scales, &c->field_ring}) {
         b->release();
     }
     c->staging.release();
@@ -956,6 +1177,7 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
     c->gv.release();
     c->ring.release();
     for (cudaEvent_t e : c->chunk_events) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->chunk_events2) cudaEventDestroy(e);
     for (cudaEvent_t e : c->timing_events) cudaEventDestroy(e);
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);
@@ -1080,6 +1302,7 @@ void dopinf_b200_block_destroy(dopinf_b200_block* b) {
     b->means.release();
     b->varmax.release();
     b->phi.release();
+    b->field.release();
     cudaSetDevice(prev);
     delete b;
 }
@@ -1318,28 +1541,10 @@ int dopinf_b200_basis(dopinf_b200_block* b, const double* tr, size_t r, double* 
     if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
     auto* c = b->ctx;
     return guarded(c, [&] {
-        require(r >= 1, "basis: bad map");
-        materialize(b);
-        const int r_pad = project::basis_cols_pad(static_cast<int>(r));
-        // T_rᵀ, zero padded to r_pad rows, pitch = block pitch (host T_r, or the
-        // context's device T_r when tr == nullptr).
-        const double* dtr = tr_operand(c, tr, b->nt, r);
-        double* dtrt = c->trt.get<double>(static_cast<size_t>(r_pad) * b->ld, "trt");
-        ck(eig::launch_transpose_pad(dtr, static_cast<int>(b->nt), static_cast<int>(r), r_pad, b->ld, dtrt,
-                                     c->stream),
-           "T_r transpose");
-        double* dphi = b->phi.get<double>(std::max<size_t>(b->rows, 1) * r_pad, "phi");
-        b->phi_ld = r_pad;
-        c->record(DOPINF_B200_STAGE_BASIS, 0);
-        if (b->rows > 0) {
-            ck(project::launch_basis(b->q, b->ld, static_cast<long long>(b->rows), static_cast<int>(b->nt),
-                                     dtrt, b->ld, r_pad, dphi, c->num_sms, c->stream),
-               "basis");
-        }
-        c->record(DOPINF_B200_STAGE_BASIS, 1);
+        const int r_pad = do_basis(b, tr, r);
         if (phi && b->rows > 0) {
             c->record(DOPINF_B200_STAGE_DOWNLOAD, 0);
-            ck(cudaMemcpy2DAsync(phi, r * sizeof(double), dphi, r_pad * sizeof(double), r * sizeof(double),
+            ck(cudaMemcpy2DAsync(phi, r * sizeof(double), b->phi.p, r_pad * sizeof(double), r * sizeof(double),
                                  b->rows, cudaMemcpyDeviceToHost, c->stream),
                "phi D2H");
             c->record(DOPINF_B200_STAGE_DOWNLOAD, 1);
@@ -1354,6 +1559,66 @@ int dopinf_b200_basis_device(dopinf_b200_block* b, double** phi, size_t* ld) {
         require(b->phi_ld > 0, "basis_device: no basis computed");
         *phi = static_cast<double*>(b->phi.p);
         *ld = static_cast<size_t>(b->phi_ld);
+    });
+}
+
+int dopinf_b200_reconstruct_field(dopinf_b200_block* b, const double* tr, size_t r, const double* qtilde,
+                                  size_t nt_p, const double* means, const double* scales, int scaling,
+                                  double* field) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(qtilde != nullptr && nt_p >= 1, "reconstruct_field: null or empty trajectory");
+        require(b->rows == 0 || means != nullptr, "reconstruct_field: null means");
+        require(!scaling || scales != nullptr, "reconstruct_field: null scales");
+        const int r_pad = do_basis(b, tr, r);
+        const FieldOperands f = field_operands(b, qtilde, r, nt_p, r_pad, means, scales, scaling != 0);
+        const size_t ldo = (nt_p + 1) / 2 * 2;
+        double* out = b->field.get<double>(std::max<size_t>(b->rows, 1) * ldo, "field");
+        b->field_ld = ldo;
+        c->record(DOPINF_B200_STAGE_FIELD, 0);
+        if (b->rows > 0) do_field_rows(b, f, 0, static_cast<long long>(b->rows), out, ldo);
+        c->record(DOPINF_B200_STAGE_FIELD, 1);
+        if (field && b->rows > 0) {
+            c->record(DOPINF_B200_STAGE_DOWNLOAD, 0);
+            d2h_2d(c, field, nt_p, out, ldo, b->rows, nt_p, "field D2H");
+            c->record(DOPINF_B200_STAGE_DOWNLOAD, 1);
+        }
+        c->sync("reconstruct_field");
+    });
+}
+
+int dopinf_b200_field_device(dopinf_b200_block* b, double** field, size_t* ld) {
+    if (!b || !field || !ld) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    return guarded(b->ctx, [&] {
+        require(b->field_ld > 0, "field_device: no field reconstructed");
+        *field = static_cast<double*>(b->field.p);
+        *ld = b->field_ld;
+    });
+}
+
+int dopinf_b200_write_field(dopinf_b200_block* b, const double* tr, size_t r, const double* qtilde, size_t nt_p,
+                            const double* means, const double* scales, int scaling, const char* names,
+                            const char* path) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(names != nullptr && path != nullptr, "write_field: null names or path");
+        require(qtilde != nullptr, "write_field: null trajectory");
+        require(b->rows == 0 || means != nullptr, "write_field: null means");
+        require(!scaling || scales != nullptr, "write_field: null scales");
+        // the header write_snapshots would write (pipeline.cpp:333-337), same checks (data.cpp:105-107)
+        Snp1 h;
+        h.n_vars = b->n_vars;
+        h.nx = b->nx_i;
+        h.nt = nt_p;
+        for (const char* p = names; h.names.size() < b->n_vars; p += h.names.back().size() + 1) {
+            h.names.emplace_back(p);
+        }
+        validate_snp1(h);
+        const int r_pad = do_basis(b, tr, r);
+        const FieldOperands f = field_operands(b, qtilde, r, nt_p, r_pad, means, scales, scaling != 0);
+        write_field_file(b, f, h, path);
     });
 }
 

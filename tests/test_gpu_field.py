@@ -1,0 +1,135 @@
+"""Step V field reconstruction on the B200 through the C ABI
+(dopinf_b200_reconstruct_field / _write_field) against the UNMODIFIED
+reference's postprocess::reconstruct_field (postprocess.cpp:63-70) on the same
+transformed block, T_r and trajectory Q̃.
+
+Tolerance: the field is s·(Q·T_r)·Q̃ᵀ + mean; Φ_r = Q·T_r runs on the FP64
+tensor pipe (north star: Φ_r within 1e-9 of the reference), the contraction
+with Q̃ too, so the field is held to the same order: relative Frobenius error
+≤ FIELD_TOL = 1e-10 against the reference (observed ~1e-15). The inverse
+transform itself is one FMA per entry, exactly the reference's scale_shift."""
+import struct
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIELD_TOL = 1e-10
+
+
+def api():
+    from paper_2504_14338_b200 import api as a
+
+    return a
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _setup(ctx, oracle, nv, nx, nt, r, nt_p, scaling, seed):
+    a = api()
+    rng = oracle.rng(seed)
+    raw = rng.matrix(nv * nx, nt) * np.repeat(10.0 ** np.arange(nv), nx)[:, None] + 1.5
+    b = a.LocalBlock(ctx, nv, a.RowRange(0, nx), nt, values=raw)
+    params, _ = a.snapshot_pass(b, scaling)
+    tr = rng.matrix(nt, r) * 0.1
+    qt = rng.matrix(nt_p, r)
+    return b, params, tr, qt
+
+
+@pytest.mark.parametrize("nv,nx,nt,r,nt_p,scaling", [
+    (2, 1000, 64, 3, 7, True),        # r < 4: the scalar tail only
+    (1, 4097, 120, 10, 240, False),   # config-1 r, odd rows
+    (3, 2000, 96, 20, 129, True),     # odd nt_p
+    (2, 3001, 200, 40, 400, True),    # config-2 r
+    (1, 2500, 150, 68, 300, True),    # config-4 r
+    (2, 1500, 160, 80, 333, True),    # config-5 largest r
+    (1, 700, 180, 100, 65, True),     # r_pad 112 > 96: two k-slabs
+    (2, 600, 300, 130, 64, False),    # r_pad 256: three k-slabs
+])
+def test_field_matches_reference(ctx, oracle, reference, nv, nx, nt, r, nt_p, scaling):
+    a = api()
+    b, params, tr, qt = _setup(ctx, oracle, nv, nx, nt, r, nt_p, scaling, seed=nt + r)
+    field = a.reconstruct_field(b, tr, qt, params)
+    want = reference.reconstruct_field(b.values, nv, tr, qt, params.local_means,
+                                       params.scales if scaling else None, scaling)
+    assert field.shape == (nv * nx, nt_p)
+    assert rel(field, want) <= FIELD_TOL
+    # Φ_r the field was built from is left on the device, as after basis()
+    phi = a.basis(b, tr)
+    assert rel(phi, oracle.matmul(b.values, tr)) <= 1e-12
+
+
+def test_field_device_t_r_and_device_output(ctx, oracle, reference):
+    a = api()
+    nv, nx, nt, r, nt_p = 2, 3000, 128, 12, 256
+    rng = oracle.rng(3)
+    b = a.LocalBlock(ctx, nv, a.RowRange(0, nx), nt)
+    b.synth_lowrank(seed=4, rank=30, amplitude=5.0)
+    params, _ = a.snapshot_pass(b, True)
+    a.eig_sym_desc(ctx)
+    tr = a.reduced_map(ctx, r)                      # device T_r (and its host copy)
+    qt = rng.matrix(nt_p, r)
+    f_dev = a.reconstruct_field(b, None, qt, params, r=r)
+    f_host = a.reconstruct_field(b, tr, qt, params)
+    assert np.array_equal(f_dev, f_host)
+    a.reconstruct_field(b, tr, qt, params, download=False)
+    ptr, ld = a.field_device(b)
+    assert ptr and ld >= nt_p
+    want = reference.reconstruct_field(b.values, nv, tr, qt, params.local_means, params.scales, True)
+    assert rel(f_host, want) <= FIELD_TOL
+
+
+def test_field_deterministic_and_pinned_out(ctx, oracle):
+    a = api()
+    b, params, tr, qt = _setup(ctx, oracle, 2, 5000, 100, 40, 200, True, seed=11)
+    f1 = a.reconstruct_field(b, tr, qt, params)
+    import torch
+
+    pinned = torch.empty((b.rows, qt.shape[0]), dtype=torch.float64).pin_memory().numpy()
+    f2 = a.reconstruct_field(b, tr, qt, params, out=pinned)
+    assert np.array_equal(f1, f2)
+
+
+@pytest.mark.parametrize("nt_p", [2, 301])
+def test_write_field_matches_reference_file(tmp_path, ctx, oracle, reference, nt_p):
+    a = api()
+    nv, nx, nt, r = 3, 70001, 16, 8   # several 128-row chunks per variable
+    b, params, tr, qt = _setup(ctx, oracle, nv, nx, nt, r, nt_p, True, seed=nt_p)
+    names = ["rho", "u_x", "energy"]
+    path = tmp_path / "field_rank0.snp1"
+    a.write_field(b, tr, qt, params, names, str(path))
+    want = reference.reconstruct_field(b.values, nv, tr, qt, params.local_means, params.scales, True)
+    ref_path = tmp_path / "ref.snp1"
+    reference.write_snapshots(ref_path, names, [want[j * nx:(j + 1) * nx] for j in range(nv)])
+    ours, theirs = path.read_bytes(), ref_path.read_bytes()
+    head = 28 + sum(4 + len(n) for n in names)
+    assert len(ours) == len(theirs) and ours[:head] == theirs[:head]
+    got = np.frombuffer(ours[head:], dtype="<f8").reshape(nv * nx, nt_p)
+    assert rel(got, want) <= FIELD_TOL
+    assert reference.read_header(path) == (nv, nx, nt_p, names)
+    assert np.array_equal(got, a.reconstruct_field(b, tr, qt, params))
+
+
+def test_field_errors(tmp_path, ctx, oracle):
+    a = api()
+    b, params, tr, qt = _setup(ctx, oracle, 2, 100, 12, 4, 9, True, seed=1)
+    with pytest.raises(a.InvalidArgumentError):
+        a.reconstruct_field(b, tr, qt[:, :3], params)
+    with pytest.raises(a.InvalidArgumentError):
+        a.reconstruct_field(b, tr[:5], qt, params)
+    with pytest.raises(a.DataFormatError, match="duplicate variable name 'v'"):
+        a.write_field(b, tr, qt, params, ["v", "v"], str(tmp_path / "f.snp1"))
+    with pytest.raises(a.DataFormatError, match="nt must be >= 2"):
+        a.write_field(b, tr, qt[:1], params, ["v", "w"], str(tmp_path / "f.snp1"))
+    with pytest.raises(a.DataFormatError, match="cannot create snapshot file"):
+        a.write_field(b, tr, qt, params, ["v", "w"], str(tmp_path / "no_such_dir" / "f.snp1"))
+    # an empty slice (nx_i = 0) has no rows: empty field; its file header is invalid (nx = 0)
+    e = a.LocalBlock(ctx, 2, a.RowRange(5, 5), 12)
+    pe, _ = a.snapshot_pass(e, False)
+    assert a.reconstruct_field(e, tr, qt, pe).shape == (0, 9)
+    with pytest.raises(a.DataFormatError, match="nx must be >= 1"):
+        a.write_field(e, tr, qt, pe, ["v", "w"], str(tmp_path / "e.snp1"))
+    assert struct.calcsize("<QQQ") == 24

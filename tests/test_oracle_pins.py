@@ -168,3 +168,23 @@ def test_oracle_pass_vs_reference(oracle, reference, nv, nx, nt, p):
     oq, om, os_, od = oracle_pass(oracle, q, nv, nx, p)
     assert np.array_equal(rq, oq) and np.array_equal(rm, om) and np.array_equal(rs, os_)
     assert np.array_equal(rd, od)
+
+
+@pytest.mark.parametrize("nv,nx,nt,r,nt_p,scaling", [(2, 15, 11, 3, 7, True), (1, 40, 33, 10, 21, False),
+                                                   (3, 50, 64, 20, 128, True), (2, 30, 90, 40, 181, True),
+                                                   (1, 20, 70, 68, 9, True), (2, 9, 12, 5, 2, False)])
+def test_oracle_field_vs_reference(oracle, reference, nv, nx, nt, r, nt_p, scaling):
+    # postprocess::reconstruct_field (postprocess.cpp:63-70), bit for bit: matmul's
+    # FMA chains, matmul_nt's 8-lane dot (incl. the 4-block and the tail), scale_shift
+    rng = oracle.rng(nt + r)
+    raw = rng.matrix(nv * nx, nt)
+    q, means = oracle.center(raw)
+    scales = None
+    if scaling:
+        scales, _ = oracle.reduce_scales(oracle.local_maxabs(q, nv, nx)[None, :])
+        q = oracle.scale(q, nv, nx, scales)
+    tr = rng.matrix(nt, r)
+    qt = rng.matrix(nt_p, r)
+    want = reference.reconstruct_field(q, nv, tr, qt, means, scales, scaling)
+    got = oracle.reconstruct_field(q, tr, qt, means, scales, nx, scaling)
+    assert np.array_equal(got, want)
