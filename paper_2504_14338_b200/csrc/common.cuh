@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -18,6 +19,8 @@ constexpr int kWarp = 32;
 void note_launch();
 // cudaFuncAttributeMaxDynamicSharedMemorySize, set once per (kernel, device).
 cudaError_t set_smem_attr_once(const void* func, int bytes);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (null if absent).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 
 // ---- mbarrier ------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -55,6 +58,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+
+// Order this thread's generic-proxy shared-memory accesses before later
+// async-proxy (TMA) accesses to the same shared memory.
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 // ---- TMA -----------------------------------------------------------------

@@ -308,19 +308,6 @@ __global__ void ordered_sum_kernel(const double* __restrict__ parts, int p, size
     }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess) {
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-        }
-    }
-    return fn;
-}
 
 }  // namespace
 
@@ -421,7 +408,7 @@ Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes)
 }
 
 cudaError_t make_tensor_map(CUtensorMap* map, const double* q, long long n_rows, int K, size_t ld) {
-    auto fn = encode_fn();
+    auto fn = tensor_map_encoder();
     if (!fn) return cudaErrorNotSupported;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(n_rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * sizeof(double))};

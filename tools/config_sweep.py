@@ -5,9 +5,11 @@ and writes them to gpurun_out/config_sweep.jsonl.
   c1   2 vars x 16384, K=600: snapshot pass (stage times)
   c3   1 var x 4194304, K in {256..4096}, N(0,1) + 10 x rank-50: Gram TFLOP/s per K
   c5   config-2 data, r in {20,40,80}: Phi_r = Q T_r and 1000 probe rows (basis_rows)
+  c5f  config-2 data, r in {20,40,80}: field reconstruction (nt_p = 2400) + SNP1 field writer
   c4   8 vars x 4194304 per GPU, K=1500 (403 GB): streamed from a device ring
 """
 import argparse
+import os
 import json
 import sys
 import time
@@ -100,6 +102,58 @@ def run_c5(ctx, out, rs, n_probes=1000):
     b.close()
 
 
+def run_c5_field(ctx, out, rs, nt_p=2400, write_dir="/tmp"):
+    """Step V at config 5: field = s·(Q·T_r)·Q̃ᵀ + mean over all 1,048,576 rows and
+    nt_p = 2K = 2400 (20 GB of output), device-resident; then the streamed SNP1
+    field writer at r = 40, and the reference's reconstruct_field on a row sample."""
+    nv, nx, K = 4, 262144, 1200
+    b = api.LocalBlock(ctx, nv, api.RowRange(0, nx), K)
+    b.synth_oscillator(seed=2, n_modes=40, dt=1e-3, noise=1e-4)
+    params, d = api.snapshot_pass(b, scaling=True)
+    n = nv * nx
+    rng = np.random.default_rng(6)
+    for r in rs:
+        tr = tr_from(d, r)
+        qt = rng.standard_normal((nt_p, r))
+        ts = []
+        for rep in range(3):
+            api.reconstruct_field(b, tr, qt, params, download=False)
+            ts.append(ctx.stage_ms("field"))
+        best = min(ts)
+        flops = 2 * n * nt_p * r
+        byts = 8 * n * nt_p + 8 * n * r
+        rec = {"config": "c5_field", "n": n, "K": K, "r": r, "nt_p": nt_p, "field_ms": round(best, 3),
+               "basis_ms": round(ctx.stage_ms("basis"), 3), "tflops": round(flops / best / 1e9, 3),
+               "write_gbs": round(8 * n * nt_p / best / 1e6, 1),
+               "frac_fp64": round(flops / best / 1e9 / PEAK_FP64, 4),
+               "frac_hbm": round(byts / best / 1e6 / PEAK_HBM, 4),
+               "roofline_ms": round(max(flops / PEAK_FP64 / 1e9, byts / PEAK_HBM / 1e6), 3)}
+        if r == 40:
+            path = os.path.join(write_dir, "dopinf_field_rank0.snp1")
+            t0 = time.perf_counter()
+            api.write_field(b, tr, qt, params, [f"var{j}" for j in range(nv)], path)
+            wall = time.perf_counter() - t0
+            rec["write_field_wall_s"] = round(wall, 3)
+            rec["write_field_gbs"] = round(8 * n * nt_p / wall / 1e9, 2)
+            os.remove(path)
+            try:
+                from oracle.cpu import Reference
+
+                if Reference.available():
+                    sample = 8192
+                    q = b.values[:sample]
+                    t0 = time.perf_counter()
+                    Reference().reconstruct_field(q, 1, tr, qt, params.local_means[:sample], params.scales[:1], True)
+                    rs_ = time.perf_counter() - t0
+                    rec["reference_sample_rows"] = sample
+                    rec["reference_s_per_row"] = rs_ / sample
+                    rec["reference_extrapolated_s"] = round(rs_ / sample * n, 1)
+            except Exception as e:  # noqa: BLE001 - dev tool
+                rec["reference_error"] = str(e)
+        emit(rec, out)
+    b.close()
+
+
 def run_c4(ctx, out, r=68):
     """Config 4 per GPU: 8 vars x 4,194,304 points (33.5M rows), K = 1500, 60-mode
     oscillator with per-variable magnitudes 1e-2..1e5, scaling on, r = 68 —
@@ -137,6 +191,8 @@ def main():
             run_c3(ctx, out, [int(k) for k in args.ks.split(",")])
         if "c5" in cfgs:
             run_c5(ctx, out, [20, 40, 80])
+        if "c5f" in cfgs:
+            run_c5_field(ctx, out, [20, 40, 80])
         if "c4" in cfgs:
             run_c4(ctx, out)
 
