@@ -10,6 +10,7 @@
 //   dopinf_b200::pod::project(tr, d)                             pod.hpp:49
 //   dopinf_b200::postprocess::basis_rows(block, tr, rows)        postprocess.hpp:25-26
 //   dopinf_b200::postprocess::basis(block, tr)  (Φ_r of reconstruct_field, postprocess.cpp:66)
+//   dopinf_b200::postprocess::reconstruct_field(block, tr, qtilde, params)  postprocess.hpp:43-45
 //   dopinf_b200::data::partition_rows(nx, p)                     data.hpp:47
 //   dopinf_b200::data::read_header<HeaderT>(path)                data.hpp:52
 //   dopinf_b200::data::read_block<LocalBlockT>(path, plan, rank, header)  data.hpp:54
@@ -403,6 +404,30 @@ MatrixT basis(const LocalBlockT& block, const MatrixT& tr) {
     DeviceBlock d = detail::uploaded(block, detail::n_vars_of(block));
     MatrixT out(block.values.rows(), tr.cols());
     Context::check(dopinf_b200_basis(d.handle(), tr.data(), tr.cols(), out.data()), d.context().handle(), "basis");
+    return out;
+}
+
+// postprocess::reconstruct_field (postprocess.cpp:63-70): (Q·T_r)·Q̃ᵀ mapped back
+// with the TransformParams, (n_vars·nx_i) × nt_p; DMMA with the inverse
+// transform fused.
+template <class LocalBlockT, class MatrixT, class ParamsT>
+MatrixT reconstruct_field(const LocalBlockT& block, const MatrixT& tr, const MatrixT& qtilde, const ParamsT& params) {
+    if (block.values.cols() != tr.rows()) throw InvalidArgumentError("matmul: inner dimensions differ");
+    if (qtilde.cols() != tr.cols()) throw InvalidArgumentError("matmul_nt: column counts differ");
+    if (block.values.rows() != params.local_means.size()) {
+        throw InvalidArgumentError("inverse_transform_block: row count does not match the transform");
+    }
+    const std::size_t n_vars = detail::n_vars_of(block);
+    if (params.scaling_enabled && params.scales.size() != n_vars) {
+        throw InvalidArgumentError("reconstruct_field: scales do not match the block's variables");
+    }
+    DeviceBlock d = detail::uploaded(block, n_vars);
+    MatrixT out(block.values.rows(), qtilde.rows());
+    Context::check(dopinf_b200_reconstruct_field(d.handle(), tr.data(), tr.cols(), qtilde.data(), qtilde.rows(),
+                                                 params.local_means.data(),
+                                                 params.scaling_enabled ? params.scales.data() : nullptr,
+                                                 params.scaling_enabled ? 1 : 0, out.data()),
+                   d.context().handle(), "reconstruct_field");
     return out;
 }
 }  // namespace postprocess

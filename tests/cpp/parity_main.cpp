@@ -339,7 +339,7 @@ int main() {
         for (std::size_t v = 0; v < spec.n_vars; ++v)
             for (std::size_t i = 0; i < spec.nx; ++i)
                 for (std::size_t t = 0; t < spec.nt; ++t) raw(v * spec.nx + i, t) = made.variables[v](i, t);
-        double traj_gap = 0, err_gap = 0, lam_gap = 0;
+        double traj_gap = 0, err_gap = 0, lam_gap = 0, field_same = 0, field_chain = 0;
         std::string err_detail;
         bool pair_same = true;
         std::size_t r_ref = 0, r_gpu = 0;
@@ -380,12 +380,30 @@ int main() {
                 num += std::min(dp, dm);
             }
             traj_gap = std::max(traj_gap, std::sqrt(num / den));
+            // Step V field (postprocess.cpp:63-70): same inputs, and the whole B200 chain
+            // (per-mode signs cancel in Φ_r·Q̃ᵀ, so no normalisation is needed)
+            auto params_of = [&](const PassOut& o) {
+                transform::TransformParams tp;
+                tp.local_means = o.means;
+                tp.scales = o.scales;
+                tp.scaling_enabled = scaling;
+                return tp;
+            };
+            const data::LocalBlock br = whole(r.q, spec.nx), bg = whole(g.q, spec.nx);
+            const Matrix trr = pod::reduced_map(sr, r_ref), trg = pod::reduced_map(sg, r_gpu);
+            const Matrix fr = postprocess::reconstruct_field(br, trr, orf.trajectory, params_of(r));
+            field_same = std::max(field_same, rel_frob(dopinf_b200::postprocess::reconstruct_field(
+                                                           br, trr, orf.trajectory, params_of(r)), fr));
+            field_chain = std::max(field_chain, rel_frob(dopinf_b200::postprocess::reconstruct_field(
+                                                             bg, trg, ogp.trajectory, params_of(g)), fr));
         }
         report(lam_gap <= 1e-10, "pipeline eigenvalues", "rel to lambda1 " + fmt(lam_gap) + " <= 1e-10");
         report(pair_same, "pipeline r and optimal (beta1, beta2) identical", "r = " + std::to_string(r_gpu));
         report(err_gap <= 1e-10, "pipeline training error (acceptance criterion-2 run)",
                err_detail + "centered run rel <= 1e-10");
         report(traj_gap <= 1e-8, "ROM prediction over 2x horizon", "rel " + fmt(traj_gap) + " <= 1e-8");
+        report(field_same <= 1e-10 && field_chain <= 1e-8, "reconstruct_field vs postprocess::reconstruct_field",
+               "same inputs rel " + fmt(field_same) + " <= 1e-10; whole chain rel " + fmt(field_chain) + " <= 1e-8");
     }
 
     std::printf("parity: %s\n", g_fail == 0 ? "all checks passed" : "FAILURES");
