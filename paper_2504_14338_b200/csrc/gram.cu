@@ -39,8 +39,8 @@ namespace gram {
 namespace {
 
 constexpr int BT = kTileEdge;         // 128 columns per block
-constexpr int BK = kRowsPerStage;     // 16 rows per stage
-constexpr int STAGES = 6;
+constexpr int BK = kRowsPerStage;     // rows per stage
+constexpr int STAGES = 2;
 constexpr int CONSUMERS = kConsumerWarps;  // 16 = 4 consumer warpgroups
 constexpr int THREADS = (CONSUMERS + 1) * kWarp;  // + one TMA producer warp
 constexpr int FLAG_FIRST = 1, FLAG_LAST = 2, FLAG_DONE = 4;
