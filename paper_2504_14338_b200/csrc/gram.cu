@@ -72,7 +72,12 @@ __device__ __forceinline__ void decode(uint32_t e, int& wm, int& wn, bool& diag,
 // The swizzle then puts the quarter-warp's 8 loads in 8 distinct chunks:
 // conflict-free (4 wavefronts per 512 B). ks permutes the contraction order
 // only; the output mapping is unchanged.
-template <bool kFull>
+// MASK: the mma tiles (bit mi*4 + ni) of the warp tile, fixed at compile
+// time so skipped tiles cost nothing (a predicated-off DMMA still occupies
+// the tensor pipe). The partial masks that occur for any K are few:
+// diagonal 0xCCFF, column edge 0x1111/0x3333/0x7777, and their combinations
+// 0x0001/0x0033/0x0477 (enumerated by plan_tiles; kPartialMasks below).
+template <uint32_t MASK>
 __device__ __forceinline__ void stage_mma(double (&acc)[16][2], const double* __restrict__ as,
                                           const double* __restrict__ bs, int xg0, int xg1, uint32_t mask) {
 #pragma unroll
@@ -88,17 +93,32 @@ __device__ __forceinline__ void stage_mma(double (&acc)[16][2], const double* __
         for (int mi = 0; mi < 4; ++mi) {
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni) {
-                if (kFull || ((mask >> (mi * 4 + ni)) & 1u)) {
-                    dmma_8x8x4(acc[mi * 4 + ni][0], acc[mi * 4 + ni][1], a[mi], b[ni]);
-                }
+                const bool on = MASK != 0 ? ((MASK >> (mi * 4 + ni)) & 1u) != 0 : ((mask >> (mi * 4 + ni)) & 1u) != 0;
+                if (on) dmma_8x8x4(acc[mi * 4 + ni][0], acc[mi * 4 + ni][1], a[mi], b[ni]);
             }
         }
     }
 }
 
+// Dispatch on the warp tile's mask (warp-uniform); MASK 0 = generic predicated path.
+__device__ __forceinline__ void stage_mma_any(double (&acc)[16][2], const double* __restrict__ as,
+                                              const double* __restrict__ bs, int xg0, int xg1, uint32_t mask) {
+    switch (mask) {
+        case 0xFFFFu: stage_mma<0xFFFFu>(acc, as, bs, xg0, xg1, mask); break;
+        case 0xCCFFu: stage_mma<0xCCFFu>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x7777u: stage_mma<0x7777u>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x3333u: stage_mma<0x3333u>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x1111u: stage_mma<0x1111u>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x0477u: stage_mma<0x0477u>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x0033u: stage_mma<0x0033u>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x0001u: stage_mma<0x0001u>(acc, as, bs, xg0, xg1, mask); break;
+        default: stage_mma<0u>(acc, as, bs, xg0, xg1, mask); break;
+    }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     gram_dmma_kernel(const __grid_constant__ CUtensorMap tmap, const TileInfo* __restrict__ tiles,
-                     int n_tiles, int n_items, long long n_rows, int chunk_rows, int big_splits,
+                     int n_tiles, int n_items, long long n_rows, int K, int chunk_rows, int big_splits,
                      int small_rows,
                      double* __restrict__ work, int* __restrict__ counters, int accumulate) {
     extern __shared__ unsigned char smem_raw[];
@@ -143,22 +163,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                     min(static_cast<long long>(split < big_splits ? chunk_rows : small_rows), n_rows - row0);
                 const int nkb = static_cast<int>((rows + BK - 1) / BK);
                 const bool diag = (I == J);
-                const uint32_t bytes = (diag ? 1u : 2u) * BK * BT * sizeof(double);
+                // boxes entirely beyond column K are never read by an active mma
+                // tile: skip them (no TMA, no zero fill)
+                const int boxes_a = min(BT / 16, (K - I * BT + 15) / 16);
+                const int boxes_b = diag ? 0 : min(BT / 16, (K - J * BT + 15) / 16);
+                const uint32_t bytes = static_cast<uint32_t>(boxes_a + boxes_b) * BK * 16 * sizeof(double);
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&s.empty[stage], phase ^ 1u);
                     s.meta_item[stage] = item;
                     s.meta_flags[stage] = (kb == 0 ? FLAG_FIRST : 0) | (kb == nkb - 1 ? FLAG_LAST : 0);
                     mbar_arrive_expect_tx(&s.full[stage], bytes);
                     const int y = static_cast<int>(row0 + static_cast<long long>(kb) * BK);
-#pragma unroll
-                    for (int box = 0; box < BT / 16; ++box) {
+                    for (int box = 0; box < boxes_a; ++box) {
                         tma_load_2d(s.a[stage] + box * BK * 16, &tmap, I * BT + box * 16, y, &s.full[stage]);
                     }
-                    if (!diag) {
-#pragma unroll
-                        for (int box = 0; box < BT / 16; ++box) {
-                            tma_load_2d(s.b[stage] + box * BK * 16, &tmap, J * BT + box * 16, y, &s.full[stage]);
-                        }
+                    for (int box = 0; box < boxes_b; ++box) {
+                        tma_load_2d(s.b[stage] + box * BK * 16, &tmap, J * BT + box * 16, y, &s.full[stage]);
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -188,11 +208,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (mask) {
                 const double* as = s.a[stage] + (2 * wm) * BK * 16 + 2 * t * 16;
                 const double* bs = (diag ? s.a[stage] : s.b[stage]) + (2 * wn) * BK * 16 + 2 * t * 16;
-                if (mask == 0xFFFFu) {
-                    stage_mma<true>(acc, as, bs, xg0, xg1, mask);
-                } else {
-                    stage_mma<false>(acc, as, bs, xg0, xg1, mask);
-                }
+                stage_mma_any(acc, as, bs, xg0, xg1, mask);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.empty[stage]);
@@ -429,7 +445,8 @@ cudaError_t launch_gram(const Plan& plan, const CUtensorMap& map, const TileInfo
                                              static_cast<int>(smem_bytes()));
     if (e != cudaSuccess) return e;
     gram_dmma_kernel<<<plan.grid, THREADS, smem_bytes(), stream>>>(
-        map, d_tiles, plan.n_tiles, plan.n_items, plan.n_rows, plan.chunk_rows, plan.big_splits, plan.small_rows,
+        map, d_tiles, plan.n_tiles, plan.n_items, plan.n_rows, plan.K, plan.chunk_rows, plan.big_splits,
+        plan.small_rows,
         work, counters, accumulate ? 1 : 0);
     note_launch();
     return cudaGetLastError();
