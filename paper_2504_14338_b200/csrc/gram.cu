@@ -386,7 +386,8 @@ Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes)
     p.n_tiles = static_cast<int>(plan_tiles(K).size());
     // Enough items for load balance, and chunks short enough (kTargetChunkRows)
     // that the CTAs working on one split stay within an L2-resident window of
-    // rows (measured: 31.8K-row chunks re-read Q ~4x from HBM, 8K-row ~1.5x).
+    // rows (measured at C2 with 40-row stages: 8K-row chunks re-read Q 2.5x
+    // from HBM, 4K-row 1.2x; the extra split partials cost ~0.1 ms of reduce).
     const long long target_items = static_cast<long long>(num_sms) * kItemsPerCta;
     long long S = (target_items + p.n_tiles - 1) / p.n_tiles;
     S = std::max<long long>(S, (n_rows + kTargetChunkRows - 1) / kTargetChunkRows);

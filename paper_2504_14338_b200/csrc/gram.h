@@ -18,8 +18,8 @@ constexpr int kWarpFragDoubles = 16 * 32 * 2;                   // 16 mma × 32 
 constexpr int kItemDoubles = kConsumerWarps * kWarpFragDoubles;  // 16384 (128 KiB)
 constexpr int kItemsPerCta = 16;     // queue granularity target (tail vs workspace)
 constexpr long long kMinRowsPerSplit = 768;
-constexpr long long kTargetChunkRows = 8192;  // L2 window of rows shared by a split's CTAs
-constexpr size_t kWorkspaceCapBytes = size_t(1) << 30;
+constexpr long long kTargetChunkRows = 4096;  // L2 window of rows shared by a split's CTAs (C2: 8K rows re-read Q 2.5x from HBM with 40-row stages, 4K rows 1.2x)
+constexpr size_t kWorkspaceCapBytes = size_t(2) << 30;
 
 struct TileInfo {
     int I, J;
