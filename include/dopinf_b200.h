@@ -27,6 +27,8 @@
  *   data::read_block (data.hpp:54, data.cpp:164-202)         dopinf_b200_block_read
  *   pipeline::run_rank read + Steps II-III (pipeline.cpp:254-280)
  *                                                            dopinf_b200_snapshot_pass_file
+ *   rom_search::grid_search (rom_search.cpp:185-262)        dopinf_b200_grid_search
+ *   rom_search::integrate (rom_search.cpp:60-85)            dopinf_b200_rom_integrate
  *   postprocess::reconstruct_field (postprocess.cpp:63-70)   dopinf_b200_reconstruct_field
  *   Step V field_rank<r>.snp1 output (pipeline.cpp:330-350) dopinf_b200_write_field
  *
@@ -59,7 +61,8 @@ typedef enum dopinf_b200_status {
     DOPINF_B200_ERR_NOT_PSD = 7,            /* NotPsdError            (errors.hpp:40-43) */
     DOPINF_B200_ERR_RANK_DEFICIENCY = 8,    /* RankDeficiencyError    (errors.hpp:46-49) */
     DOPINF_B200_ERR_SOLVE = 9,              /* SolveError             (errors.hpp:52-55) */
-    DOPINF_B200_ERR_DATA_FORMAT = 10        /* DataFormatError        (errors.hpp:15-18) */
+    DOPINF_B200_ERR_DATA_FORMAT = 10,       /* DataFormatError        (errors.hpp:15-18) */
+    DOPINF_B200_ERR_NO_ADMISSIBLE_PAIR = 11 /* NoAdmissiblePairError  (errors.hpp:57-60) */
 } dopinf_b200_status;
 
 /* Collective ops, same order as comm::ReduceOp (comm.hpp:9). */
@@ -266,6 +269,31 @@ int dopinf_b200_block_read(dopinf_b200_ctx* ctx, const char* path, size_t row_be
 int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* ctx, const char* path, size_t row_begin,
                                    size_t row_end, int scaling, dopinf_b200_block** out, double* means,
                                    double* scales, double* d);
+
+/* ---- Step IV: OpInf regularisation grid search (rom_search.hpp) ----------- */
+/* rom_search::grid_search (rom_search.cpp:185-262) on the device. qhat: host
+ * r x nt (pod::project's Q̂), or NULL for the context's device Q̂ of the last
+ * dopinf_b200_project (r, nt must match it). Candidate pair idx = i1*n2 + i2
+ * is (b1[i1], b2[i2]); pairs are split over the context's ranks as
+ * distribute_pairs does, each rank solves, integrates and scores its slice
+ * (DhatᵀDhat and Dhatᵀ Qhat2ᵀ once; cuSOLVER Cholesky per pair; all ROMs
+ * integrated concurrently, bit-identical steps to rom_search::integrate for
+ * the same operators), and the winner — lowest training error among the
+ * admissible pairs, first index on ties — is agreed with MIN collectives and
+ * its trajectory broadcast from the owner. Outputs (host, each may be NULL):
+ * pair_opt[2] = {beta1, beta2}, train_err, owner, rom_seconds (device time of
+ * the integration launch), trajectory nt_p x r. Errors as the reference:
+ * InvalidArgumentError, SolveError, NoAdmissiblePairError (same messages). */
+int dopinf_b200_grid_search(dopinf_b200_ctx* ctx, const double* qhat, size_t r, size_t nt, const double* b1,
+                            size_t n1, const double* b2, size_t n2, double max_growth, size_t nt_p,
+                            double* pair_opt, double* train_err, int* owner, double* rom_seconds,
+                            double* trajectory);
+/* rom_search::integrate (rom_search.cpp:60-85): q_{k+1} = A q_k + F quad(q_k) + c
+ * from q0 for n_steps rows (row 0 = q0), bit-identical to the reference for
+ * the same operators. a: r x r, f: r x r(r+1)/2, c: r, q0: r (host);
+ * traj: host n_steps x r; finite: 1 iff every entry is finite. */
+int dopinf_b200_rom_integrate(dopinf_b200_ctx* ctx, const double* a, const double* f, const double* c, size_t r,
+                              const double* q0, size_t n_steps, double* traj, int* finite);
 
 /* ---- Step V: field reconstruction (postprocess.hpp:40-45) ----------------- */
 /* postprocess::reconstruct_field (postprocess.cpp:63-70): this rank's field

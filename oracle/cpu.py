@@ -252,6 +252,8 @@ class Reference:
             lib.ref_write_snapshots.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_char_p, _dp]
             lib.ref_read_header.argtypes = [C.c_char_p, _sp, C.c_char_p, C.c_size_t]
             lib.ref_read_block.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
+            lib.ref_integrate.argtypes = [_dp, _dp, _dp, C.c_size_t, _dp, C.c_size_t, _dp, C.POINTER(C.c_int)]
+            lib.ref_solve_opinf.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_double, C.c_double, _dp, _dp, _dp]
             lib.ref_reconstruct_field.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp,
                                                   C.c_size_t, _dp, _dp, C.c_int, _dp]
             Reference._lib = lib
@@ -342,6 +344,24 @@ class Reference:
         self._ok(self.lib.ref_grid_search(_d(qhat), r, nt, _d(b1), b1.size, _d(b2), b2.size, max_growth, nt_p,
                                           _d(traj), _d(pe)))
         return traj, (pe[0], pe[1]), pe[2]
+
+    def integrate(self, a, f, c, q0, n_steps):
+        """rom_search::integrate (rom_search.cpp:60-85) -> (trajectory n_steps x r, finite)."""
+        a, f, c, q0 = _f(a), _f(f), _f(c), _f(q0)
+        r = a.shape[0]
+        traj = np.empty((n_steps, r))
+        fin = C.c_int()
+        self._ok(self.lib.ref_integrate(_d(a), _d(f), _d(c), r, _d(q0), n_steps, _d(traj), C.byref(fin)))
+        return traj, bool(fin.value)
+
+    def solve_opinf(self, qhat, beta1, beta2):
+        """opinf::solve_opinf on assemble_data(qhat) -> (A, F, c)."""
+        qhat = _f(qhat)
+        r, nt = qhat.shape
+        s = r * (r + 1) // 2
+        a, f, c = np.empty((r, r)), np.empty((r, s)), np.empty(r)
+        self._ok(self.lib.ref_solve_opinf(_d(qhat), r, nt, beta1, beta2, _d(a), _d(f), _d(c)))
+        return a, f, c
 
     # ---- data.cpp: SNP1 container ---------------------------------------------------
     def write_snapshots(self, path, names, variables):

@@ -38,6 +38,8 @@ int fail(const std::exception& e) {
     if (dynamic_cast<const NotPsdError*>(&e)) return 7;
     if (dynamic_cast<const RankDeficiencyError*>(&e)) return 8;
     if (dynamic_cast<const DataFormatError*>(&e)) return 10;
+    if (dynamic_cast<const NoAdmissiblePairError*>(&e)) return 11;
+    if (dynamic_cast<const SolveError*>(&e)) return 9;
     return 99;
 }
 
@@ -356,6 +358,41 @@ int ref_reconstruct_field(const double* q, std::size_t n_vars, std::size_t nx_i,
         params.scaling_enabled = scaling != 0;
         from_matrix(postprocess::reconstruct_field(block, to_matrix(tr, nt, r), to_matrix(qtilde, nt_p, r), params),
                     out);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// rom_search::integrate (rom_search.cpp:60-85) with caller operators:
+// a r x r, f r x s, c r, q0 r -> traj n_steps x r; returns finite in *finite.
+int ref_integrate(const double* a, const double* f, const double* c, std::size_t r, const double* q0,
+                  std::size_t n_steps, double* traj, int* finite) {
+    try {
+        opinf::ReducedOperators ops;
+        ops.a = to_matrix(a, r, r);
+        ops.f = to_matrix(f, r, opinf::quad_len(r));
+        ops.c.assign(c, c + r);
+        const rom_search::IntegrateResult res = rom_search::integrate(ops, std::vector<double>(q0, q0 + r), n_steps);
+        from_matrix(res.trajectory, traj);
+        *finite = res.finite ? 1 : 0;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// opinf::solve_opinf (opinf.cpp:69-92) for one pair on assemble_data(qhat):
+// a r x r, f r x s, c r.
+int ref_solve_opinf(const double* qhat, std::size_t r, std::size_t nt, double beta1, double beta2, double* a,
+                    double* f, double* c) {
+    try {
+        const opinf::OpInfData data = opinf::assemble_data(to_matrix(qhat, r, nt));
+        const auto gamma = opinf::build_regularizer(r, opinf::quad_len(r), {beta1, beta2});
+        const opinf::ReducedOperators ops = opinf::solve_opinf(data, gamma);
+        from_matrix(ops.a, a);
+        from_matrix(ops.f, f);
+        std::memcpy(c, ops.c.data(), r * sizeof(double));
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

@@ -23,6 +23,7 @@ ERR_NOT_PSD = 7
 ERR_RANK_DEFICIENCY = 8
 ERR_SOLVE = 9
 ERR_DATA_FORMAT = 10
+ERR_NO_ADMISSIBLE_PAIR = 11
 
 SUM, MAX, MIN = 0, 1, 2
 GRAM_REDUCE_ORDERED, GRAM_REDUCE_NCCL = 0, 1
@@ -80,6 +81,10 @@ SIGNATURES = {
                                                  C.c_int, C.c_double, C.c_double, _dp, C.c_int, _dp, _dp, _dp]),
     "dopinf_b200_snp1_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t,
                                           C.POINTER(C.c_size_t)]),
+    "dopinf_b200_grid_search": (C.c_int, [_vp, _dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp, C.c_size_t,
+                                          C.c_double, C.c_size_t, _dp, _dp, C.POINTER(C.c_int), _dp, _dp]),
+    "dopinf_b200_rom_integrate": (C.c_int, [_vp, _dp, _dp, _dp, C.c_size_t, _dp, C.c_size_t, _dp,
+                                            C.POINTER(C.c_int)]),
     "dopinf_b200_reconstruct_field": (C.c_int, [_vp, _dp, C.c_size_t, _dp, C.c_size_t, _dp, _dp, C.c_int, _dp]),
     "dopinf_b200_field_device": (C.c_int, [_vp, C.POINTER(_dp), C.POINTER(C.c_size_t)]),
     "dopinf_b200_write_field": (C.c_int, [_vp, _dp, C.c_size_t, _dp, C.c_size_t, _dp, _dp, C.c_int, C.c_char_p,

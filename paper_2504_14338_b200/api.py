@@ -62,6 +62,10 @@ class SolveError(Error):
     pass
 
 
+class NoAdmissiblePairError(Error):
+    pass
+
+
 class InvalidArgumentError(Error):
     pass
 
@@ -81,6 +85,7 @@ _STATUS = {
     _lib.ERR_RANK_DEFICIENCY: RankDeficiencyError,
     _lib.ERR_SOLVE: SolveError,
     _lib.ERR_DATA_FORMAT: DataFormatError,
+    _lib.ERR_NO_ADMISSIBLE_PAIR: NoAdmissiblePairError,
 }
 
 
@@ -550,6 +555,85 @@ def basis(block: LocalBlock, tr, download: bool = True, r: int | None = None):
     out = np.empty((block.rows, r), dtype=np.float64) if download else None
     _check(_lib.load().dopinf_b200_basis(block._h, _lib.dptr(tr), r, _lib.dptr(out)), block.ctx, "basis")
     return out
+
+
+# ---- rom_search.hpp (Step IV) ------------------------------------------------------
+def logspace(lo: float, hi: float, n: int) -> list:
+    """rom_search::logspace (rom_search.cpp:13-29)."""
+    import math
+
+    if n < 1:
+        raise InvalidArgumentError("logspace: need at least one value")
+    if not (lo > 0.0) or not (hi > 0.0):
+        raise InvalidArgumentError("logspace: bounds must be positive")
+    if n == 1:
+        return [lo]
+    a, b = math.log10(lo), math.log10(hi)
+    return [10.0 ** (a + k * (b - a) / (n - 1)) for k in range(n)]
+
+
+def default_b1() -> list:
+    return logspace(1e-10, 1e0, 8)
+
+
+def default_b2() -> list:
+    return logspace(1e-4, 1e4, 8)
+
+
+@dataclass
+class SearchConfig:
+    """rom_search::SearchConfig (rom_search.hpp:19-24)."""
+    b1: list
+    b2: list
+    max_growth: float = 1.2
+    nt_p: int = 0
+
+
+@dataclass
+class SearchOutcome:
+    """rom_search::SearchOutcome (rom_search.hpp:35-41)."""
+    pair_opt: tuple
+    owner_rank: int
+    train_err: float
+    trajectory: np.ndarray
+    rom_seconds: float
+
+
+def grid_search(qhat, config: SearchConfig, comm: DeviceContext, r: int | None = None,
+                nt: int | None = None) -> SearchOutcome:
+    """rom_search::grid_search (rom_search.cpp:185-262) on the device. `qhat` is
+    the r × nt reduced trajectory (host), or None for the context's device Q̂ of
+    the last projection (pass r and nt)."""
+    if qhat is not None:
+        q = _f64(qhat)
+        r, nt = q.shape
+    else:
+        q = None
+    b1, b2 = _f64(list(config.b1)), _f64(list(config.b2))
+    nt_p = int(config.nt_p)
+    traj = np.empty((max(nt_p, 0), r), dtype=np.float64)
+    pair = np.empty(2, dtype=np.float64)
+    err = C.c_double()
+    owner = C.c_int()
+    secs = C.c_double()
+    rc = _lib.load().dopinf_b200_grid_search(comm._h, _lib.dptr(q), r, nt, _lib.dptr(b1), b1.size, _lib.dptr(b2),
+                                             b2.size, float(config.max_growth), nt_p, _lib.dptr(pair),
+                                             C.byref(err), C.byref(owner), C.byref(secs), _lib.dptr(traj))
+    _check(rc, comm)
+    return SearchOutcome((float(pair[0]), float(pair[1])), int(owner.value), float(err.value), traj,
+                         float(secs.value))
+
+
+def rom_integrate(ctx: DeviceContext, a, f, c, q0, n_steps: int):
+    """rom_search::integrate (rom_search.cpp:60-85) on the device -> (trajectory, finite)."""
+    a, f, c, q0 = _f64(a), _f64(f), _f64(c), _f64(q0)
+    r = a.shape[0]
+    traj = np.empty((max(n_steps, 0), r), dtype=np.float64)
+    fin = C.c_int()
+    rc = _lib.load().dopinf_b200_rom_integrate(ctx._h, _lib.dptr(a), _lib.dptr(f), _lib.dptr(c), r, _lib.dptr(q0),
+                                               n_steps, _lib.dptr(traj), C.byref(fin))
+    _check(rc, ctx)
+    return traj, bool(fin.value)
 
 
 def _field_args(block: LocalBlock, tr, qtilde, params: TransformParams, r: int | None, what: str):

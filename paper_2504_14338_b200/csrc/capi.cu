@@ -11,9 +11,11 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <mutex>
 #include <new>
 #include <set>
@@ -28,6 +30,7 @@
 #include "field.h"
 #include "gram.h"
 #include "project.h"
+#include "rom.h"
 #include "synth.h"
 #include "transform.h"
 
@@ -215,6 +218,10 @@ struct dopinf_b200_ctx {
     // device eigensolve (dopinf_b200_eig_sym_desc / dopinf_b200_reduced_map)
     eig::Solver solver;
     DBuf eig_a, eig_w, eig_work, eig_info, eig_v, eig_lambda, tr_dev;
+    size_t qhat_r = 0, qhat_nt = 0;  // shape of the device Q̂ of the last projection
+    // grid search (dopinf_b200_grid_search)
+    DBuf rom_qhat, rom_dhat, rom_q2t, rom_qrows, rom_rhs, rom_g, rom_lhs, rom_rhsb, rom_betas, rom_traj, rom_scores,
+        rom_work, rom_info, rom_tiles, rom_gwork, rom_counters, rom_packed, rom_packet;
     int eig_K = 0;      // size of the held eigendecomposition (0: none)
     size_t tr_dev_r = 0;
 
@@ -845,6 +852,237 @@ void do_block_read(dopinf_b200_block* b, const StreamSource& src) {
     ck(cudaEventSynchronize(c->chunk_events[chunks.size() - 1]), "ring");
 }
 
+// ---- Step IV: OpInf grid search (rom_search.cpp:185-262) --------------------
+// Host span all-reduce over NCCL (comm::allreduce_scalar's role).
+void host_allreduce(dopinf_b200_ctx* c, double* data, size_t count, ncclRedOp_t op) {
+    double* buf = c->span.get<double>(count, "span");
+    ck(cudaMemcpyAsync(buf, data, count * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+    ckn(ncclAllReduce(buf, buf, count, ncclFloat64, op, c->comm, c->stream), "allreduce");
+    ck(cudaMemcpyAsync(data, buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    c->sync("allreduce");
+}
+
+// rom_search::distribute_pairs (rom_search.cpp:147-160).
+std::pair<size_t, size_t> distribute_pairs(size_t n_reg, int rank, int size) {
+    const size_t ranks = static_cast<size_t>(size), rk = static_cast<size_t>(rank);
+    if (ranks > n_reg) return rk < n_reg ? std::make_pair(rk, rk + 1) : std::make_pair(n_reg, n_reg);
+    const size_t base = n_reg / ranks;
+    return {rk * base, (rk + 1 == ranks) ? n_reg : (rk + 1) * base};
+}
+
+// G = DhatᵀDhat (d × d, full, bitwise symmetric) with the Gram kernel on the
+// grid search's own plan/tiles (the snapshot pass's cached plan stays intact).
+void rom_gram(dopinf_b200_ctx* c, const double* dhat, size_t ldd, int K, int d, double* g) {
+    const std::vector<gram::TileInfo> t = gram::plan_tiles(d);
+    auto* tiles = c->rom_tiles.get<gram::TileInfo>(t.size(), "rom tiles");
+    ck(cudaMemcpyAsync(tiles, t.data(), t.size() * sizeof(gram::TileInfo), cudaMemcpyHostToDevice, c->stream),
+       "tiles H2D");
+    const gram::Plan plan = gram::make_plan(K, d, c->num_sms, size_t(256) << 20);
+    int* counters = c->rom_counters.get<int>(2, "rom counters");
+    ck(cudaMemsetAsync(counters, 0, 2 * sizeof(int), c->stream), "memset");
+    double* work = c->rom_gwork.get<double>(plan.workspace_doubles, "rom gram workspace");
+    double* packed = c->rom_packed.get<double>(gram::packed_count(d), "rom packed");
+    CUtensorMap map;
+    ck(gram::make_tensor_map(&map, dhat, K, d, ldd), "tensor map");
+    ck(gram::launch_gram(plan, map, tiles, work, counters, c->stream), "gram");
+    ck(gram::launch_reduce(plan, tiles, work, packed, c->stream), "gram reduce");
+    ck(gram::launch_unpack(packed, d, g, c->stream), "unpack");
+    c->sync("rom gram");  // the host tile table must outlive its copy
+}
+
+struct GridOutcome {
+    double beta1 = 0.0, beta2 = 0.0, train_err = 0.0, rom_seconds = 0.0;
+    int owner = -1;
+};
+
+GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r, size_t nt, const double* b1,
+                           size_t n1, const double* b2, size_t n2, double max_growth, size_t nt_p,
+                           double* traj_host) {
+    // rom_search.cpp:187-203 (same checks, same order, same messages)
+    if (n1 == 0 || n2 == 0) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "grid_search: empty candidate grid");
+    require(b1 && b2, "grid_search: null candidate arrays");
+    for (size_t i = 0; i < n1; ++i) {
+        if (!(b1[i] > 0.0)) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "grid_search: b1 candidates must be positive");
+    }
+    for (size_t i = 0; i < n2; ++i) {
+        if (!(b2[i] > 0.0)) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "grid_search: b2 candidates must be positive");
+    }
+    if (!(max_growth > 0.0)) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "grid_search: max_growth must be positive");
+    if (nt_p < nt) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "grid_search: trial horizon shorter than training");
+    if (nt < 2) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "assemble_data: need at least 2 snapshots");
+    require(r >= 1 && r <= 180, "grid_search: r must lie in [1, 180]");
+    const int R = static_cast<int>(r), NT = static_cast<int>(nt), NTP = static_cast<int>(nt_p);
+    const int S = R * (R + 1) / 2, D = R + S + 1, KK = NT - 1;
+    const size_t ldd = (static_cast<size_t>(D) + 1) / 2 * 2;
+
+    // Q̂ (r × nt) on the device
+    const double* dq;
+    if (qhat_host) {
+        double* q = c->rom_qhat.get<double>(r * nt, "rom qhat");
+        ck(cudaMemcpyAsync(q, qhat_host, r * nt * sizeof(double), cudaMemcpyHostToDevice, c->stream), "qhat H2D");
+        dq = q;
+    } else {
+        require(c->qhat_r == r && c->qhat_nt == nt, "grid_search: no device Q-hat of this shape on the context");
+        dq = c->qhat.get<double>(r * nt, "qhat");
+    }
+    // pair-independent data: Dhat, Qhat2ᵀ, qhat_rows, G = DhatᵀDhat, Dhatᵀ Qhat2ᵀ
+    double* dhat = c->rom_dhat.get<double>(static_cast<size_t>(KK) * ldd, "dhat");
+    double* q2t = c->rom_q2t.get<double>(static_cast<size_t>(KK) * r, "qhat2t");
+    double* qrows = c->rom_qrows.get<double>(nt * r, "qhat rows");
+    double* g = c->rom_g.get<double>(static_cast<size_t>(D) * D, "dhat gram");
+    double* rhs = c->rom_rhs.get<double>(static_cast<size_t>(D) * r, "rhs");
+    ck(rom::launch_assemble(dq, R, NT, dhat, ldd, q2t, c->stream), "assemble");
+    ck(rom::launch_transpose(dq, R, NT, qrows, c->stream), "transpose");
+    rom_gram(c, dhat, ldd, KK, D, g);
+    ck(rom::launch_rhs(dhat, ldd, q2t, KK, D, R, rhs, c->stream), "rhs");
+
+    // this rank's candidates, solved / integrated / scored in batches that fit
+    const size_t n_reg = n1 * n2;
+    const auto mine = distribute_pairs(n_reg, c->rank, c->size);
+    const size_t np = mine.second - mine.first;
+    const size_t per_pair = static_cast<size_t>(D) * D + static_cast<size_t>(D) * r + nt_p * r;
+    const size_t batch = std::max<size_t>(1, std::min<size_t>(std::max<size_t>(np, 1),
+                                                               (size_t(8) << 30) / (per_pair * sizeof(double))));
+    std::string err;
+    const size_t lwork = np ? c->solver.potrf_workspace_doubles(D, &err) : 0;
+    if (np && !err.empty()) fail(DOPINF_B200_ERR_DEVICE, err);
+    double* work = c->rom_work.get<double>(std::max<size_t>(lwork, 1), "potrf workspace");
+    int* info = c->rom_info.get<int>(2 * batch, "potrf info");
+    double* betas = c->rom_betas.get<double>(2 * batch, "betas");
+    double* lhs = c->rom_lhs.get<double>(batch * D * D, "lhs");
+    double* rhsb = c->rom_rhsb.get<double>(batch * D * r, "rhs batch");
+    double* traj = c->rom_traj.get<double>(batch * nt_p * r, "trajectories");
+    double* scores = c->rom_scores.get<double>(batch * rom::kScoreFields, "scores");
+    cudaEvent_t ev[2];
+    ck(cudaEventCreate(&ev[0]), "event");
+    ck(cudaEventCreate(&ev[1]), "event");
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            cudaEventDestroy(e[0]);
+            cudaEventDestroy(e[1]);
+        }
+    } evg{ev};
+
+    double best_err = std::numeric_limits<double>::infinity();
+    size_t best = n_reg;
+    double n_diverged = 0.0, n_growth = 0.0, rom_ms = 0.0;
+    std::vector<double> best_traj;
+    for (size_t p0 = mine.first; p0 < mine.second; p0 += batch) {
+        const size_t nb = std::min(batch, mine.second - p0);
+        std::vector<double> hb(2 * nb);
+        for (size_t k = 0; k < nb; ++k) {
+            hb[k] = b1[(p0 + k) / n2];
+            hb[nb + k] = b2[(p0 + k) % n2];
+        }
+        ck(cudaMemcpyAsync(betas, hb.data(), 2 * nb * sizeof(double), cudaMemcpyHostToDevice, c->stream), "betas");
+        ck(rom::launch_systems(g, D, R, betas, betas + nb, static_cast<int>(nb), rhs, lhs, rhsb, c->stream),
+           "systems");
+        ck(cudaMemsetAsync(info, 0, 2 * nb * sizeof(int), c->stream), "memset");
+        if (c->solver.spd_solve(lhs, D, static_cast<int>(nb), rhsb, R, work, lwork, info, c->stream, &err) !=
+            cudaSuccess) {
+            fail(DOPINF_B200_ERR_DEVICE, err);
+        }
+        ck(cudaEventRecord(ev[0], c->stream), "event");
+        ck(rom::launch_integrate(rhsb, R, qrows, NTP, static_cast<int>(nb), traj, c->stream), "integrate");
+        ck(cudaEventRecord(ev[1], c->stream), "event");
+        ck(rom::launch_score(traj, NTP, R, qrows, NT, static_cast<int>(nb), scores, c->stream), "score");
+        std::vector<int> hinfo(2 * nb);
+        std::vector<double> sc(nb * rom::kScoreFields);
+        ck(cudaMemcpyAsync(hinfo.data(), info, hinfo.size() * sizeof(int), cudaMemcpyDeviceToHost, c->stream),
+           "info D2H");
+        ck(cudaMemcpyAsync(sc.data(), scores, sc.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+           "scores D2H");
+        c->sync("grid search");
+        float f = 0.0f;
+        cudaEventElapsedTime(&f, ev[0], ev[1]);
+        rom_ms += f;
+        // pairs in index order, as the reference's loop (rom_search.cpp:214-225)
+        for (size_t k = 0; k < nb; ++k) {
+            if (hinfo[k] != 0 || hinfo[nb + k] != 0) {
+                fail(DOPINF_B200_ERR_SOLVE, "positive definite solve failed (dposv info=" +
+                                                std::to_string(hinfo[k] != 0 ? hinfo[k] : hinfo[nb + k]) + ")");
+            }
+            const double* o = &sc[k * rom::kScoreFields];
+            double score = std::numeric_limits<double>::infinity();
+            if (o[0] == 0.0) {
+                n_diverged += 1.0;
+            } else {
+                if (o[3] >= 0.0) {
+                    fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "training_error: reference row " +
+                                                               std::to_string(static_cast<long long>(o[3])) +
+                                                               " has zero norm");
+                }
+                if (o[4] != 0.0) {
+                    fail(DOPINF_B200_ERR_INVALID_ARGUMENT,
+                         "growth_ratio: training data is constant; deviation ratio undefined");
+                }
+                if (o[2] < max_growth) {
+                    score = o[1];
+                } else {
+                    n_growth += 1.0;
+                }
+            }
+            if (score < best_err) {
+                best_err = score;
+                best = p0 + k;
+                best_traj.resize(nt_p * r);
+                ck(cudaMemcpy(best_traj.data(), traj + k * nt_p * r, nt_p * r * sizeof(double),
+                              cudaMemcpyDeviceToHost),
+                   "trajectory D2H");
+            }
+        }
+    }
+
+    // agree on the winner across ranks (rom_search.cpp:227-261)
+    GridOutcome out;
+    double global_min = best_err;
+    if (c->size > 1) {
+        std::vector<double> v = {best_err};
+        host_allreduce(c, v.data(), 1, ncclMin);
+        global_min = v[0];
+    }
+    if (global_min == std::numeric_limits<double>::infinity()) {
+        std::vector<double> counts = {n_diverged, n_growth};
+        if (c->size > 1) host_allreduce(c, counts.data(), 2, ncclSum);
+        fail(DOPINF_B200_ERR_NO_ADMISSIBLE_PAIR,
+             "no admissible regularization pair among " + std::to_string(n_reg) + " candidates (" +
+                 std::to_string(static_cast<long>(counts[0])) + " diverged, " +
+                 std::to_string(static_cast<long>(counts[1])) + " exceeded growth bound " +
+                 std::to_string(max_growth) + ")");
+    }
+    int owner = 0;
+    if (c->size > 1) {
+        std::vector<double> claim = {best_err == global_min ? static_cast<double>(c->rank)
+                                                            : static_cast<double>(c->size)};
+        host_allreduce(c, claim.data(), 1, ncclMin);
+        owner = static_cast<int>(claim[0]);
+    }
+    std::vector<double> packet(3 + nt_p * r, 0.0);
+    if (c->rank == owner) {
+        packet[0] = b1[best / n2];
+        packet[1] = b2[best % n2];
+        packet[2] = rom_ms * 1e-3;
+        std::copy(best_traj.begin(), best_traj.end(), packet.begin() + 3);
+    }
+    if (c->size > 1) {
+        double* dp = c->rom_packet.get<double>(packet.size(), "packet");
+        ck(cudaMemcpyAsync(dp, packet.data(), packet.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+           "packet H2D");
+        ckn(ncclBroadcast(dp, dp, packet.size(), ncclFloat64, owner, c->comm, c->stream), "broadcast");
+        ck(cudaMemcpyAsync(packet.data(), dp, packet.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+           "packet D2H");
+        c->sync("broadcast");
+    }
+    out.beta1 = packet[0];
+    out.beta2 = packet[1];
+    out.rom_seconds = packet[2];
+    out.train_err = global_min;
+    out.owner = owner;
+    if (traj_host) std::memcpy(traj_host, packet.data() + 3, nt_p * r * sizeof(double));
+    return out;
+}
+
 // T_r operand: the caller's host T_r (uploaded) or, for tr_host == nullptr,
 // the context's device T_r from dopinf_b200_reduced_map.
 const double* tr_operand(dopinf_b200_ctx* c, const double* tr_host, size_t nt, size_t r) {
@@ -867,6 +1105,8 @@ void do_project(dopinf_b200_ctx* c, const double* tr_host, const double* d_dev, 
     ck(project::launch_project(dtr, d_dev, static_cast<int>(nt), static_cast<int>(r), dq, c->stream),
        "project");
     c->record(DOPINF_B200_STAGE_PROJECT, 1);
+    c->qhat_r = r;
+    c->qhat_nt = nt;
     if (qhat_host) c->d2h(qhat_host, dq, nt * r * sizeof(double), "qhat D2H");
 }
 
@@ -1106,6 +1346,7 @@ const char* dopinf_b200_status_string(int status) {
         case DOPINF_B200_ERR_RANK_DEFICIENCY: return "RankDeficiencyError";
         case DOPINF_B200_ERR_SOLVE: return "SolveError";
         case DOPINF_B200_ERR_DATA_FORMAT: return "DataFormatError";
+        case DOPINF_B200_ERR_NO_ADMISSIBLE_PAIR: return "NoAdmissiblePairError";
         default: return "unknown status";
     }
 }
@@ -1180,7 +1421,10 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
     for (DBuf* b : {&c->tiles, &c->work, &c->counters, &c->packed, &c->gather, &c->dmat, &c->dhost_in,
                     &c->scales, &c->tr, &c->trt, &c->qhat, &c->sel, &c->rows_out, &c->span, &c->eig_a,
                     &c->eig_w, &c->eig_work, &c->eig_info, &c->eig_v, &c->eig_lambda, &c->tr_dev, &c->field_qt,
-                    &c->field_means, &c->field_scales, &c->field_ring}) {
+                    &c->field_means, &c->field_scales, &c->field_ring, &c->rom_qhat, &c->rom_dhat, &c->rom_q2t,
+                    &c->rom_qrows, &c->rom_rhs, &c->rom_g, &c->rom_lhs, &c->rom_rhsb, &c->rom_betas, &c->rom_traj,
+                    &c->rom_scores, &c->rom_work, &c->rom_info, &c->rom_tiles, &c->rom_gwork, &c->rom_counters,
+                    &c->rom_packed, &c->rom_packet}) {
         b->release();
     }
     c->staging.release();
@@ -1570,6 +1814,51 @@ int dopinf_b200_basis_device(dopinf_b200_block* b, double** phi, size_t* ld) {
         require(b->phi_ld > 0, "basis_device: no basis computed");
         *phi = static_cast<double*>(b->phi.p);
         *ld = static_cast<size_t>(b->phi_ld);
+    });
+}
+
+int dopinf_b200_grid_search(dopinf_b200_ctx* c, const double* qhat, size_t r, size_t nt, const double* b1,
+                            size_t n1, const double* b2, size_t n2, double max_growth, size_t nt_p,
+                            double* pair_opt, double* train_err, int* owner, double* rom_seconds,
+                            double* trajectory) {
+    return guarded(c, [&] {
+        const GridOutcome o = do_grid_search(c, qhat, r, nt, b1, n1, b2, n2, max_growth, nt_p, trajectory);
+        if (pair_opt) {
+            pair_opt[0] = o.beta1;
+            pair_opt[1] = o.beta2;
+        }
+        if (train_err) *train_err = o.train_err;
+        if (owner) *owner = o.owner;
+        if (rom_seconds) *rom_seconds = o.rom_seconds;
+    });
+}
+
+int dopinf_b200_rom_integrate(dopinf_b200_ctx* c, const double* a, const double* f, const double* cvec, size_t r,
+                              const double* q0, size_t n_steps, double* traj, int* finite) {
+    return guarded(c, [&] {
+        if (n_steps < 1) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "integrate: need at least one step");
+        require(r >= 1 && r <= 180, "integrate: r must lie in [1, 180]");
+        require(a && f && cvec && q0, "integrate: null operator");
+        const size_t s = r * (r + 1) / 2, d = r + s + 1;
+        // the solve's layout: column i = [A_i, F_i, c_i] (column-major d × r)
+        std::vector<double> x(d * r);
+        for (size_t i = 0; i < r; ++i) {
+            std::memcpy(&x[i * d], a + i * r, r * sizeof(double));
+            std::memcpy(&x[i * d + r], f + i * s, s * sizeof(double));
+            x[i * d + r + s] = cvec[i];
+        }
+        double* dx = c->rom_rhsb.get<double>(d * r, "operators");
+        double* dq0 = c->rom_qrows.get<double>(r, "q0");
+        double* dt = c->rom_traj.get<double>(n_steps * r, "trajectory");
+        ck(cudaMemcpyAsync(dx, x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "ops H2D");
+        ck(cudaMemcpyAsync(dq0, q0, r * sizeof(double), cudaMemcpyHostToDevice, c->stream), "q0 H2D");
+        ck(rom::launch_integrate(dx, static_cast<int>(r), dq0, static_cast<int>(n_steps), 1, dt, c->stream),
+           "integrate");
+        std::vector<double> h(n_steps * r);
+        ck(cudaMemcpyAsync(h.data(), dt, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        c->sync("integrate");
+        if (traj) std::memcpy(traj, h.data(), h.size() * sizeof(double));
+        if (finite) *finite = std::all_of(h.begin(), h.end(), [](double v) { return std::isfinite(v); }) ? 1 : 0;
     });
 }
 

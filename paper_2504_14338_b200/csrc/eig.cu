@@ -33,6 +33,10 @@ using BufFn = cusolverStatus_t (*)(cusolverDnHandle_t, cusolverEigMode_t, cublas
                                    const double*, int*);
 using SyevdFn = cusolverStatus_t (*)(cusolverDnHandle_t, cusolverEigMode_t, cublasFillMode_t, int, double*, int,
                                      double*, double*, int, int*);
+using PotrfBufFn = cusolverStatus_t (*)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, int*);
+using PotrfFn = cusolverStatus_t (*)(cusolverDnHandle_t, cublasFillMode_t, int, double*, int, double*, int, int*);
+using PotrsFn = cusolverStatus_t (*)(cusolverDnHandle_t, cublasFillMode_t, int, int, const double*, int, double*, int,
+                                     int*);
 
 struct Api {
     void* dl = nullptr;
@@ -41,6 +45,9 @@ struct Api {
     SetStreamFn set_stream = nullptr;
     BufFn buffer_size = nullptr;
     SyevdFn syevd = nullptr;
+    PotrfBufFn potrf_buffer_size = nullptr;
+    PotrfFn potrf = nullptr;
+    PotrsFn potrs = nullptr;
     std::string error;
 };
 
@@ -62,8 +69,12 @@ const Api& api() {
         a.set_stream = reinterpret_cast<SetStreamFn>(dlsym(a.dl, "cusolverDnSetStream"));
         a.buffer_size = reinterpret_cast<BufFn>(dlsym(a.dl, "cusolverDnDsyevd_bufferSize"));
         a.syevd = reinterpret_cast<SyevdFn>(dlsym(a.dl, "cusolverDnDsyevd"));
-        if (!a.create || !a.destroy || !a.set_stream || !a.buffer_size || !a.syevd) {
-            a.error = "cuSOLVER is missing dsyevd entry points";
+        a.potrf_buffer_size = reinterpret_cast<PotrfBufFn>(dlsym(a.dl, "cusolverDnDpotrf_bufferSize"));
+        a.potrf = reinterpret_cast<PotrfFn>(dlsym(a.dl, "cusolverDnDpotrf"));
+        a.potrs = reinterpret_cast<PotrsFn>(dlsym(a.dl, "cusolverDnDpotrs"));
+        if (!a.create || !a.destroy || !a.set_stream || !a.buffer_size || !a.syevd || !a.potrf_buffer_size ||
+            !a.potrf || !a.potrs) {
+            a.error = "cuSOLVER is missing dsyevd / dpotrf / dpotrs entry points";
         }
     });
     return a;
@@ -192,6 +203,57 @@ size_t Solver::workspace_doubles(int n, std::string* err) {
         return 0;
     }
     return static_cast<size_t>(lwork);
+}
+
+bool Solver::ensure_handle(std::string* err) {
+    const Api& x = api();
+    if (!x.error.empty()) {
+        *err = x.error;
+        return false;
+    }
+    if (!handle_) {
+        cusolverDnHandle_t h;
+        if (x.create(&h) != CUSOLVER_STATUS_SUCCESS) {
+            *err = "cusolverDnCreate failed";
+            return false;
+        }
+        handle_ = h;
+    }
+    return true;
+}
+
+size_t Solver::potrf_workspace_doubles(int n, std::string* err) {
+    if (!ensure_handle(err)) return 0;
+    int lwork = 0;
+    if (api().potrf_buffer_size(static_cast<cusolverDnHandle_t>(handle_), CUBLAS_FILL_MODE_LOWER, n, nullptr, n,
+                                &lwork) != CUSOLVER_STATUS_SUCCESS) {
+        *err = "cusolverDnDpotrf_bufferSize failed";
+        return 0;
+    }
+    return static_cast<size_t>(lwork);
+}
+
+cudaError_t Solver::spd_solve(double* a, int n, int batch, double* b, int nrhs, double* work_dev,
+                              size_t work_doubles, int* info_dev, cudaStream_t stream, std::string* err) {
+    if (!ensure_handle(err)) return cudaErrorNotSupported;
+    const Api& x = api();
+    auto h = static_cast<cusolverDnHandle_t>(handle_);
+    x.set_stream(h, stream);
+    for (int i = 0; i < batch; ++i) {
+        double* ai = a + static_cast<size_t>(i) * n * n;
+        double* bi = b + static_cast<size_t>(i) * n * nrhs;
+        if (x.potrf(h, CUBLAS_FILL_MODE_LOWER, n, ai, n, work_dev, static_cast<int>(work_doubles), info_dev + i) !=
+            CUSOLVER_STATUS_SUCCESS) {
+            *err = "cusolverDnDpotrf failed";
+            return cudaErrorUnknown;
+        }
+        if (x.potrs(h, CUBLAS_FILL_MODE_LOWER, n, nrhs, ai, n, bi, n, info_dev + batch + i) !=
+            CUSOLVER_STATUS_SUCCESS) {
+            *err = "cusolverDnDpotrs failed";
+            return cudaErrorUnknown;
+        }
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_reduced_map(const double* v, const double* lambda, int n, int r, double* tr, cudaStream_t stream) {

@@ -21,7 +21,15 @@ public:
     cudaError_t run(const double* d, int n, double* a_scratch, double* w, double* work_dev, size_t work_doubles,
                     int* info_dev, double* v_out, double* lambda_out, cudaStream_t stream, std::string* err);
 
+    // Cholesky solves of `batch` SPD n×n systems a_i (column-major, lda n;
+    // factored in place) with nrhs right-hand sides b_i (column-major, ldb n;
+    // overwritten by the solutions). info_dev[2·batch]: potrf infos, then potrs.
+    size_t potrf_workspace_doubles(int n, std::string* err);
+    cudaError_t spd_solve(double* a, int n, int batch, double* b, int nrhs, double* work_dev, size_t work_doubles,
+                          int* info_dev, cudaStream_t stream, std::string* err);
+
 private:
+    bool ensure_handle(std::string* err);
     void* handle_ = nullptr;
 };
 

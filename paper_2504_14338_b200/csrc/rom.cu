@@ -1,0 +1,324 @@
+// rom.cu — §8(f) next-row 2: the OpInf regularisation grid search on the
+// device (reference proj/src/rom_search.cpp:185-262, opinf.cpp:34-92).
+//
+// The reference, per candidate pair (β1, β2): rebuilds Dhatᵀ Dhat, solves
+// (DhatᵀDhat + diag γ) X = Dhatᵀ Qhat2ᵀ with LAPACK dposv, integrates the
+// quadratic ROM for nt_p steps and scores it. Here the pair-independent work
+// runs once — Dhat (assemble_data) on the device, DhatᵀDhat on the FP64
+// tensor pipe (the Gram kernel), Dhatᵀ Qhat2ᵀ in the reference's FMA order —
+// then every pair of this rank's slice gets its Cholesky solve (cuSOLVER
+// dpotrf/dpotrs), all pairs integrate concurrently (one CTA per pair) and are
+// scored in one kernel; the winner is chosen as the reference does.
+//
+// The integrator reproduces rom_step_into (rom_search.cpp:38-48) bit for bit:
+// per output i, c_i + dot(A_i, q) + dot(F_i, quad(q)) with kernels::dot's
+// AVX2 order (kernels_avx2.cpp:32-46: lanes l = 0..7 each an FMA chain over
+// elements 8b + l, lanes 0..3 also take the trailing block of four; then
+// (l0+l4, l1+l5, l2+l6, l3+l7) summed as ((v0+v2)+(v1+v3)); the scalar tail
+// unfused). Eight threads run the eight chains of one output. The scores
+// follow training_error / growth_ratio (rom_search.cpp:94-145) in the
+// reference's (unfused) order.
+#include <algorithm>
+
+#include "common.cuh"
+#include "rom.h"
+
+namespace dopinf_b200 {
+namespace rom {
+
+namespace {
+
+// opinf.cpp:34-58 assemble_data: Dhat row k = [q_k, quad(q_k), 1], target row
+// k = q_{k+1}; qhat is r × nt row-major (pitch nt).
+__global__ void assemble_kernel(const double* __restrict__ qhat, int r, int nt, double* __restrict__ dhat,
+                                size_t ldd, double* __restrict__ q2t) {
+    const int k = blockIdx.x;  // 0 .. nt-2
+    const int s = r * (r + 1) / 2;
+    double* row = dhat + static_cast<size_t>(k) * ldd;
+    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+        row[i] = qhat[static_cast<size_t>(i) * nt + k];
+        q2t[static_cast<size_t>(k) * r + i] = qhat[static_cast<size_t>(i) * nt + k + 1];
+    }
+    // quad_features_into (opinf.cpp:8-15): pos runs over i ≤ j in row order
+    for (int pos = threadIdx.x; pos < s; pos += blockDim.x) {
+        // invert pos = i*r - i*(i-1)/2 + (j - i)
+        int i = 0, base = 0;
+        while (base + (r - i) <= pos) {
+            base += r - i;
+            ++i;
+        }
+        const int j = i + (pos - base);
+        row[r + pos] = __dmul_rn(qhat[static_cast<size_t>(i) * nt + k], qhat[static_cast<size_t>(j) * nt + k]);
+    }
+    if (threadIdx.x == 0) {
+        row[r + s] = 1.0;
+        for (size_t c = r + s + 1; c < ldd; ++c) row[c] = 0.0;  // pitch padding
+    }
+}
+
+// rhs (d × r, column-major: rhs[i + j·d]) = Dhatᵀ Qhat2ᵀ with linalg::matmul_tn's
+// order (linalg.cpp:28-37: c.row(i) += a(l, i)·b.row(l) by axpy, an FMA chain over l).
+__global__ void matmul_tn_cm_kernel(const double* __restrict__ a, size_t lda, const double* __restrict__ b, int K,
+                                    int d, int r, double* __restrict__ out) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= static_cast<long long>(d) * r) return;
+    const int i = static_cast<int>(e % d), j = static_cast<int>(e / d);
+    double acc = 0.0;
+    for (int l = 0; l < K; ++l) acc = __fma_rn(a[static_cast<size_t>(l) * lda + i], b[static_cast<size_t>(l) * r + j], acc);
+    out[e] = acc;
+}
+
+// Pair p's system: lhs_p = G + diag(γ_p) (opinf.cpp:76-77; build_regularizer
+// opinf.cpp:60-67: β1 on the r state columns and the ones column, β2 on the s
+// quadratic ones), rhs_p = rhs.
+__global__ void systems_kernel(const double* __restrict__ g, int d, int r, const double* __restrict__ beta1,
+                               const double* __restrict__ beta2, const double* __restrict__ rhs,
+                               double* __restrict__ lhs, double* __restrict__ rhs_batch) {
+    const int p = blockIdx.y;
+    const size_t dd = static_cast<size_t>(d) * d;
+    const int s = r * (r + 1) / 2;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < dd;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        double v = g[e];
+        const int i = static_cast<int>(e / d), j = static_cast<int>(e % d);
+        if (i == j) v = __dadd_rn(v, (i >= r && i < r + s) ? beta2[p] : beta1[p]);
+        lhs[static_cast<size_t>(p) * dd + e] = v;
+    }
+    const size_t dr = static_cast<size_t>(d) * r;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < dr;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        rhs_batch[static_cast<size_t>(p) * dr + e] = rhs[e];
+    }
+}
+
+// One kernels::dot (kernels_avx2.cpp:32-46) by the 8 lanes of a group:
+// lane l's FMA chain, the lane combine and hsum, lane 0's unfused tail.
+// Returns the dot on lane 0 of the group (other lanes: garbage).
+__device__ __forceinline__ double group_dot(const double* __restrict__ a, const double* __restrict__ b, int n,
+                                            int l, unsigned gmask) {
+    const int nb8 = n / 8;
+    const bool four = n - 8 * nb8 >= 4;
+    double acc = 0.0;
+    for (int blk = 0; blk < nb8; ++blk) acc = __fma_rn(a[8 * blk + l], b[8 * blk + l], acc);
+    if (four && l < 4) acc = __fma_rn(a[8 * nb8 + l], b[8 * nb8 + l], acc);
+    // v_l = acc0_l + acc1_l (lanes l and l + 4)
+    const double hi = __shfl_down_sync(gmask, acc, 4, 8);
+    const double v = __dadd_rn(acc, hi);
+    // hsum: (v0 + v2) + (v1 + v3)
+    const double v2 = __shfl_down_sync(gmask, v, 2, 8);
+    const double w = __dadd_rn(v, v2);  // lane 0: v0+v2, lane 1: v1+v3
+    const double w1 = __shfl_down_sync(gmask, w, 1, 8);
+    double h = __dadd_rn(w, w1);
+    if (l == 0) {
+        for (int t = 8 * nb8 + (four ? 4 : 0); t < n; ++t) h = __dadd_rn(h, __dmul_rn(a[t], b[t]));
+    }
+    return h;
+}
+
+// All pairs' ROMs in parallel, one CTA per pair: integrate (rom_search.cpp:
+// 60-85) from q0 for n_steps rows. ops_p: column-major d × r (column i =
+// [A_i (r), F_i (s), c_i]: the solve's output layout). traj_p: n_steps × r.
+__global__ void __launch_bounds__(1024)
+    integrate_kernel(const double* __restrict__ ops, int r, const double* __restrict__ q0, int n_steps,
+                     double* __restrict__ traj) {
+    extern __shared__ double sm[];
+    const int s = r * (r + 1) / 2;
+    const int d = r + s + 1;
+    const int p = blockIdx.x;
+    const double* x = ops + static_cast<size_t>(p) * d * r;
+    double* tp = traj + static_cast<size_t>(p) * n_steps * r;
+    double* q = sm;           // r: current state
+    double* feat = sm + r;    // s: quad(q)
+    int* pi = reinterpret_cast<int*>(feat + s);  // s: (i << 16 | j) of feature pos
+    const int groups = blockDim.x / 8;
+    const int g = threadIdx.x / 8, l = threadIdx.x % 8;
+    const unsigned gmask = 0xFFu << (8 * ((threadIdx.x % 32) / 8));
+    for (int i = 0, pos = 0; i < r; ++i) {
+        for (int j = i; j < r; ++j, ++pos) {
+            if (pos % blockDim.x == static_cast<int>(threadIdx.x)) pi[pos] = (i << 16) | j;
+        }
+    }
+    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+        q[i] = q0[i];
+        tp[i] = q0[i];
+    }
+    __syncthreads();
+    for (int k = 0; k + 1 < n_steps; ++k) {
+        for (int pos = threadIdx.x; pos < s; pos += blockDim.x) {
+            const int e = pi[pos];
+            feat[pos] = __dmul_rn(q[e >> 16], q[e & 0xFFFF]);
+        }
+        __syncthreads();
+        double outv[8];  // outputs of this group (r ≤ 8·groups·8)
+        int n_out = 0;
+        for (int i = g; i < r; i += groups, ++n_out) {
+            const double* col = x + static_cast<size_t>(i) * d;
+            const double da = group_dot(col, q, r, l, gmask);
+            const double df = group_dot(col + r, feat, s, l, gmask);
+            outv[n_out & 7] = __dadd_rn(__dadd_rn(col[r + s], da), df);  // c_i + dot(A_i, q) + dot(F_i, feat)
+        }
+        __syncthreads();  // everyone has read q and feat
+        n_out = 0;
+        for (int i = g; i < r; i += groups, ++n_out) {
+            if (l == 0) {
+                q[i] = outv[n_out & 7];
+                tp[static_cast<size_t>(k + 1) * r + i] = outv[n_out & 7];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Scores of one pair per CTA: finite (integrate's check), training_error over
+// the first nt rows against qhat_rows (nt × r), growth_ratio; flags a zero-norm
+// reference row / constant training data the way the reference throws.
+__global__ void __launch_bounds__(256)
+    score_kernel(const double* __restrict__ traj, int n_steps, int r, const double* __restrict__ qrows, int nt,
+                 double* __restrict__ out) {
+    const int p = blockIdx.x;
+    const double* t = traj + static_cast<size_t>(p) * n_steps * r;
+    __shared__ double red[256];
+    __shared__ int flag;
+    if (threadIdx.x == 0) flag = 0;
+    __syncthreads();
+    // finite over the whole trajectory
+    int bad = 0;
+    for (size_t e = threadIdx.x; e < static_cast<size_t>(n_steps) * r; e += blockDim.x) bad |= !isfinite(t[e]);
+    if (bad) atomicOr(&flag, 1);
+    __syncthreads();
+    const bool finite = flag == 0;
+    // training_error (rom_search.cpp:94-115): max over rows of sqrt(num/den)
+    double worst = 0.0;
+    int zero_row = -1;
+    for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+        double num = 0.0, den = 0.0;
+        for (int j = 0; j < r; ++j) {
+            const double ref = qrows[static_cast<size_t>(k) * r + j];
+            const double diff = __dsub_rn(t[static_cast<size_t>(k) * r + j], ref);
+            num = __dadd_rn(num, __dmul_rn(diff, diff));
+            den = __dadd_rn(den, __dmul_rn(ref, ref));
+        }
+        if (den == 0.0) {
+            if (zero_row < 0) zero_row = k;
+        } else {
+            worst = fmax(worst, sqrt(num / den));
+        }
+    }
+    red[threadIdx.x] = worst;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + st]);
+        __syncthreads();
+    }
+    const double train_err = red[0];
+    __syncthreads();
+    // growth_ratio (rom_search.cpp:117-145): per-mode mean of the training rows
+    double train_dev = 0.0, trial_dev = 0.0;
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        double mu = 0.0;
+        for (int k = 0; k < nt; ++k) mu = __dadd_rn(mu, qrows[static_cast<size_t>(k) * r + j]);
+        mu = __ddiv_rn(mu, static_cast<double>(nt));
+        for (int k = 0; k < nt; ++k) train_dev = fmax(train_dev, fabs(__dsub_rn(qrows[static_cast<size_t>(k) * r + j], mu)));
+        for (int k = 0; k < n_steps; ++k) trial_dev = fmax(trial_dev, fabs(__dsub_rn(t[static_cast<size_t>(k) * r + j], mu)));
+    }
+    red[threadIdx.x] = train_dev;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + st]);
+        __syncthreads();
+    }
+    const double tdev = red[0];
+    __syncthreads();
+    red[threadIdx.x] = trial_dev;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + st]);
+        __syncthreads();
+    }
+    const double rdev = red[0];
+    __syncthreads();
+    // first zero-norm row over the block
+    __shared__ int zr;
+    if (threadIdx.x == 0) zr = 0x7FFFFFFF;
+    __syncthreads();
+    if (zero_row >= 0) atomicMin(&zr, zero_row);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double* o = out + static_cast<size_t>(p) * kScoreFields;
+        o[0] = finite ? 1.0 : 0.0;
+        o[1] = train_err;
+        o[2] = tdev == 0.0 ? 0.0 : rdev / tdev;
+        o[3] = zr == 0x7FFFFFFF ? -1.0 : static_cast<double>(zr);
+        o[4] = tdev == 0.0 ? 1.0 : 0.0;
+    }
+}
+
+__global__ void transpose_kernel(const double* __restrict__ a, int rows, int cols, double* __restrict__ t) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= static_cast<long long>(rows) * cols) return;
+    const int i = static_cast<int>(e / cols), j = static_cast<int>(e % cols);
+    t[static_cast<size_t>(j) * rows + i] = a[e];
+}
+
+}  // namespace
+
+cudaError_t launch_assemble(const double* qhat, int r, int nt, double* dhat, size_t ldd, double* q2t,
+                            cudaStream_t stream) {
+    if (nt < 2) return cudaSuccess;
+    assemble_kernel<<<nt - 1, 256, 0, stream>>>(qhat, r, nt, dhat, ldd, q2t);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rhs(const double* dhat, size_t ldd, const double* q2t, int K, int d, int r, double* rhs_cm,
+                       cudaStream_t stream) {
+    const long long total = static_cast<long long>(d) * r;
+    matmul_tn_cm_kernel<<<static_cast<int>((total + 127) / 128), 128, 0, stream>>>(dhat, ldd, q2t, K, d, r, rhs_cm);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_systems(const double* g, int d, int r, const double* beta1, const double* beta2, int n_pairs,
+                           const double* rhs_cm, double* lhs, double* rhs_batch, cudaStream_t stream) {
+    if (n_pairs <= 0) return cudaSuccess;
+    const size_t dd = static_cast<size_t>(d) * d;
+    const int gx = static_cast<int>(std::min<size_t>((dd + 255) / 256, 256));
+    systems_kernel<<<dim3(gx, n_pairs), 256, 0, stream>>>(g, d, r, beta1, beta2, rhs_cm, lhs, rhs_batch);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_integrate(const double* ops, int r, const double* q0, int n_steps, int n_pairs, double* traj,
+                             cudaStream_t stream) {
+    if (n_pairs <= 0) return cudaSuccess;
+    const int s = r * (r + 1) / 2;
+    const int threads = std::min(1024, std::max(32, ((8 * r + 31) / 32) * 32));
+    const int groups = threads / 8;
+    if ((r + groups - 1) / groups > 8) return cudaErrorInvalidValue;  // outputs per group
+    const size_t smem = static_cast<size_t>(r + s) * sizeof(double) + static_cast<size_t>(s) * sizeof(int);
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(integrate_kernel), 200 * 1024);
+    if (e != cudaSuccess) return e;
+    integrate_kernel<<<n_pairs, threads, smem, stream>>>(ops, r, q0, n_steps, traj);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_score(const double* traj, int n_steps, int r, const double* qrows, int nt, int n_pairs,
+                         double* out, cudaStream_t stream) {
+    if (n_pairs <= 0) return cudaSuccess;
+    score_kernel<<<n_pairs, 256, 0, stream>>>(traj, n_steps, r, qrows, nt, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const double* a, int rows, int cols, double* t, cudaStream_t stream) {
+    const long long total = static_cast<long long>(rows) * cols;
+    if (total == 0) return cudaSuccess;
+    transpose_kernel<<<static_cast<int>((total + 255) / 256), 256, 0, stream>>>(a, rows, cols, t);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace rom
+}  // namespace dopinf_b200

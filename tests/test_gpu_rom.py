@@ -1,0 +1,140 @@
+"""Step IV on the B200 through the C ABI: dopinf_b200_rom_integrate is
+bit-identical to the reference's rom_search::integrate for the same operators,
+and dopinf_b200_grid_search picks the reference's pair with the reference's
+training error and ROM trajectory (north star ROM tolerance 1e-8: the
+operators come from cuSOLVER's Cholesky instead of LAPACK dposv, so they agree
+to rounding, not bitwise), on the committed golden run and on the reference
+run live here. Error paths carry the reference's classes and messages."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROM_TOL = 1e-8  # north star: ROM within 1e-8
+
+
+def api():
+    from paper_2504_14338_b200 import api as a
+
+    return a
+
+
+def golden():
+    return np.load(Path(__file__).parent / "golden" / "reference_vectors.npz")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _qhat(oracle, r, nt, seed, decay=0.05):
+    """A smooth r-mode reduced trajectory (damped oscillations + a little noise)."""
+    rng = oracle.rng(seed)
+    t = np.arange(nt) * 0.05
+    q = np.empty((r, nt))
+    for i in range(r):
+        q[i] = np.exp(-decay * (i + 1) * t) * np.cos((i + 2) * t + i) * (1.0 / (i + 1))
+    return q + 1e-3 * rng.matrix(r, nt)
+
+
+@pytest.mark.parametrize("r,nt,steps", [(1, 20, 50), (3, 40, 80), (4, 40, 80), (5, 30, 400), (9, 60, 120),
+                                        (12, 50, 100)])
+def test_integrate_bit_identical(ctx, oracle, reference, r, nt, steps):
+    a = api()
+    q = _qhat(oracle, r, nt, seed=r)
+    A, F, c = reference.solve_opinf(q, 1e-3, 1e-1)
+    want, fin_w = reference.integrate(A, F, c, q[:, 0], steps)
+    got, fin_g = a.rom_integrate(ctx, A, F, c, q[:, 0], steps)
+    assert fin_g == fin_w
+    assert np.array_equal(got, want)  # kernels::dot's lane order, unfused tail, c + dotA + dotF
+
+
+def test_integrate_divergent(ctx, oracle, reference):
+    a = api()
+    r = 3
+    A = np.eye(r) * 1.5
+    F = np.ones((r, r * (r + 1) // 2)) * 0.7
+    c = np.ones(r)
+    q0 = np.array([1.0, 2.0, 3.0])
+    want, fin_w = reference.integrate(A, F, c, q0, 60)
+    got, fin_g = a.rom_integrate(ctx, A, F, c, q0, 60)
+    assert not fin_w and not fin_g
+    both = np.isfinite(want) & np.isfinite(got)
+    assert np.array_equal(np.isfinite(want), np.isfinite(got))
+    assert np.array_equal(got[both], want[both])
+
+
+def test_grid_search_golden(ctx):
+    # the reference's own run, committed by tests/golden/make_golden.py
+    a = api()
+    g = golden()
+    qhat = g["pipeline_qhat"]
+    nt = qhat.shape[1]
+    cfg = a.SearchConfig(list(np.logspace(-6, 2, 4)), list(np.logspace(-6, 2, 4)), 1.2, 2 * nt)
+    out = a.grid_search(qhat, cfg, ctx)
+    b1, b2, err = g["pipeline_pair_err"]
+    assert out.pair_opt == (b1, b2)
+    assert abs(out.train_err - err) <= ROM_TOL * err
+    assert rel(out.trajectory, g["pipeline_traj"]) <= ROM_TOL
+    assert out.owner_rank == 0 and out.rom_seconds > 0
+
+
+@pytest.mark.parametrize("r,nt,grid", [(4, 80, 8), (6, 120, 8), (10, 200, 6)])
+def test_grid_search_matches_reference(ctx, oracle, reference, r, nt, grid):
+    a = api()
+    q = _qhat(oracle, r, nt, seed=100 + r)
+    b1 = np.logspace(-10, 0, grid)
+    b2 = np.logspace(-4, 4, grid)
+    traj_w, pair_w, err_w = reference.grid_search(q, b1, b2, 1.2, 2 * nt)
+    out = a.grid_search(q, a.SearchConfig(list(b1), list(b2), 1.2, 2 * nt), ctx)
+    assert out.pair_opt == pair_w
+    assert abs(out.train_err - err_w) <= ROM_TOL * err_w
+    assert rel(out.trajectory, traj_w) <= ROM_TOL
+
+
+def test_grid_search_on_device_qhat(ctx, oracle, reference):
+    # Steps II-IV resident: snapshot pass -> device eig -> device T_r -> device Q̂ -> grid search
+    a = api()
+    nv, nx, nt, r = 2, 3000, 60, 5
+    b = a.LocalBlock(ctx, nv, a.RowRange(0, nx), nt)
+    b.synth_oscillator(seed=7, n_modes=6, dt=5e-2, noise=1e-4)
+    a.snapshot_pass(b, True)
+    a.eig_sym_desc(ctx)
+    a.reduced_map(ctx, r, download=False)
+    qhat = a.project_resident(ctx, None, r=r)
+    cfg = a.SearchConfig(list(np.logspace(-8, 0, 5)), list(np.logspace(-4, 4, 5)), 1.2, 2 * nt)
+    out_dev = a.grid_search(None, cfg, ctx, r=r, nt=nt)
+    out_host = a.grid_search(qhat, cfg, ctx)
+    assert out_dev.pair_opt == out_host.pair_opt
+    assert np.array_equal(out_dev.trajectory, out_host.trajectory)
+    traj_w, pair_w, err_w = reference.grid_search(qhat, cfg.b1, cfg.b2, 1.2, 2 * nt)
+    assert out_dev.pair_opt == pair_w
+    assert rel(out_dev.trajectory, traj_w) <= ROM_TOL
+
+
+def test_grid_search_errors(ctx, oracle, reference):
+    a = api()
+    from oracle.cpu import RefError
+
+    q = _qhat(oracle, 3, 30, seed=1)
+    good = dict(b1=[1e-3], b2=[1e-2], max_growth=1.2, nt_p=60)
+    cases = [dict(good, b1=[]), dict(good, b1=[1e-3, -1.0]), dict(good, b2=[0.0]), dict(good, max_growth=0.0),
+             dict(good, nt_p=29)]
+    for cfg in cases:
+        with pytest.raises(RefError) as want:
+            reference.grid_search(q, np.array(cfg["b1"]), np.array(cfg["b2"]), cfg["max_growth"], cfg["nt_p"])
+        with pytest.raises(a.InvalidArgumentError) as got:
+            a.grid_search(q, a.SearchConfig(cfg["b1"], cfg["b2"], cfg["max_growth"], cfg["nt_p"]), ctx)
+        assert str(got.value) == want.value.msg
+    # every pair rejected: the reference's NoAdmissiblePairError text, counts included
+    b1, b2 = np.logspace(-6, 0, 3), np.logspace(-2, 2, 2)
+    with pytest.raises(RefError) as want:
+        reference.grid_search(q, b1, b2, 1e-9, 60)
+    with pytest.raises(a.NoAdmissiblePairError) as got:
+        a.grid_search(q, a.SearchConfig(list(b1), list(b2), 1e-9, 60), ctx)
+    assert want.value.code == 11
+    assert str(got.value) == want.value.msg
+    with pytest.raises(a.InvalidArgumentError, match="need at least one step"):
+        a.rom_integrate(ctx, np.eye(2), np.zeros((2, 3)), np.zeros(2), np.ones(2), 0)
