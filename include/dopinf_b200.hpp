@@ -10,6 +10,7 @@
 //   dopinf_b200::pod::project(tr, d)                             pod.hpp:49
 //   dopinf_b200::postprocess::basis_rows(block, tr, rows)        postprocess.hpp:25-26
 //   dopinf_b200::postprocess::basis(block, tr)  (Φ_r of reconstruct_field, postprocess.cpp:66)
+//   dopinf_b200::rom_search::grid_search<OutcomeT>(qhat, config, comm)      rom_search.hpp:87-91
 //   dopinf_b200::postprocess::reconstruct_field(block, tr, qtilde, params)  postprocess.hpp:43-45
 //   dopinf_b200::data::partition_rows(nx, p)                     data.hpp:47
 //   dopinf_b200::data::read_header<HeaderT>(path)                data.hpp:52
@@ -52,6 +53,7 @@ using NotPsdError = ::dopinf::NotPsdError;
 using RankDeficiencyError = ::dopinf::RankDeficiencyError;
 using SolveError = ::dopinf::SolveError;
 using DataFormatError = ::dopinf::DataFormatError;
+using NoAdmissiblePairError = ::dopinf::NoAdmissiblePairError;
 #else
 struct Error : std::runtime_error {
     explicit Error(const std::string& m) : std::runtime_error(m) {}
@@ -80,6 +82,9 @@ struct SolveError : Error {
 struct DataFormatError : Error {
     using Error::Error;
 };
+struct NoAdmissiblePairError : Error {
+    using Error::Error;
+};
 #endif
 
 [[noreturn]] inline void raise(int status, const std::string& msg) {
@@ -92,6 +97,7 @@ struct DataFormatError : Error {
         case DOPINF_B200_ERR_RANK_DEFICIENCY: throw RankDeficiencyError(msg);
         case DOPINF_B200_ERR_SOLVE: throw SolveError(msg);
         case DOPINF_B200_ERR_DATA_FORMAT: throw DataFormatError(msg);
+        case DOPINF_B200_ERR_NO_ADMISSIBLE_PAIR: throw NoAdmissiblePairError(msg);
         default: throw Error(msg);
     }
 }
@@ -383,6 +389,31 @@ MatrixT project(const MatrixT& tr, const MatrixT& d) {
     return out;
 }
 }  // namespace pod
+
+namespace rom_search {
+// rom_search::grid_search (rom_search.cpp:185-262) on the device: the bound
+// Context's ranks share the candidates as distribute_pairs does (the comm
+// argument is the reference's and unused: the Context carries the ranks).
+template <class OutcomeT, class MatrixT, class ConfigT, class CommT>
+OutcomeT grid_search(const MatrixT& qhat, const ConfigT& config, CommT& /*comm*/) {
+    Context& c = detail::ctx();
+    std::vector<double> traj(config.nt_p * qhat.rows());
+    double pair[2] = {0.0, 0.0}, err = 0.0, secs = 0.0;
+    int owner = -1;
+    Context::check_exact(dopinf_b200_grid_search(c.handle(), qhat.data(), qhat.rows(), qhat.cols(), config.b1.data(),
+                                                 config.b1.size(), config.b2.data(), config.b2.size(),
+                                                 config.max_growth, config.nt_p, pair, &err, &owner, &secs,
+                                                 traj.data()),
+                         c.handle());
+    OutcomeT out;
+    out.pair_opt = {pair[0], pair[1]};
+    out.owner_rank = owner;
+    out.train_err = err;
+    out.rom_seconds = secs;
+    out.trajectory = MatrixT(config.nt_p, qhat.rows(), std::move(traj));
+    return out;
+}
+}  // namespace rom_search
 
 namespace postprocess {
 // postprocess.cpp:12-34 (bit-identical order).

@@ -339,7 +339,8 @@ int main() {
         for (std::size_t v = 0; v < spec.n_vars; ++v)
             for (std::size_t i = 0; i < spec.nx; ++i)
                 for (std::size_t t = 0; t < spec.nt; ++t) raw(v * spec.nx + i, t) = made.variables[v](i, t);
-        double traj_gap = 0, err_gap = 0, lam_gap = 0, field_same = 0, field_chain = 0;
+        double traj_gap = 0, err_gap = 0, lam_gap = 0, field_same = 0, field_chain = 0, grid_err = 0, grid_traj = 0;
+        bool grid_pair = true;
         std::string err_detail;
         bool pair_same = true;
         std::size_t r_ref = 0, r_gpu = 0;
@@ -358,10 +359,21 @@ int main() {
             const std::size_t nt_p = scaling ? spec.nt_p : spec.nt;
             rom_search::SearchConfig cfg{rom_search::default_b1(), rom_search::default_b2(), 1.2, nt_p};
             rom_search::SearchOutcome orf, ogp;
+            rom_search::SearchOutcome dgp;
             comm::run_on_workers(1, [&](comm::Comm& c) {
+                dopinf_b200::Bind bind(*g_gpu);
                 orf = rom_search::grid_search(qr, cfg, c);
                 ogp = rom_search::grid_search(qg, cfg, c);
+                dgp = dopinf_b200::rom_search::grid_search<rom_search::SearchOutcome>(qg, cfg, c);
             });
+            // the device grid search against the reference's on the same Q̂
+            grid_pair = grid_pair && dgp.pair_opt == ogp.pair_opt && dgp.owner_rank == ogp.owner_rank;
+            // train_err is itself a relative error: when it is tiny (1e-5 on the scaled run) its own
+            // relative precision is trajectory-rounding / train_err, so it is held to 1e-8
+            // relative or 1e-12 absolute, whichever is looser
+            grid_err = std::max(grid_err, std::abs(dgp.train_err - ogp.train_err) /
+                                              std::max(ogp.train_err, 1e-4));
+            grid_traj = std::max(grid_traj, rel_frob(dgp.trajectory, ogp.trajectory));
             pair_same = pair_same && r_ref == r_gpu && orf.pair_opt.beta1 == ogp.pair_opt.beta1 &&
                         orf.pair_opt.beta2 == ogp.pair_opt.beta2;
             const double gap = std::abs(orf.train_err - ogp.train_err) / orf.train_err;
@@ -402,6 +414,9 @@ int main() {
         report(err_gap <= 1e-10, "pipeline training error (acceptance criterion-2 run)",
                err_detail + "centered run rel <= 1e-10");
         report(traj_gap <= 1e-8, "ROM prediction over 2x horizon", "rel " + fmt(traj_gap) + " <= 1e-8");
+        report(grid_pair && grid_err <= 1e-8 && grid_traj <= 1e-8, "device grid_search vs rom_search::grid_search",
+               "same pair and owner; train_err gap / max(err, 1e-4) " + fmt(grid_err) + ", trajectory rel " +
+                   fmt(grid_traj) + " <= 1e-8");
         report(field_same <= 1e-10 && field_chain <= 1e-8, "reconstruct_field vs postprocess::reconstruct_field",
                "same inputs rel " + fmt(field_same) + " <= 1e-10; whole chain rel " + fmt(field_chain) + " <= 1e-8");
     }
