@@ -944,9 +944,6 @@ GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r
     const size_t batch = std::max<size_t>(1, std::min<size_t>(std::max<size_t>(np, 1),
                                                                (size_t(8) << 30) / (per_pair * sizeof(double))));
     std::string err;
-    const size_t lwork = np ? c->solver.potrf_workspace_doubles(D, &err) : 0;
-    if (np && !err.empty()) fail(DOPINF_B200_ERR_DEVICE, err);
-    double* work = c->rom_work.get<double>(std::max<size_t>(lwork, 1), "potrf workspace");
     int* info = c->rom_info.get<int>(2 * batch, "potrf info");
     double* betas = c->rom_betas.get<double>(2 * batch, "betas");
     double* lhs = c->rom_lhs.get<double>(batch * D * D, "lhs");
@@ -979,8 +976,7 @@ GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r
         ck(rom::launch_systems(g, D, R, betas, betas + nb, static_cast<int>(nb), rhs, lhs, rhsb, c->stream),
            "systems");
         ck(cudaMemsetAsync(info, 0, 2 * nb * sizeof(int), c->stream), "memset");
-        if (c->solver.spd_solve(lhs, D, static_cast<int>(nb), rhsb, R, work, lwork, info, c->stream, &err) !=
-            cudaSuccess) {
+        if (c->solver.spd_solve(lhs, D, static_cast<int>(nb), rhsb, R, info, c->stream, &err) != cudaSuccess) {
             fail(DOPINF_B200_ERR_DEVICE, err);
         }
         ck(cudaEventRecord(ev[0], c->stream), "event");

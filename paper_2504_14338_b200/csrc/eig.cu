@@ -15,6 +15,7 @@
 #include <cusolverDn.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -149,6 +150,7 @@ const char* unavailable_reason() {
 
 Solver::~Solver() {
     if (handle_) api().destroy(static_cast<cusolverDnHandle_t>(handle_));
+    if (start_) cudaEventDestroy(start_);
 }
 
 cudaError_t Solver::run(const double* d, int n, double* a_scratch, double* w, double* work_dev, size_t work_doubles,
@@ -222,28 +224,58 @@ bool Solver::ensure_handle(std::string* err) {
     return true;
 }
 
-size_t Solver::potrf_workspace_doubles(int n, std::string* err) {
-    if (!ensure_handle(err)) return 0;
-    int lwork = 0;
-    if (api().potrf_buffer_size(static_cast<cusolverDnHandle_t>(handle_), CUBLAS_FILL_MODE_LOWER, n, nullptr, n,
-                                &lwork) != CUSOLVER_STATUS_SUCCESS) {
-        *err = "cusolverDnDpotrf_bufferSize failed";
-        return 0;
-    }
-    return static_cast<size_t>(lwork);
+// Cholesky lanes: the pairs' factorisations are small (n ≈ 10²–10³), so a
+// few run concurrently, each lane with its own handle, stream and workspace.
+Solver::CholLane::~CholLane() {
+    if (handle) api().destroy(static_cast<cusolverDnHandle_t>(handle));
+    if (stream) cudaStreamDestroy(stream);
+    if (done) cudaEventDestroy(done);
+    if (work) cudaFree(work);
 }
 
-cudaError_t Solver::spd_solve(double* a, int n, int batch, double* b, int nrhs, double* work_dev,
-                              size_t work_doubles, int* info_dev, cudaStream_t stream, std::string* err) {
+cudaError_t Solver::spd_solve(double* a, int n, int batch, double* b, int nrhs, int* info_dev, cudaStream_t stream,
+                              std::string* err) {
     if (!ensure_handle(err)) return cudaErrorNotSupported;
     const Api& x = api();
-    auto h = static_cast<cusolverDnHandle_t>(handle_);
-    x.set_stream(h, stream);
+    const int lanes = std::min(kCholLanes, std::max(batch, 1));
+    cudaError_t e = cudaSuccess;
+    if (!start_ && (e = cudaEventCreateWithFlags(&start_, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(start_, stream)) != cudaSuccess) return e;
+    for (int l = 0; l < lanes; ++l) {
+        CholLane& ln = lanes_[l];
+        if (!ln.handle) {
+            cusolverDnHandle_t h;
+            if (x.create(&h) != CUSOLVER_STATUS_SUCCESS) {
+                *err = "cusolverDnCreate failed";
+                return cudaErrorUnknown;
+            }
+            ln.handle = h;
+            if ((e = cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+            x.set_stream(static_cast<cusolverDnHandle_t>(ln.handle), ln.stream);
+        }
+        int lwork = 0;
+        if (x.potrf_buffer_size(static_cast<cusolverDnHandle_t>(ln.handle), CUBLAS_FILL_MODE_LOWER, n, a, n,
+                                &lwork) != CUSOLVER_STATUS_SUCCESS) {
+            *err = "cusolverDnDpotrf_bufferSize failed";
+            return cudaErrorUnknown;
+        }
+        if (static_cast<size_t>(lwork) > ln.work_doubles) {
+            if (ln.work) cudaFree(ln.work);
+            ln.work = nullptr;
+            ln.work_doubles = 0;
+            if ((e = cudaMalloc(&ln.work, static_cast<size_t>(lwork) * sizeof(double))) != cudaSuccess) return e;
+            ln.work_doubles = static_cast<size_t>(lwork);
+        }
+        if ((e = cudaStreamWaitEvent(ln.stream, start_, 0)) != cudaSuccess) return e;
+    }
     for (int i = 0; i < batch; ++i) {
+        CholLane& ln = lanes_[i % lanes];
+        auto h = static_cast<cusolverDnHandle_t>(ln.handle);
         double* ai = a + static_cast<size_t>(i) * n * n;
         double* bi = b + static_cast<size_t>(i) * n * nrhs;
-        if (x.potrf(h, CUBLAS_FILL_MODE_LOWER, n, ai, n, work_dev, static_cast<int>(work_doubles), info_dev + i) !=
-            CUSOLVER_STATUS_SUCCESS) {
+        if (x.potrf(h, CUBLAS_FILL_MODE_LOWER, n, ai, n, static_cast<double*>(ln.work),
+                    static_cast<int>(ln.work_doubles), info_dev + i) != CUSOLVER_STATUS_SUCCESS) {
             *err = "cusolverDnDpotrf failed";
             return cudaErrorUnknown;
         }
@@ -252,6 +284,10 @@ cudaError_t Solver::spd_solve(double* a, int n, int batch, double* b, int nrhs, 
             *err = "cusolverDnDpotrs failed";
             return cudaErrorUnknown;
         }
+    }
+    for (int l = 0; l < lanes; ++l) {
+        if ((e = cudaEventRecord(lanes_[l].done, lanes_[l].stream)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(stream, lanes_[l].done, 0)) != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }

@@ -23,14 +23,26 @@ public:
 
     // Cholesky solves of `batch` SPD n×n systems a_i (column-major, lda n;
     // factored in place) with nrhs right-hand sides b_i (column-major, ldb n;
-    // overwritten by the solutions). info_dev[2·batch]: potrf infos, then potrs.
-    size_t potrf_workspace_doubles(int n, std::string* err);
-    cudaError_t spd_solve(double* a, int n, int batch, double* b, int nrhs, double* work_dev, size_t work_doubles,
-                          int* info_dev, cudaStream_t stream, std::string* err);
+    // overwritten by the solutions), spread over kCholLanes concurrent
+    // cuSOLVER streams and joined back into `stream`. info_dev[2·batch]:
+    // potrf infos, then potrs.
+    cudaError_t spd_solve(double* a, int n, int batch, double* b, int nrhs, int* info_dev, cudaStream_t stream,
+                          std::string* err);
 
 private:
+    static constexpr int kCholLanes = 8;
+    struct CholLane {
+        void* handle = nullptr;
+        cudaStream_t stream = nullptr;
+        cudaEvent_t done = nullptr;
+        void* work = nullptr;
+        size_t work_doubles = 0;
+        ~CholLane();
+    };
     bool ensure_handle(std::string* err);
     void* handle_ = nullptr;
+    cudaEvent_t start_ = nullptr;
+    CholLane lanes_[kCholLanes];
 };
 
 cudaError_t launch_reduced_map(const double* v, const double* lambda, int n, int r, double* tr, cudaStream_t stream);

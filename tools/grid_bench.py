@@ -38,14 +38,18 @@ def main():
     qhat = api.project_resident(ctx, None, r=r)
     cfg = api.SearchConfig(api.default_b1(), api.default_b2(), 1.2, 2 * nt)
     best = None
-    for _ in range(args.reps):
-        t0 = time.perf_counter()
-        out = api.grid_search(qhat, cfg, ctx)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    rec = {"r": r, "nt": nt, "nt_p": 2 * nt, "pairs": 64, "device_wall_s": round(best, 4),
-           "device_rom_integrate_s": round(out.rom_seconds, 4), "pair_opt": out.pair_opt,
-           "train_err": out.train_err}
+    rec = {"r": r, "nt": nt, "nt_p": 2 * nt, "pairs": 64}
+    try:
+        for _ in range(args.reps):
+            t0 = time.perf_counter()
+            out = api.grid_search(qhat, cfg, ctx)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        rec.update({"device_wall_s": round(best, 4), "device_rom_integrate_s": round(out.rom_seconds, 4),
+                    "pair_opt": out.pair_opt, "train_err": out.train_err})
+    except api.Error as e:
+        rec["device_error"] = f"{type(e).__name__}: {e}"
+
     try:
         from oracle.cpu import Reference
 
@@ -55,8 +59,8 @@ def main():
             t0 = time.perf_counter()
             try:
                 ref.grid_search(qhat, b1, np.array(cfg.b2[:1]), 1.2, 2 * nt)
-            except RuntimeError:  # a 2-pair sample may have no admissible pair; the work is done
-                pass
+            except RuntimeError as e:  # a 2-pair sample may have no admissible pair; the work is done
+                rec["reference_sample_error"] = str(e)
             per_pair = (time.perf_counter() - t0) / args.ref_pairs
             rec.update({"reference_s_per_pair_1core": round(per_pair, 3),
                         "reference_64_pairs_1core_s": round(64 * per_pair, 1),
