@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -358,18 +359,42 @@ std::vector<TileInfo> plan_tiles(int K) {
                     if (mask) entries.push_back({wm, wn, __builtin_popcount(mask), mask});
                 }
             }
-            // LPT over the 4 SM sub-partitions (warp w runs on SMSP w % 4).
+            // Balance the warp tiles over the 4 SM sub-partitions (warp w runs
+            // on SMSP w % 4, at most 4 each): exact min-max assignment by a
+            // pruned search (≤ 16 tiles of a few distinct costs), which beats
+            // LPT on diagonal tiles (6 × 16 + 4 × 12 mma: LPT max 40, optimum 36).
             std::stable_sort(entries.begin(), entries.end(),
                              [](const Entry& a, const Entry& b) { return a.cost > b.cost; });
+            const int n = static_cast<int>(entries.size());
+            std::vector<int> cur(n, 0), best_assign(n, 0);
             int load[4] = {0, 0, 0, 0}, used[4] = {0, 0, 0, 0};
-            for (const Entry& e : entries) {
-                int q = -1;
-                for (int c = 0; c < 4; ++c) {
-                    if (used[c] < 4 && (q < 0 || load[c] < load[q])) q = c;
+            int best_max = 1 << 30;
+            std::function<void(int, int)> dfs = [&](int k, int cur_max) {
+                if (cur_max >= best_max) return;
+                if (k == n) {
+                    best_max = cur_max;
+                    best_assign = cur;
+                    return;
                 }
-                const int w = q + 4 * used[q];
-                ++used[q];
-                load[q] += e.cost;
+                for (int c = 0; c < 4; ++c) {
+                    if (used[c] >= 4) continue;
+                    bool seen = false;  // SMSPs in the same state are interchangeable
+                    for (int c2 = 0; c2 < c; ++c2) seen |= used[c2] < 4 && load[c2] == load[c] && used[c2] == used[c];
+                    if (seen) continue;
+                    load[c] += entries[k].cost;
+                    ++used[c];
+                    cur[k] = c;
+                    dfs(k + 1, std::max(cur_max, load[c]));
+                    load[c] -= entries[k].cost;
+                    --used[c];
+                }
+            };
+            dfs(0, 0);
+            int slot[4] = {0, 0, 0, 0};
+            for (int k = 0; k < n; ++k) {
+                const Entry& e = entries[k];
+                const int q = best_assign[k];
+                const int w = q + 4 * slot[q]++;
                 ti.warp[w] = static_cast<uint32_t>(e.wm) | (static_cast<uint32_t>(e.wn) << 2) |
                              (static_cast<uint32_t>(I == J) << 4) | (e.mask << 16);
             }
