@@ -117,6 +117,17 @@ struct DBuf {
     }
 };
 
+// rows × width doubles between pitched buffers; one linear copy when both
+// pitches equal the width (the copy engines stream it at the full link rate).
+cudaError_t copy_rows(double* dst, size_t dld, const double* src, size_t sld, size_t width, size_t rows,
+                      cudaMemcpyKind kind, cudaStream_t stream) {
+    if (dld == width && sld == width) {
+        return cudaMemcpyAsync(dst, src, rows * width * sizeof(double), kind, stream);
+    }
+    return cudaMemcpy2DAsync(dst, dld * sizeof(double), src, sld * sizeof(double), width * sizeof(double), rows,
+                             kind, stream);
+}
+
 bool is_pinned(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -664,8 +675,7 @@ void file_chunk_h2d(dopinf_b200_block* b, const StreamSource& src, const std::ve
     if (!pread_parallel(src.fd, slot, bytes, src.file->data_offset + first * b->nt * sizeof(double))) {
         format_fail("snapshot file truncated in variable '" + src.file->names[ch.var] + "': " + *src.path);
     }
-    ck(cudaMemcpy2DAsync(b->q + ch.r0 * b->ld, b->ld * sizeof(double), slot, b->nt * sizeof(double),
-                         b->nt * sizeof(double), ch.rows, cudaMemcpyHostToDevice, c->copy_stream),
+    ck(copy_rows(b->q + ch.r0 * b->ld, b->ld, slot, b->nt, b->nt, ch.rows, cudaMemcpyHostToDevice, c->copy_stream),
        "chunk H2D");
     ck(cudaEventRecord(c->chunk_events[k], c->copy_stream), "event");
 }
@@ -738,9 +748,8 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
         if (from_file && !chunks.empty()) file_chunk_h2d(b, src, chunks, 0, fring, slot_doubles);
         for (size_t k = 0; !from_file && k < chunks.size(); ++k) {
             const StreamChunk& ch = chunks[k];
-            ck(cudaMemcpy2DAsync(b->q + ch.r0 * b->ld, b->ld * sizeof(double), src.host + ch.r0 * src.host_ld,
-                                 src.host_ld * sizeof(double), b->nt * sizeof(double), ch.rows,
-                                 cudaMemcpyHostToDevice, c->copy_stream),
+            ck(copy_rows(b->q + ch.r0 * b->ld, b->ld, src.host + ch.r0 * src.host_ld, src.host_ld, b->nt, ch.rows,
+                         cudaMemcpyHostToDevice, c->copy_stream),
                "chunk H2D");
             ck(cudaEventRecord(c->chunk_events[k], c->copy_stream), "event");
         }
