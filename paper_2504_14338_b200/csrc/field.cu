@@ -186,6 +186,10 @@ __global__ void __launch_bounds__(THREADS, 2)
                 }
             }
 
+            // epilogue half by half: the first half's results are final while the
+            // second half's DMMAs still drain
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi) {
                 const int lr = wm * 32 + mi * 8 + g;
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(THREADS, 2)
                 const double s_row = sm.scale[lr], m_row = sm.mean[lr];
                 double* dst = out + static_cast<size_t>(row) * ldo;
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) {
+                for (int ni = 2 * h; ni < 2 * h + 2; ++ni) {
                     const int col = c * BN + wn * 32 + ni * 8 + 2 * t;
                     if (accumulate && col < nt_p) {  // r > max_r_pad(): earlier k-slabs' raw sums
                         acc[mi][ni][0] += dst[col];
