@@ -1,0 +1,515 @@
+// capi_io.cu — the C ABI's streamed passes (host rows, SNP1 files, device-
+// generated rows) and the SNP1 container (reference data.hpp / data.cpp):
+// header parsing with the reference's checks and messages, the pinned-ring
+// file reader, and Steps II–III over chunks whose H2D / read overlaps the
+// compute of the chunk before.
+#include "capi_internal.h"
+
+namespace dopinf_b200 {
+namespace capi {
+
+namespace {
+
+// ---- streamed Steps II-III ----------------------------------------------------------
+// dopinf_b200_snapshot_pass_host: rows arrive from host memory into the
+// resident block (H2D on the copy stream overlaps the compute stream).
+// dopinf_b200_stream_pass_synth: rows are generated on the device chunk by chunk
+// into a two-slot ring — the block is never resident (config 4: 403 GB/GPU).
+constexpr long long kStreamChunkRows = 32768;   // rows per H2D chunk (315 MB at K = 1200)
+
+constexpr long long kStreamSplitRows = 2048;    // rows per Gram item inside a host chunk
+
+constexpr long long kSynthChunkRows = 262144;   // rows per generated chunk (3.1 GB at K = 1500)
+
+constexpr long long kSynthSplitRows = 8192;
+
+struct StreamChunk {
+    int var;
+    long long r0, rows;
+    bool first_of_var, last_of_var;
+};
+
+struct StreamSource {
+    const double* host = nullptr;  // host rows (pitch host_ld) → resident block
+    size_t host_ld = 0;
+    bool synth = false;            // device-generated rows → ring buffer, block not resident
+    uint64_t seed = 0;
+    int n_modes = 0;
+    double dt = 0.0, noise = 0.0;
+    const double* amps = nullptr;  // host [n_vars] or null
+    int fd = -1;                   // SNP1 file rows → pinned ring → resident block
+    const Snp1* file = nullptr;
+    const std::string* path = nullptr;
+};
+
+// File source: read chunk k of the block's rows into pinned ring slot k % 2
+// and enqueue its H2D on the copy stream; chunk_events[k] marks the copy done
+// (the compute stream waits on it; the read of chunk k + 2 into the same slot
+// waits on it from the host).
+void file_chunk_h2d(dopinf_b200_block* b, const StreamSource& src, const std::vector<StreamChunk>& chunks,
+                    size_t k, double* ring, size_t slot_doubles) {
+    auto* c = b->ctx;
+    const StreamChunk& ch = chunks[k];
+    if (k >= 2) ck(cudaEventSynchronize(c->chunk_events[k - 2]), "ring slot");
+    double* slot = ring + (k % 2) * slot_doubles;
+    const uint64_t local0 = static_cast<uint64_t>(ch.r0) - static_cast<uint64_t>(ch.var) * b->nx_i;
+    const uint64_t first = static_cast<uint64_t>(ch.var) * src.file->nx + b->row_begin + local0;
+    const size_t bytes = static_cast<size_t>(ch.rows) * b->nt * sizeof(double);
+    if (!pread_parallel(src.fd, slot, bytes, src.file->data_offset + first * b->nt * sizeof(double))) {
+        format_fail("snapshot file truncated in variable '" + src.file->names[ch.var] + "': " + *src.path);
+    }
+    ck(copy_rows(b->q + ch.r0 * b->ld, b->ld, slot, b->nt, b->nt, ch.rows, cudaMemcpyHostToDevice, c->copy_stream),
+       "chunk H2D");
+    ck(cudaEventRecord(c->chunk_events[k], c->copy_stream), "event");
+}
+
+std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b, long long chunk_rows) {
+    std::vector<StreamChunk> out;
+    for (size_t v = 0; v < b->n_vars; ++v) {
+        const long long v0 = static_cast<long long>(v * b->nx_i), v1 = v0 + static_cast<long long>(b->nx_i);
+        for (long long r0 = v0; r0 < v1; r0 += chunk_rows) {
+            const long long rows = std::min(chunk_rows, v1 - r0);
+            out.push_back({static_cast<int>(v), r0, rows, r0 == v0, r0 + rows == v1});
+        }
+    }
+    return out;
+}
+
+// On the compute stream each landed chunk gets its row means / max-abs (stats
+// pass), is centered in place, and its Gram items accumulate (chunk order)
+// into the split slots of its variable. When a variable's last chunk is done
+// its slots are reduced into G_v, its MAX goes over the ranks and (resident
+// block) its rows are scaled. D = Σ_v G_v / s_v².
+void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling, double* means_host,
+                    double* scales_host) {
+    auto* c = b->ctx;
+    const int K = static_cast<int>(b->nt);
+    const size_t count = gram::packed_count(K);
+    const long long chunk_rows = src.synth ? kSynthChunkRows : kStreamChunkRows;
+    const long long split_rows = src.synth ? kSynthSplitRows : kStreamSplitRows;
+    b->pending_center = false;
+    b->stats_valid = false;
+    c->have_gram = false;
+    c->K = K;
+    const std::vector<StreamChunk> chunks = stream_chunks(b, chunk_rows);
+    while (c->chunk_events.size() < chunks.size() + 1) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        c->chunk_events.push_back(e);
+    }
+    ensure_tiles(c, K);
+    int* counters = ensure_counters(c);
+    const auto* tiles = c->tiles.get<gram::TileInfo>(gram::plan_tiles(K).size(), "tiles");
+    const long long first_rows = std::min<long long>(chunk_rows, static_cast<long long>(b->nx_i));
+    const gram::Plan full =
+        gram::make_stream_plan(std::max<long long>(first_rows, 1), K, c->num_sms, split_rows);
+    double* work = c->work.get<double>(full.workspace_doubles, "workspace");
+    double* gv = c->gv.get<double>(count * b->n_vars, "per-variable Grams");
+    double* vm = b->varmax.get<double>(b->n_vars, "varmax");
+    double* ds = c->scales.get<double>(b->n_vars, "scales");
+    double* mn = b->means.get<double>(std::max<size_t>(b->rows, 1), "means");
+    double* packed = c->packed.get<double>(count, "packed");
+    double* ring = src.synth ? c->ring.get<double>(2 * static_cast<size_t>(first_rows) * b->ld, "chunk ring")
+                             : nullptr;
+    const bool from_file = src.fd >= 0;
+    const size_t slot_doubles = static_cast<size_t>(first_rows) * b->nt;
+    double* fring = from_file && !chunks.empty()
+                        ? static_cast<double*>(c->file_ring.get(2 * slot_doubles * sizeof(double)))
+                        : nullptr;
+    std::vector<double> amps_v;  // per-variable amplitude slice for the generator
+    if (src.synth && src.amps) amps_v.assign(src.amps, src.amps + b->n_vars);
+    c->stream_gram_ms_events.clear();
+
+    c->record(DOPINF_B200_STAGE_STREAM, 0);
+    ck(cudaMemsetAsync(vm, 0, b->n_vars * sizeof(double), c->stream), "memset");
+    ck(cudaMemsetAsync(gv, 0, count * b->n_vars * sizeof(double), c->stream), "memset");
+    if (!src.synth) {
+        // The copy stream must not overwrite the block before earlier work on it is done.
+        cudaEvent_t ready = c->chunk_events[chunks.size()];
+        ck(cudaEventRecord(ready, c->stream), "event");
+        ck(cudaStreamWaitEvent(c->copy_stream, ready, 0), "event wait");
+        if (from_file && !chunks.empty()) file_chunk_h2d(b, src, chunks, 0, fring, slot_doubles);
+        for (size_t k = 0; !from_file && k < chunks.size(); ++k) {
+            const StreamChunk& ch = chunks[k];
+            ck(copy_rows(b->q + ch.r0 * b->ld, b->ld, src.host + ch.r0 * src.host_ld, src.host_ld, b->nt, ch.rows,
+                         cudaMemcpyHostToDevice, c->copy_stream),
+               "chunk H2D");
+            ck(cudaEventRecord(c->chunk_events[k], c->copy_stream), "event");
+        }
+    }
+    gram::Plan first_plan = full;
+    for (size_t k = 0; k < chunks.size(); ++k) {
+        const StreamChunk& ch = chunks[k];
+        double* qk;
+        if (src.synth) {
+            qk = ring + (k % 2) * static_cast<size_t>(first_rows) * b->ld;
+            const long long local0 = ch.r0 - static_cast<long long>(ch.var) * static_cast<long long>(b->nx_i);
+            ck(synth::oscillator(qk, b->ld, ch.rows, K, ch.rows, static_cast<long long>(b->row_begin) + local0, 1,
+                                 src.seed, src.n_modes, src.dt, src.noise, src.amps ? &amps_v[ch.var] : nullptr,
+                                 c->num_sms, c->stream, ch.var),
+               "synth chunk");
+        } else {
+            ck(cudaStreamWaitEvent(c->stream, c->chunk_events[k], 0), "event wait");
+            qk = b->q + ch.r0 * b->ld;
+        }
+        // chunk = one variable's rows: present it to the kernels as a 1-variable block
+        ck(transform::launch_stats(qk, b->ld, ch.rows, K, ch.rows, 1, true, mn + ch.r0, vm + ch.var, c->num_sms,
+                                   c->stream),
+           "stats");
+        ck(transform::launch_apply(qk, b->ld, ch.rows, K, ch.rows, mn + ch.r0, nullptr, c->num_sms, c->stream),
+           "center");
+        CUtensorMap map;
+        ck(gram::make_tensor_map(&map, qk, ch.rows, K, b->ld), "tensor map");
+        const gram::Plan plan = gram::make_stream_plan(ch.rows, K, c->num_sms, split_rows);
+        if (ch.first_of_var) first_plan = plan;
+        c->gram_event_pair();
+        ck(gram::launch_gram(plan, map, tiles, work, counters, c->stream, !ch.first_of_var), "gram");
+        c->gram_event_pair();
+        if (ch.last_of_var) {
+            ck(gram::launch_reduce(first_plan, tiles, work, gv + static_cast<size_t>(ch.var) * count, c->stream),
+               "gram reduce");
+            if (scaling) {
+                if (c->size > 1) {
+                    ckn(ncclAllReduce(vm + ch.var, ds + ch.var, 1, ncclFloat64, ncclMax, c->comm, c->stream),
+                        "allreduce(MAX)");
+                } else {
+                    ck(cudaMemcpyAsync(ds + ch.var, vm + ch.var, sizeof(double), cudaMemcpyDeviceToDevice,
+                                       c->stream),
+                       "copy");
+                }
+                if (!src.synth) {
+                    const long long v0 = static_cast<long long>(ch.var) * static_cast<long long>(b->nx_i);
+                    ck(transform::launch_apply(b->q + v0 * b->ld, b->ld, static_cast<long long>(b->nx_i), K,
+                                               static_cast<long long>(b->nx_i), nullptr, ds + ch.var, c->num_sms,
+                                               c->stream),
+                       "scale");
+                }
+            }
+        }
+        // the host reads chunk k + 1 while the device copies and reduces chunk k
+        if (from_file && k + 1 < chunks.size()) file_chunk_h2d(b, src, chunks, k + 1, fring, slot_doubles);
+    }
+    // the pinned ring is free for the next call once the last copy has landed
+    if (from_file && !chunks.empty()) ck(cudaEventSynchronize(c->chunk_events[chunks.size() - 1]), "ring");
+    if (b->rows == 0 && scaling) {  // an empty rank still joins the MAX collectives
+        for (size_t v = 0; v < b->n_vars; ++v) {
+            if (c->size > 1) {
+                ckn(ncclAllReduce(vm + v, ds + v, 1, ncclFloat64, ncclMax, c->comm, c->stream), "allreduce(MAX)");
+            } else {
+                ck(cudaMemcpyAsync(ds + v, vm + v, sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
+            }
+        }
+    }
+    ck(gram::launch_combine_vars(gv, static_cast<int>(b->n_vars), count, scaling ? ds : nullptr, packed,
+                                 c->stream),
+       "combine");
+    c->record(DOPINF_B200_STAGE_STREAM, 1);
+    c->have_gram = true;
+    if (means_host && b->rows > 0) c->d2h(means_host, mn, b->rows * sizeof(double), "means D2H");
+    if (scaling) {
+        std::vector<double> s(b->n_vars);
+        c->d2h(s.data(), ds, b->n_vars * sizeof(double), "scales D2H");
+        if (scales_host) std::memcpy(scales_host, s.data(), s.size() * sizeof(double));
+        for (size_t j = 0; j < b->n_vars; ++j) {
+            if (s[j] == 0.0) {
+                fail(DOPINF_B200_ERR_DEGENERATE_VARIABLE,
+                     "variable " + std::to_string(j) + " is constant in time; max-abs scaling is undefined");
+            }
+        }
+    }
+}
+
+// data::read_block (data.cpp:164-202) into the device block: the file rows go
+// through the pinned ring, each H2D overlapping the next chunk's read.
+void do_block_read(dopinf_b200_block* b, const StreamSource& src) {
+    auto* c = b->ctx;
+    b->pending_center = false;
+    b->stats_valid = false;
+    const std::vector<StreamChunk> chunks = stream_chunks(b, kStreamChunkRows);
+    if (chunks.empty()) return;
+    while (c->chunk_events.size() < chunks.size() + 1) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        c->chunk_events.push_back(e);
+    }
+    const size_t slot_doubles = static_cast<size_t>(std::min<long long>(kStreamChunkRows, b->nx_i)) * b->nt;
+    auto* fring = static_cast<double*>(c->file_ring.get(2 * slot_doubles * sizeof(double)));
+    c->record(DOPINF_B200_STAGE_UPLOAD, 0);
+    cudaEvent_t ready = c->chunk_events[chunks.size()];
+    ck(cudaEventRecord(ready, c->stream), "event");
+    ck(cudaStreamWaitEvent(c->copy_stream, ready, 0), "event wait");
+    for (size_t k = 0; k < chunks.size(); ++k) file_chunk_h2d(b, src, chunks, k, fring, slot_doubles);
+    ck(cudaStreamWaitEvent(c->stream, c->chunk_events[chunks.size() - 1], 0), "event wait");
+    c->record(DOPINF_B200_STAGE_UPLOAD, 1);
+    ck(cudaEventSynchronize(c->chunk_events[chunks.size() - 1]), "ring");
+}
+
+// Open + validate the file and create the device block of rows
+// [row_begin, row_end) of every variable (pipeline.cpp:254-258).
+dopinf_b200_block* open_file_block(dopinf_b200_ctx* c, const char* path, size_t row_begin, size_t row_end,
+                                   Fd& f, Snp1& h) {
+    require(path != nullptr, "null path");
+    open_snp1(f, path);
+    h = read_snp1_header(f.fd, path);
+    if (row_begin > row_end || row_end > h.nx) {
+        fail(DOPINF_B200_ERR_PARTITION, "read_block: rows [" + std::to_string(row_begin) + ", " +
+                                            std::to_string(row_end) + ") outside the file's " +
+                                            std::to_string(h.nx) + " rows");
+    }
+    require(h.nt <= (1u << 20), "snapshot file: nt too large");
+    dopinf_b200_block* b = nullptr;
+    const int rc = dopinf_b200_block_create(c, h.n_vars, row_end - row_begin, row_begin, h.nt, &b);
+    if (rc != DOPINF_B200_OK) fail(rc, c->err);
+    return b;
+}
+
+}  // namespace
+
+// Exactly `bytes` at `off`, or false (EOF / error).
+bool pread_all(int fd, void* dst, size_t bytes, uint64_t off) {
+    auto* p = static_cast<char*>(dst);
+    while (bytes > 0) {
+        const ssize_t n = pread(fd, p, bytes, static_cast<off_t>(off));
+        if (n < 0 && errno == EINTR) continue;
+        if (n <= 0) return false;
+        p += n;
+        bytes -= static_cast<size_t>(n);
+        off += static_cast<uint64_t>(n);
+    }
+    return true;
+}
+
+void open_snp1(Fd& f, const std::string& path) {
+    f.fd = open(path.c_str(), O_RDONLY | O_CLOEXEC);
+    if (f.fd < 0) format_fail("cannot open snapshot file: " + path);  // data.cpp:61-65
+}
+
+// data.cpp:35-48 (same checks, same order, same messages).
+void validate_snp1(const Snp1& h) {
+    if (h.n_vars < 1) format_fail("snapshot header: n_vars must be >= 1");
+    if (h.nx < 1) format_fail("snapshot header: nx must be >= 1");
+    if (h.nt < 2) format_fail("snapshot header: nt must be >= 2");
+    if (h.names.size() != h.n_vars) format_fail("snapshot header: name count does not match n_vars");
+    std::set<std::string> seen;
+    for (const auto& name : h.names) {
+        if (name.empty()) format_fail("snapshot header: empty variable name");
+        if (!seen.insert(name).second) format_fail("snapshot header: duplicate variable name '" + name + "'");
+    }
+}
+
+// data.cpp:69-82: a payload shorter than the header promises names the
+// variable the missing bytes belong to.
+void check_snp1_payload(const Snp1& h, const std::string& path) {
+    const unsigned __int128 per_var = static_cast<unsigned __int128>(h.nx) * h.nt * sizeof(double);
+    const unsigned __int128 expected = h.data_offset + h.n_vars * per_var;
+    if (h.file_bytes < expected) {
+        const uint64_t have = h.file_bytes - std::min(h.file_bytes, h.data_offset);
+        const uint64_t var =
+            static_cast<uint64_t>(std::min<unsigned __int128>(have / per_var, h.n_vars - 1));
+        format_fail("snapshot file truncated in variable '" + h.names[var] + "': " + path);
+    }
+}
+
+// data::read_header (data.cpp:133-162).
+Snp1 read_snp1_header(int fd, const std::string& path) {
+    struct stat st;
+    if (fstat(fd, &st) != 0) format_fail("cannot open snapshot file: " + path);
+    Snp1 h;
+    h.file_bytes = static_cast<uint64_t>(st.st_size);
+    char magic[4] = {};
+    if (!pread_all(fd, magic, 4, 0) || std::memcmp(magic, "SNP1", 4) != 0) {
+        format_fail("not a snapshot file (bad magic): " + path);
+    }
+    uint64_t off = 4;
+    auto u64 = [&](const char* field) {
+        uint64_t v = 0;
+        if (!pread_all(fd, &v, sizeof v, off)) format_fail(std::string("snapshot file truncated in ") + field);
+        off += sizeof v;
+        return v;
+    };
+    h.n_vars = u64("n_vars");
+    h.nx = u64("nx");
+    h.nt = u64("nt");
+    if (h.n_vars > (1u << 20)) format_fail("snapshot header: implausible n_vars");
+    for (uint64_t j = 0; j < h.n_vars; ++j) {
+        const std::string where = "snapshot file truncated in name of variable " + std::to_string(j);
+        uint32_t len = 0;
+        if (!pread_all(fd, &len, sizeof len, off)) format_fail(where);
+        off += sizeof len;
+        if (off + len > h.file_bytes) format_fail(where);  // before allocating `len` bytes
+        std::string name(len, '\0');
+        if (!pread_all(fd, name.data(), len, off)) format_fail(where);
+        off += len;
+        h.names.push_back(std::move(name));
+    }
+    h.data_offset = off;  // data.cpp:51-58: 4 + 3*8 + sum(4 + len)
+    validate_snp1(h);
+    check_snp1_payload(h, path);
+    return h;
+}
+
+// Reader threads per chunk: a page-cache or NVMe read of a few hundred MB is
+// bound by one core's memcpy, so the byte range is split over several.
+int file_reader_threads() {
+    static const int n = [] {
+        const unsigned hw = std::thread::hardware_concurrency();
+        return static_cast<int>(std::max(1u, std::min(16u, hw / 2)));
+    }();
+    return n;
+}
+
+// pread `bytes` at `off` into `dst` on up to file_reader_threads() threads.
+bool pread_parallel(int fd, void* dst, size_t bytes, uint64_t off) {
+    constexpr size_t kPiece = size_t(8) << 20;
+    const int n = static_cast<int>(std::min<size_t>(file_reader_threads(), (bytes + kPiece - 1) / kPiece));
+    if (n <= 1) return pread_all(fd, dst, bytes, off);
+    const size_t per = (bytes / n + 4095) / 4096 * 4096;
+    std::vector<std::thread> threads;
+    std::vector<char> ok(n, 0);
+    for (int i = 0; i < n; ++i) {
+        const size_t b0 = std::min(bytes, per * i), b1 = std::min(bytes, per * (i + 1));
+        threads.emplace_back([&, i, b0, b1] {
+            ok[i] = pread_all(fd, static_cast<char*>(dst) + b0, b1 - b0, off + b0) ? 1 : 0;
+        });
+    }
+    for (auto& t : threads) t.join();
+    return std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
+}
+
+}  // namespace capi
+}  // namespace dopinf_b200
+
+extern "C" {
+
+int dopinf_b200_snapshot_pass_host(dopinf_b200_block* b, const double* host, size_t host_ld, int scaling,
+                                   double* means, double* scales, double* d) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(host_ld >= b->nt && (b->rows == 0 || host), "snapshot_pass_host: bad host buffer");
+        StreamSource src;
+        src.host = host;
+        src.host_ld = host_ld;
+        do_stream_pass(b, src, scaling != 0, means, scales);
+        unpack(c);
+        do_global_gram(c, d);
+        c->sync("snapshot_pass_host");
+    });
+}
+
+int dopinf_b200_snp1_header(const char* path, uint64_t* dims, char* names, size_t names_cap,
+                            size_t* names_len) {
+    return guarded_free([&] {
+        require(path && dims, "snp1_header: null path or dims");
+        Fd f;
+        open_snp1(f, path);
+        const Snp1 h = read_snp1_header(f.fd, path);
+        dims[0] = h.n_vars;
+        dims[1] = h.nx;
+        dims[2] = h.nt;
+        dims[3] = h.data_offset;
+        size_t need = 0;
+        for (const auto& n : h.names) need += n.size() + 1;
+        if (names_len) *names_len = need;
+        if (names) {
+            require(names_cap >= need, "snp1_header: names buffer too small");
+            size_t at = 0;
+            for (const auto& n : h.names) {
+                std::memcpy(names + at, n.c_str(), n.size() + 1);
+                at += n.size() + 1;
+            }
+        }
+    });
+}
+
+int dopinf_b200_block_read(dopinf_b200_ctx* c, const char* path, size_t row_begin, size_t row_end,
+                           dopinf_b200_block** out) {
+    if (!out) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    dopinf_b200_block* b = nullptr;
+    const int rc = guarded(c, [&] {
+        Fd f;
+        Snp1 h;
+        b = open_file_block(c, path, row_begin, row_end, f, h);
+        StreamSource src;
+        src.fd = f.fd;
+        src.file = &h;
+        const std::string p(path);
+        src.path = &p;
+        do_block_read(b, src);
+        c->sync("block_read");
+    });
+    if (rc != DOPINF_B200_OK) {
+        dopinf_b200_block_destroy(b);
+        return rc;
+    }
+    *out = b;
+    return DOPINF_B200_OK;
+}
+
+int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* c, const char* path, size_t row_begin, size_t row_end,
+                                   int scaling, dopinf_b200_block** out, double* means, double* scales,
+                                   double* d) {
+    if (!out) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    dopinf_b200_block* b = nullptr;
+    const int rc = guarded(c, [&] {
+        Fd f;
+        Snp1 h;
+        b = open_file_block(c, path, row_begin, row_end, f, h);
+        StreamSource src;
+        src.fd = f.fd;
+        src.file = &h;
+        const std::string p(path);
+        src.path = &p;
+        do_stream_pass(b, src, scaling != 0, means, scales);
+        unpack(c);
+        do_global_gram(c, d);
+        c->sync("snapshot_pass_file");
+    });
+    if (rc != DOPINF_B200_OK) {
+        dopinf_b200_block_destroy(b);
+        return rc;
+    }
+    *out = b;
+    return DOPINF_B200_OK;
+}
+
+int dopinf_b200_stream_pass_synth(dopinf_b200_ctx* c, size_t n_vars, size_t nx_i, size_t row_begin, size_t nt,
+                                  uint64_t seed, int n_modes, double dt, double noise, const double* amps,
+                                  int scaling, double* means, double* scales, double* d) {
+    return guarded(c, [&] {
+        require(n_vars >= 1 && nt >= 1 && nt <= (1u << 20), "stream_pass_synth: bad shape");
+        require(n_modes >= 1 && n_modes <= 128, "stream_pass_synth: n_modes must lie in [1, 128]");
+        // A block that is never resident: means/varmax live on the device, values stream through a ring.
+        dopinf_b200_block view;
+        view.ctx = c;
+        view.n_vars = n_vars;
+        view.nx_i = nx_i;
+        view.row_begin = row_begin;
+        view.nt = nt;
+        view.ld = (nt + 1) / 2 * 2;
+        view.rows = n_vars * nx_i;
+        struct Release {
+            dopinf_b200_block& b;
+            ~Release() {
+                cudaStreamSynchronize(b.ctx->stream);
+                b.means.release();
+                b.varmax.release();
+            }
+        } release{view};
+        StreamSource src;
+        src.synth = true;
+        src.seed = seed;
+        src.n_modes = n_modes;
+        src.dt = dt;
+        src.noise = noise;
+        src.amps = amps;
+        do_stream_pass(&view, src, scaling != 0, means, scales);
+        unpack(c);
+        do_global_gram(c, d);
+        c->sync("stream_pass_synth");
+    });
+}
+
+}  // extern "C"
