@@ -90,17 +90,6 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                  : "d"(a), "d"(b));
 }
 
-// Same, issued only when `on` is non-zero (warp-uniform): a skipped mma costs
-// an issue slot, not a DMMA, and keeps one code path for masked warp tiles.
-__device__ __forceinline__ void dmma_8x8x4_if(double& c0, double& c1, double a, double b, uint32_t on) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@p mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n\t}\n"
-        : "+d"(c0), "+d"(c1)
-        : "d"(a), "d"(b), "r"(on));
-}
-
 __device__ __forceinline__ double2 lds128(uint32_t saddr) {
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(saddr));
