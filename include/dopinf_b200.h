@@ -29,6 +29,7 @@
  *                                                            dopinf_b200_snapshot_pass_file
  *   rom_search::grid_search (rom_search.cpp:185-262)        dopinf_b200_grid_search
  *   rom_search::integrate (rom_search.cpp:60-85)            dopinf_b200_rom_integrate
+ *   postprocess::reconstruct_probes (postprocess.cpp:36-61)  dopinf_b200_reconstruct_probes
  *   postprocess::reconstruct_field (postprocess.cpp:63-70)   dopinf_b200_reconstruct_field
  *   Step V field_rank<r>.snp1 output (pipeline.cpp:330-350) dopinf_b200_write_field
  *
@@ -309,6 +310,18 @@ int dopinf_b200_rom_integrate(dopinf_b200_ctx* ctx, const double* a, const doubl
 int dopinf_b200_reconstruct_field(dopinf_b200_block* block, const double* tr, size_t r, const double* qtilde,
                                   size_t nt_p, const double* means, const double* scales, int scaling,
                                   double* field);
+/* postprocess::reconstruct_probes (postprocess.cpp:36-61): the time series
+ * of every probe this rank owns — probe i is (var[i], index[i]), owned when
+ * index[i] lies in [row_begin, row_begin + nx_i) — in original coordinates:
+ * series[i][t] = s·dot(Q[row]·T_r, Q̃[t]) + mean with the reference's
+ * basis_rows, kernels::dot and scale_shift orders, so bit-identical to the
+ * reference for the same block, T_r, Q̃ and TransformParams. tr: host K x r,
+ * or NULL for the context's device T_r; qtilde: host nt_p x r; means [rows],
+ * scales [n_vars] (scaling); series: host n_probes x nt_p (rows of unowned
+ * probes untouched); owned: n_probes flags, may be NULL. */
+int dopinf_b200_reconstruct_probes(dopinf_b200_block* block, const double* tr, size_t r, const double* qtilde,
+                                   size_t nt_p, const size_t* var, const size_t* index, size_t n_probes,
+                                   const double* means, const double* scales, int scaling, double* series, int* owned);
 /* Device pointer and pitch (elements) of the last reconstructed field. */
 int dopinf_b200_field_device(dopinf_b200_block* block, double** field, size_t* ld);
 /* Step V field output (pipeline.cpp:330-350): reconstruct_field + write_snapshots

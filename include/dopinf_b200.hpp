@@ -11,6 +11,7 @@
 //   dopinf_b200::postprocess::basis_rows(block, tr, rows)        postprocess.hpp:25-26
 //   dopinf_b200::postprocess::basis(block, tr)  (Φ_r of reconstruct_field, postprocess.cpp:66)
 //   dopinf_b200::rom_search::grid_search<OutcomeT>(qhat, config, comm)      rom_search.hpp:87-91
+//   dopinf_b200::postprocess::reconstruct_probes<SeriesT>(block, tr, qtilde, probes, params)  postprocess.hpp:37-40
 //   dopinf_b200::postprocess::reconstruct_field(block, tr, qtilde, params)  postprocess.hpp:43-45
 //   dopinf_b200::data::partition_rows(nx, p)                     data.hpp:47
 //   dopinf_b200::data::read_header<HeaderT>(path)                data.hpp:52
@@ -436,6 +437,37 @@ MatrixT basis(const LocalBlockT& block, const MatrixT& tr) {
     MatrixT out(block.values.rows(), tr.cols());
     Context::check(dopinf_b200_basis(d.handle(), tr.data(), tr.cols(), out.data()), d.context().handle(), "basis");
     return out;
+}
+
+// postprocess::reconstruct_probes (postprocess.cpp:36-61), bit-identical: one
+// SeriesT {probe, values} per probe whose index lies in the block's row range.
+template <class SeriesT, class LocalBlockT, class MatrixT, class ProbeSetT, class ParamsT>
+std::vector<SeriesT> reconstruct_probes(const LocalBlockT& block, const MatrixT& tr, const MatrixT& qtilde,
+                                        const ProbeSetT& probes, const ParamsT& params) {
+    const std::size_t n_vars = detail::n_vars_of(block);
+    DeviceBlock d = detail::uploaded(block, n_vars);
+    std::vector<std::size_t> var, index;
+    for (const auto& p : probes) {
+        var.push_back(p.var);
+        index.push_back(p.index);
+    }
+    std::vector<double> out(probes.size() * qtilde.rows());
+    std::vector<int> owned(probes.size());
+    Context::check_exact(dopinf_b200_reconstruct_probes(d.handle(), tr.data(), tr.cols(), qtilde.data(), qtilde.rows(),
+                                                        var.data(), index.data(), probes.size(),
+                                                        params.local_means.data(),
+                                                        params.scaling_enabled ? params.scales.data() : nullptr,
+                                                        params.scaling_enabled ? 1 : 0, out.data(), owned.data()),
+                         d.context().handle());
+    std::vector<SeriesT> series;
+    for (std::size_t i = 0; i < probes.size(); ++i) {
+        if (!owned[i]) continue;
+        SeriesT s;
+        s.probe = probes[i];
+        s.values.assign(out.begin() + i * qtilde.rows(), out.begin() + (i + 1) * qtilde.rows());
+        series.push_back(std::move(s));
+    }
+    return series;
 }
 
 // postprocess::reconstruct_field (postprocess.cpp:63-70): (Q·T_r)·Q̃ᵀ mapped back

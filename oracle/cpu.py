@@ -92,6 +92,11 @@ class Oracle:
         return _Rng(self.lib, seed)
 
     # -- kernels
+    def k_dot(self, a, b):
+        """kernels_avx2.cpp:32-46 dot_avx2."""
+        a, b = _f(a), _f(b)
+        return float(self.lib.oracle_k_dot(_d(a), _d(b), a.size))
+
     def k_sum(self, x):
         x = _f(x)
         return self.lib.oracle_k_sum(_d(x), x.size)
@@ -252,6 +257,9 @@ class Reference:
             lib.ref_write_snapshots.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_char_p, _dp]
             lib.ref_read_header.argtypes = [C.c_char_p, _sp, C.c_char_p, C.c_size_t]
             lib.ref_read_block.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
+            lib.ref_reconstruct_probes.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, _dp,
+                                                   C.c_size_t, _dp, C.c_size_t, _dp, _dp, C.c_int, _sp, _sp,
+                                                   C.c_size_t, _dp, C.POINTER(C.c_int)]
             lib.ref_integrate.argtypes = [_dp, _dp, _dp, C.c_size_t, _dp, C.c_size_t, _dp, C.POINTER(C.c_int)]
             lib.ref_solve_opinf.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_double, C.c_double, _dp, _dp, _dp]
             lib.ref_reconstruct_field.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp,
@@ -344,6 +352,22 @@ class Reference:
         self._ok(self.lib.ref_grid_search(_d(qhat), r, nt, _d(b1), b1.size, _d(b2), b2.size, max_growth, nt_p,
                                           _d(traj), _d(pe)))
         return traj, (pe[0], pe[1]), pe[2]
+
+    def reconstruct_probes(self, q, n_vars, begin, tr, qtilde, means, scales, scaling, var, index):
+        """postprocess::reconstruct_probes -> (series n_probes x nt_p, owned flags)."""
+        q, tr, qt = _f(q), _f(tr), _f(qtilde)
+        rows, nt = q.shape
+        nt_p, r = qt.shape
+        var = np.ascontiguousarray(var, dtype=np.uintp)
+        index = np.ascontiguousarray(index, dtype=np.uintp)
+        out = np.full((var.size, nt_p), np.nan)
+        owned = (C.c_int * max(var.size, 1))()
+        sc = _f(scales) if scaling else np.zeros(max(n_vars, 1))
+        self._ok(self.lib.ref_reconstruct_probes(_d(q), n_vars, rows // n_vars, begin, nt, _d(tr), r, _d(qt), nt_p,
+                                                 _d(_f(means)), _d(sc), 1 if scaling else 0,
+                                                 var.ctypes.data_as(_sp), index.ctypes.data_as(_sp), var.size,
+                                                 _d(out), owned))
+        return out, np.array(list(owned)[: var.size], dtype=bool)
 
     def integrate(self, a, f, c, q0, n_steps):
         """rom_search::integrate (rom_search.cpp:60-85) -> (trajectory n_steps x r, finite)."""

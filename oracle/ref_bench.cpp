@@ -399,4 +399,39 @@ int ref_solve_opinf(const double* qhat, std::size_t r, std::size_t nt, double be
     }
 }
 
+// postprocess::reconstruct_probes (postprocess.cpp:36-61) on one rank's block
+// (rows [begin, begin + nx_i) of every variable): owned probes' series into
+// out (n_probes x nt_p, owned rows only) and owned[i].
+int ref_reconstruct_probes(const double* q, std::size_t n_vars, std::size_t nx_i, std::size_t begin, std::size_t nt,
+                           const double* tr, std::size_t r, const double* qtilde, std::size_t nt_p,
+                           const double* means, const double* scales, int scaling, const std::size_t* var,
+                           const std::size_t* index, std::size_t n_probes, double* out, int* owned) {
+    try {
+        data::LocalBlock block;
+        block.row_range = {begin, begin + nx_i};
+        block.values = to_matrix(q, n_vars * nx_i, nt);
+        transform::TransformParams params;
+        params.local_means.assign(means, means + n_vars * nx_i);
+        if (scaling) params.scales.assign(scales, scales + n_vars);
+        params.scaling_enabled = scaling != 0;
+        postprocess::ProbeSet probes;
+        for (std::size_t i = 0; i < n_probes; ++i) probes.push_back({var[i], index[i]});
+        const auto series = postprocess::reconstruct_probes(block, to_matrix(tr, nt, r), to_matrix(qtilde, nt_p, r),
+                                                            probes, params);
+        for (std::size_t i = 0; i < n_probes; ++i) owned[i] = 0;
+        for (const auto& sr : series) {
+            for (std::size_t i = 0; i < n_probes; ++i) {
+                if (probes[i] == sr.probe && !owned[i]) {
+                    owned[i] = 1;
+                    std::memcpy(out + i * nt_p, sr.values.data(), nt_p * sizeof(double));
+                    break;
+                }
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 }  // extern "C"

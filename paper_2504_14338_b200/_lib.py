@@ -86,6 +86,8 @@ SIGNATURES = {
     "dopinf_b200_rom_integrate": (C.c_int, [_vp, _dp, _dp, _dp, C.c_size_t, _dp, C.c_size_t, _dp,
                                             C.POINTER(C.c_int)]),
     "dopinf_b200_reconstruct_field": (C.c_int, [_vp, _dp, C.c_size_t, _dp, C.c_size_t, _dp, _dp, C.c_int, _dp]),
+    "dopinf_b200_reconstruct_probes": (C.c_int, [_vp, _dp, C.c_size_t, _dp, C.c_size_t, _sp, _sp, C.c_size_t, _dp,
+                                                 _dp, C.c_int, _dp, C.POINTER(C.c_int)]),
     "dopinf_b200_field_device": (C.c_int, [_vp, C.POINTER(_dp), C.POINTER(C.c_size_t)]),
     "dopinf_b200_write_field": (C.c_int, [_vp, _dp, C.c_size_t, _dp, C.c_size_t, _dp, _dp, C.c_int, C.c_char_p,
                                           C.c_char_p]),

@@ -670,6 +670,37 @@ def reconstruct_field(block: LocalBlock, tr, qtilde, params: TransformParams, do
     return out
 
 
+@dataclass
+class Probe:
+    """postprocess::Probe (postprocess.hpp:13-18): variable and global spatial index."""
+    var: int = 0
+    index: int = 0
+
+
+@dataclass
+class ProbeSeries:
+    probe: Probe
+    values: np.ndarray  # nt_p entries, original coordinates
+
+
+def reconstruct_probes(block: LocalBlock, tr, qtilde, probes, params: TransformParams,
+                       r: int | None = None) -> list:
+    """postprocess::reconstruct_probes (postprocess.cpp:36-61) on the device,
+    bit-identical to the reference: one ProbeSeries per probe this rank owns."""
+    tr, r, qt, means, scales = _field_args(block, tr, qtilde, params, r, "reconstruct_probes")
+    nt_p = qt.shape[0]
+    var = np.ascontiguousarray([p.var for p in probes], dtype=np.uintp)
+    index = np.ascontiguousarray([p.index for p in probes], dtype=np.uintp)
+    out = np.empty((len(probes), nt_p), dtype=np.float64)
+    owned = (C.c_int * max(len(probes), 1))()
+    rc = _lib.load().dopinf_b200_reconstruct_probes(block._h, _lib.dptr(tr), r, _lib.dptr(qt), nt_p, _lib.sptr(var),
+                                                    _lib.sptr(index), len(probes), _lib.dptr(means),
+                                                    _lib.dptr(scales), 1 if params.scaling_enabled else 0,
+                                                    _lib.dptr(out), owned)
+    _check(rc, block.ctx)
+    return [ProbeSeries(p, out[i].copy()) for i, p in enumerate(probes) if owned[i]]
+
+
 def field_device(block: LocalBlock):
     """(device pointer, pitch in elements) of the last reconstructed field."""
     p = _lib._dp()

@@ -494,6 +494,65 @@ int dopinf_b200_reconstruct_field(dopinf_b200_block* b, const double* tr, size_t
     });
 }
 
+int dopinf_b200_reconstruct_probes(dopinf_b200_block* b, const double* tr, size_t r, const double* qtilde,
+                                   size_t nt_p, const size_t* var, const size_t* index, size_t n_probes,
+                                   const double* means, const double* scales, int scaling, double* series,
+                                   int* owned) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(n_probes == 0 || (var && index), "reconstruct_probes: null probe arrays");
+        require(qtilde != nullptr && r >= 1, "reconstruct_probes: null trajectory");
+        require(b->rows == 0 || means != nullptr, "reconstruct_probes: null means");
+        require(!scaling || scales != nullptr, "reconstruct_probes: null scales");
+        // the owned probes' local rows, in probe order (postprocess.cpp:42-48)
+        std::vector<long long> rows;
+        std::vector<size_t> which;
+        for (size_t i = 0; i < n_probes; ++i) {
+            const bool mine = index[i] >= b->row_begin && index[i] < b->row_begin + b->nx_i;
+            if (owned) owned[i] = mine ? 1 : 0;
+            if (!mine) continue;
+            const size_t row = var[i] * b->nx_i + (index[i] - b->row_begin);
+            if (row >= b->rows) {  // basis_rows' check (postprocess.cpp:20-23)
+                fail(DOPINF_B200_ERR_INVALID_ARGUMENT,
+                     "basis_rows: row " + std::to_string(row) + " outside the local block");
+            }
+            rows.push_back(static_cast<long long>(row));
+            which.push_back(i);
+        }
+        if (rows.empty()) return;
+        materialize(b);
+        const int nsel = static_cast<int>(rows.size());
+        const double* dtr = tr_operand(c, tr, b->nt, r);
+        long long* dsel = c->sel.get<long long>(rows.size(), "sel");
+        double* dbasis = c->rows_out.get<double>(rows.size() * r, "probe basis");
+        double* dqt = c->field_qt.get<double>(nt_p * r, "qtilde");
+        double* dm = c->field_means.get<double>(b->rows, "means");
+        double* ds = scaling ? c->field_scales.get<double>(b->n_vars, "scales") : nullptr;
+        double* dout = c->field_ring.get<double>(rows.size() * nt_p, "probe series");
+        ck(cudaMemcpyAsync(dsel, rows.data(), rows.size() * sizeof(long long), cudaMemcpyHostToDevice, c->stream),
+           "rows H2D");
+        ck(cudaMemcpyAsync(dqt, qtilde, nt_p * r * sizeof(double), cudaMemcpyHostToDevice, c->stream), "qtilde H2D");
+        ck(cudaMemcpyAsync(dm, means, b->rows * sizeof(double), cudaMemcpyHostToDevice, c->stream), "means H2D");
+        if (ds) {
+            ck(cudaMemcpyAsync(ds, scales, b->n_vars * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+               "scales H2D");
+        }
+        ck(project::launch_basis_rows(b->q, b->ld, static_cast<int>(b->nt), dtr, static_cast<int>(r), dsel, nsel,
+                                      dbasis, c->stream),
+           "basis_rows");
+        ck(project::launch_probe_series(dbasis, static_cast<int>(r), dqt, static_cast<int>(nt_p), dsel, dm, ds,
+                                        static_cast<long long>(b->nx_i), nsel, dout, c->stream),
+           "probe series");
+        std::vector<double> h(rows.size() * nt_p);
+        ck(cudaMemcpyAsync(h.data(), dout, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        c->sync("reconstruct_probes");
+        for (size_t k = 0; k < which.size(); ++k) {
+            std::memcpy(series + which[k] * nt_p, &h[k * nt_p], nt_p * sizeof(double));
+        }
+    });
+}
+
 int dopinf_b200_field_device(dopinf_b200_block* b, double** field, size_t* ld) {
     if (!b || !field || !ld) return DOPINF_B200_ERR_INVALID_ARGUMENT;
     return guarded(b->ctx, [&] {

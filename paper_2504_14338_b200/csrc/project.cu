@@ -81,6 +81,44 @@ __global__ void basis_rows_kernel(const double* __restrict__ q, size_t ld, int K
     out[e] = acc;
 }
 
+// postprocess::reconstruct_probes (postprocess.cpp:36-61): series[t] =
+// kernels::dot(basis_row, Q̃.row(t), r) in the AVX2 order (kernels_avx2.cpp:
+// 32-46: two 4-lane FMA accumulators over blocks of 8, the trailing block of
+// 4 into the first, (v0+v2)+(v1+v3), then the tail with a rounded product),
+// then inverse_transform_row's scale_shift: fma(s, x, mean). One thread per
+// (probe, t) → bit-identical to the reference.
+__global__ void probe_series_kernel(const double* __restrict__ basis, int r, const double* __restrict__ qt,
+                                    int nt_p, const long long* __restrict__ rows, const double* __restrict__ means,
+                                    const double* __restrict__ scales, long long nx_i, int nsel,
+                                    double* __restrict__ out) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= static_cast<long long>(nsel) * nt_p) return;
+    const int k = static_cast<int>(e / nt_p), t = static_cast<int>(e % nt_p);
+    const double* a = basis + static_cast<size_t>(k) * r;
+    const double* b = qt + static_cast<size_t>(t) * r;
+    double c0[4] = {0.0, 0.0, 0.0, 0.0}, c1[4] = {0.0, 0.0, 0.0, 0.0};
+    int i = 0;
+    for (; i + 8 <= r; i += 8) {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            c0[l] = __fma_rn(a[i + l], b[i + l], c0[l]);
+            c1[l] = __fma_rn(a[i + 4 + l], b[i + 4 + l], c1[l]);
+        }
+    }
+    for (; i + 4 <= r; i += 4) {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) c0[l] = __fma_rn(a[i + l], b[i + l], c0[l]);
+    }
+    double v[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) v[l] = __dadd_rn(c0[l], c1[l]);
+    double acc = __dadd_rn(__dadd_rn(v[0], v[2]), __dadd_rn(v[1], v[3]));
+    for (; i < r; ++i) acc = __dadd_rn(acc, __dmul_rn(a[i], b[i]));
+    const long long row = rows[k];
+    const double s = scales ? scales[row / nx_i] : 1.0;
+    out[e] = __fma_rn(s, acc, means[row]);
+}
+
 // ---- Φ_r = Q · T_r on DMMA ---------------------------------------------------
 // Warp grid WM × WN (8 consumer warps); warp tile 32 rows × 8·NT columns.
 // CTA tile BM = 32·WM rows × BN = 8·NT·WN columns.
@@ -268,6 +306,17 @@ cudaError_t launch_basis_rows(const double* q, size_t ld, int K, const double* t
     if (total == 0) return cudaSuccess;
     basis_rows_kernel<<<static_cast<int>((total + 127) / 128), 128, 0, stream>>>(q, ld, K, tr, r,
                                                                                 rows, nsel, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_probe_series(const double* basis, int r, const double* qt, int nt_p, const long long* rows,
+                                const double* means, const double* scales, long long nx_i, int nsel, double* out,
+                                cudaStream_t stream) {
+    const long long total = static_cast<long long>(nsel) * nt_p;
+    if (total == 0) return cudaSuccess;
+    probe_series_kernel<<<static_cast<int>((total + 127) / 128), 128, 0, stream>>>(basis, r, qt, nt_p, rows, means,
+                                                                                 scales, nx_i, nsel, out);
     note_launch();
     return cudaGetLastError();
 }

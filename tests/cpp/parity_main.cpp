@@ -340,7 +340,7 @@ int main() {
             for (std::size_t i = 0; i < spec.nx; ++i)
                 for (std::size_t t = 0; t < spec.nt; ++t) raw(v * spec.nx + i, t) = made.variables[v](i, t);
         double traj_gap = 0, err_gap = 0, lam_gap = 0, field_same = 0, field_chain = 0, grid_err = 0, grid_traj = 0;
-        bool grid_pair = true;
+        bool grid_pair = true, probes_same = true;
         std::string err_detail;
         bool pair_same = true;
         std::size_t r_ref = 0, r_gpu = 0;
@@ -408,6 +408,16 @@ int main() {
                                                            br, trr, orf.trajectory, params_of(r)), fr));
             field_chain = std::max(field_chain, rel_frob(dopinf_b200::postprocess::reconstruct_field(
                                                              bg, trg, ogp.trajectory, params_of(g)), fr));
+            // probes (postprocess.cpp:36-61): bit-identical on the same inputs
+            postprocess::ProbeSet probes;
+            for (std::size_t k = 0; k < spec.nx; k += 37) probes.push_back({0, k});
+            const auto pr = postprocess::reconstruct_probes(br, trr, orf.trajectory, probes, params_of(r));
+            const auto pg = dopinf_b200::postprocess::reconstruct_probes<postprocess::ProbeSeries>(
+                br, trr, orf.trajectory, probes, params_of(r));
+            probes_same = probes_same && pr.size() == pg.size();
+            for (std::size_t k = 0; probes_same && k < pr.size(); ++k) {
+                probes_same = pr[k].probe == pg[k].probe && pr[k].values == pg[k].values;
+            }
         }
         report(lam_gap <= 1e-10, "pipeline eigenvalues", "rel to lambda1 " + fmt(lam_gap) + " <= 1e-10");
         report(pair_same, "pipeline r and optimal (beta1, beta2) identical", "r = " + std::to_string(r_gpu));
@@ -417,6 +427,7 @@ int main() {
         report(grid_pair && grid_err <= 1e-8 && grid_traj <= 1e-8, "device grid_search vs rom_search::grid_search",
                "same pair and owner; train_err gap / max(err, 1e-4) " + fmt(grid_err) + ", trajectory rel " +
                    fmt(grid_traj) + " <= 1e-8");
+        report(probes_same, "reconstruct_probes bit-identical to postprocess::reconstruct_probes", "11 probes, both runs");
         report(field_same <= 1e-10 && field_chain <= 1e-8, "reconstruct_field vs postprocess::reconstruct_field",
                "same inputs rel " + fmt(field_same) + " <= 1e-10; whole chain rel " + fmt(field_chain) + " <= 1e-8");
     }

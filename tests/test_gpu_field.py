@@ -133,3 +133,42 @@ def test_field_errors(tmp_path, ctx, oracle):
     with pytest.raises(a.DataFormatError, match="nx must be >= 1"):
         a.write_field(e, tr, qt, pe, ["v", "w"], str(tmp_path / "e.snp1"))
     assert struct.calcsize("<QQQ") == 24
+
+
+@pytest.mark.parametrize("nv,nx,nt,r,nt_p,scaling", [(2, 500, 64, 3, 7, True), (1, 4097, 120, 10, 240, False),
+                                                   (3, 2000, 96, 20, 129, True), (2, 3001, 200, 40, 400, True),
+                                                   (1, 700, 180, 100, 65, True)])
+def test_probes_bit_identical(ctx, oracle, reference, nv, nx, nt, r, nt_p, scaling):
+    # postprocess::reconstruct_probes (postprocess.cpp:36-61): basis_rows order,
+    # kernels::dot's AVX2 order (incl. the 4-block and the unfused tail) and
+    # scale_shift's FMA -> the same bits as the reference
+    a = api()
+    b, params, tr, qt = _setup(ctx, oracle, nv, nx, nt, r, nt_p, scaling, seed=nt * r)
+    rng = np.random.default_rng(r)
+    probes = [a.Probe(int(rng.integers(nv)), int(rng.integers(nx))) for _ in range(40)]
+    probes += [a.Probe(0, nx + 5), a.Probe(nv - 1, nx - 1), a.Probe(0, 0)]  # one not owned, the edges
+    got = a.reconstruct_probes(b, tr, qt, probes, params)
+    want, owned = reference.reconstruct_probes(b.values, nv, 0, tr, qt, params.local_means,
+                                               params.scales if scaling else None, scaling,
+                                               [p.var for p in probes], [p.index for p in probes])
+    assert [s.probe for s in got] == [p for p, o in zip(probes, owned) if o]
+    assert np.array_equal(np.stack([s.values for s in got]), want[owned])
+
+
+def test_probes_rank_slice_and_errors(ctx, oracle, reference):
+    # a rank's slice (row_begin > 0): only its probes come back; a bad variable raises
+    a = api()
+    nv, nx, nt, r, nt_p = 2, 300, 40, 6, 50
+    rng = oracle.rng(9)
+    raw = rng.matrix(nv * nx, nt)
+    b = a.LocalBlock(ctx, nv, a.RowRange(1000, 1000 + nx), nt, values=raw)
+    params, _ = a.snapshot_pass(b, True)
+    tr, qt = rng.matrix(nt, r), rng.matrix(nt_p, r)
+    probes = [a.Probe(1, 1000), a.Probe(0, 999), a.Probe(1, 1299), a.Probe(0, 1300), a.Probe(0, 1150)]
+    got = a.reconstruct_probes(b, tr, qt, probes, params)
+    want, owned = reference.reconstruct_probes(b.values, nv, 1000, tr, qt, params.local_means, params.scales, True,
+                                               [p.var for p in probes], [p.index for p in probes])
+    assert list(owned) == [True, False, True, False, True]
+    assert np.array_equal(np.stack([s.values for s in got]), want[owned])
+    with pytest.raises(a.InvalidArgumentError, match="outside the local block"):
+        a.reconstruct_probes(b, tr, qt, [a.Probe(2, 1100)], params)

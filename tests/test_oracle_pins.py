@@ -188,3 +188,26 @@ def test_oracle_field_vs_reference(oracle, reference, nv, nx, nt, r, nt_p, scali
     want = reference.reconstruct_field(q, nv, tr, qt, means, scales, scaling)
     got = oracle.reconstruct_field(q, tr, qt, means, scales, nx, scaling)
     assert np.array_equal(got, want)
+
+
+
+@pytest.mark.parametrize("r,nt_p", [(3, 7), (10, 21), (20, 9), (13, 5)])
+def test_oracle_probes_vs_reference(oracle, reference, r, nt_p):
+    # postprocess::reconstruct_probes restated: basis_rows, kernels::dot, then
+    # inverse_transform_row's scale_shift (one FMA per entry), bit for bit
+    nv, nx, nt = 2, 30, 17
+    rng = oracle.rng(r * 7 + nt_p)
+    q, means = oracle.center(rng.matrix(nv * nx, nt))
+    scales, _ = oracle.reduce_scales(oracle.local_maxabs(q, nv, nx)[None, :])
+    q = oracle.scale(q, nv, nx, scales)
+    tr, qt = rng.matrix(nt, r), rng.matrix(nt_p, r)
+    var, index = [0, 1, 1, 0], [3, 0, 29, 17]
+    want, owned = reference.reconstruct_probes(q, nv, 0, tr, qt, means, scales, True, var, index)
+    assert owned.all()
+    rows = [v * nx + i for v, i in zip(var, index)]
+    basis = oracle.basis_rows(q, tr, np.array(rows, dtype=np.uintp))
+    got = np.empty_like(want)
+    for k, row in enumerate(rows):
+        series = np.array([[oracle.k_dot(basis[k], qt[t]) for t in range(nt_p)]])
+        got[k] = oracle.inverse_transform(series, 1, means[row:row + 1], scales[row // nx:row // nx + 1], True)[0]
+    assert np.array_equal(got, want)
