@@ -120,6 +120,12 @@ int dopinf_b200_get_unique_id(unsigned char* id);
  * an NCCL communicator from `id` (ignored when size == 1). */
 int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* id,
                            dopinf_b200_ctx** out);
+/* A context on the caller's NCCL communicator and CUDA stream (plain
+ * pointers: ncclComm_t and cudaStream_t; either may be NULL — no
+ * communicator means one rank, no stream means the context makes its own).
+ * Rank and size come from the communicator. Neither is destroyed with the
+ * context; the caller keeps them alive until dopinf_b200_ctx_destroy. */
+int dopinf_b200_ctx_create_external(int device, void* nccl_comm, void* stream, dopinf_b200_ctx** out);
 void dopinf_b200_ctx_destroy(dopinf_b200_ctx* ctx);
 int dopinf_b200_ctx_rank(const dopinf_b200_ctx* ctx);
 int dopinf_b200_ctx_size(const dopinf_b200_ctx* ctx);

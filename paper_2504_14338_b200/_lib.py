@@ -43,6 +43,7 @@ SIGNATURES = {
     "dopinf_b200_kernel_launches": (C.c_uint64, []),
     "dopinf_b200_get_unique_id": (C.c_int, [C.c_char_p]),
     "dopinf_b200_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
+    "dopinf_b200_ctx_create_external": (C.c_int, [C.c_int, _vp, _vp, C.POINTER(_vp)]),
     "dopinf_b200_ctx_destroy": (None, [_vp]),
     "dopinf_b200_ctx_rank": (C.c_int, [_vp]),
     "dopinf_b200_ctx_size": (C.c_int, [_vp]),

@@ -173,6 +173,26 @@ class DeviceContext:
         self._blocks = weakref.WeakSet()  # destroyed before the context
         self.set_gram_reduce(gram_reduce)
 
+    @classmethod
+    def external(cls, device: int = 0, nccl_comm: int | None = None, stream: int | None = None,
+                 gram_reduce: str = "ordered") -> "DeviceContext":
+        """A context on the caller's NCCL communicator / CUDA stream (raw handle
+        values; None: one rank / own stream). Rank and size come from the
+        communicator; neither handle is destroyed with the context."""
+        lib = _lib.load()
+        h = C.c_void_p()
+        rc = lib.dopinf_b200_ctx_create_external(device, nccl_comm, stream, C.byref(h))
+        if rc != _lib.OK:
+            raise _STATUS.get(rc, Error)(f"ctx_create_external(device={device}) failed: "
+                                         f"{lib.dopinf_b200_status_string(rc).decode()}")
+        self = cls.__new__(cls)
+        self._h = h
+        self._rank, self._size = lib.dopinf_b200_ctx_rank(h), lib.dopinf_b200_ctx_size(h)
+        self.device = device
+        self._blocks = weakref.WeakSet()
+        self.set_gram_reduce(gram_reduce)
+        return self
+
     @staticmethod
     def unique_id() -> bytes:
         buf = C.create_string_buffer(_lib.UNIQUE_ID_BYTES)

@@ -317,6 +317,53 @@ int dopinf_b200_get_unique_id(unsigned char* id) {
     return DOPINF_B200_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Device checks, streams and stage events of a new context (stream: the
+// caller's, or null to create one).
+void init_ctx(dopinf_b200_ctx* c, int device, cudaStream_t stream) {
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) {
+        fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "device " + std::to_string(device) + " not present");
+    }
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0) {
+        fail(DOPINF_B200_ERR_DEVICE, std::string("device is ") + prop.name + " (sm_" + std::to_string(prop.major) +
+                                         std::to_string(prop.minor) + "); this build targets sm_100a (B200) only");
+    }
+    c->num_sms = prop.multiProcessorCount;
+    if (stream) {
+        c->stream = stream;
+        c->owns_stream = false;
+    } else {
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+    ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& pair : c->ev) {
+        ck(cudaEventCreate(&pair[0]), "cudaEventCreate");
+        ck(cudaEventCreate(&pair[1]), "cudaEventCreate");
+    }
+}
+
+int finish_create(dopinf_b200_ctx* c, int rc, dopinf_b200_ctx** out) {
+    if (rc != DOPINF_B200_OK) {
+        std::fprintf(stderr, "dopinf_b200_ctx_create: %s\n", c->err.c_str());
+        dopinf_b200_ctx_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return DOPINF_B200_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* id,
                            dopinf_b200_ctx** out) {
     if (!out || size < 1 || rank < 0 || rank >= size || (size > 1 && !id)) {
@@ -329,39 +376,32 @@ int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* 
     c->rank = rank;
     c->size = size;
     const int rc = guarded(c, [&] {
-        int ndev = 0;
-        ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
-        if (device < 0 || device >= ndev) {
-            fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "device " + std::to_string(device) + " not present");
-        }
-        ck(cudaSetDevice(device), "cudaSetDevice");
-        cudaDeviceProp prop;
-        ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-        if (prop.major != 10 || prop.minor != 0) {
-            fail(DOPINF_B200_ERR_DEVICE, std::string("device is ") + prop.name +
-                                             " (sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
-                                             "); this build targets sm_100a (B200) only");
-        }
-        c->num_sms = prop.multiProcessorCount;
-        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-        ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
-        for (auto& pair : c->ev) {
-            ck(cudaEventCreate(&pair[0]), "cudaEventCreate");
-            ck(cudaEventCreate(&pair[1]), "cudaEventCreate");
-        }
+        init_ctx(c, device, nullptr);
         if (size > 1) {
             ncclUniqueId uid;
             std::memcpy(&uid, id, sizeof uid);
             ckn(ncclCommInitRank(&c->comm, size, uid, rank), "ncclCommInitRank");
         }
     });
-    if (rc != DOPINF_B200_OK) {
-        std::fprintf(stderr, "dopinf_b200_ctx_create: %s\n", c->err.c_str());
-        dopinf_b200_ctx_destroy(c);
-        return rc;
-    }
-    *out = c;
-    return DOPINF_B200_OK;
+    return finish_create(c, rc, out);
+}
+
+int dopinf_b200_ctx_create_external(int device, void* nccl_comm, void* stream, dopinf_b200_ctx** out) {
+    if (!out) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto* c = new (std::nothrow) dopinf_b200_ctx;
+    if (!c) return DOPINF_B200_ERR_OUT_OF_MEMORY;
+    c->device = device;
+    const int rc = guarded(c, [&] {
+        init_ctx(c, device, static_cast<cudaStream_t>(stream));
+        if (nccl_comm) {
+            c->comm = static_cast<ncclComm_t>(nccl_comm);
+            c->owns_comm = false;
+            ckn(ncclCommUserRank(c->comm, &c->rank), "ncclCommUserRank");
+            ckn(ncclCommCount(c->comm, &c->size), "ncclCommCount");
+        }
+    });
+    return finish_create(c, rc, out);
 }
 
 void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
@@ -370,7 +410,7 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm && c->owns_comm) ncclCommDestroy(c->comm);
     for (auto& pair : c->ev) {
         if (pair[0]) cudaEventDestroy(pair[0]);
         if (pair[1]) cudaEventDestroy(pair[1]);
@@ -395,7 +435,7 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
         cudaStreamSynchronize(c->copy_stream);
         cudaStreamDestroy(c->copy_stream);
     }
-    if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->stream && c->owns_stream) cudaStreamDestroy(c->stream);
     cudaSetDevice(prev);
     delete c;
 }

@@ -187,6 +187,7 @@ struct dopinf_b200_ctx {
         return total;
     }
     ncclComm_t comm = nullptr;
+    bool owns_comm = true, owns_stream = true;  // false: handed in by dopinf_b200_ctx_create_external
     int gram_reduce = DOPINF_B200_GRAM_REDUCE_ORDERED;
     std::string err;
 

@@ -316,3 +316,22 @@ def test_synth_stream_pass_matches_resident(ctx, oracle):
     assert np.array_equal(p1.scales, p2.scales)
     assert rel_frob(d2, d1) <= GRAM_TOL
     assert ctx.stage_ms("stream_gram") > 0.0
+
+
+def test_external_stream_context(ctx):
+    # dopinf_b200_ctx_create_external: the caller's stream (here torch's), no communicator
+    import torch
+
+    a = api()
+    s = torch.cuda.Stream()
+    ext = a.DeviceContext.external(0, None, s.cuda_stream)
+    assert ext.rank() == 0 and ext.size() == 1 and ext.stream() == s.cuda_stream
+    rng = np.random.default_rng(4)
+    q = rng.standard_normal((2 * 3000, 40)) + 2.0
+    b1 = a.LocalBlock(ext, 2, a.RowRange(0, 3000), 40, values=q)
+    b2 = a.LocalBlock(ctx, 2, a.RowRange(0, 3000), 40, values=q)
+    p1, d1 = a.snapshot_pass(b1, True)
+    p2, d2 = a.snapshot_pass(b2, True)
+    assert np.array_equal(p1.local_means, p2.local_means) and np.array_equal(d1, d2)
+    ext.close()
+    s.synchronize()  # the caller's stream outlives the context
