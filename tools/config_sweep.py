@@ -77,7 +77,7 @@ def run_c5(ctx, out, rs, n_probes=1000):
     nv, nx, K = 4, 262144, 1200
     b = api.LocalBlock(ctx, nv, api.RowRange(0, nx), K)
     b.synth_oscillator(seed=2, n_modes=40, dt=1e-3, noise=1e-4)
-    _, d = api.snapshot_pass(b, scaling=True)
+    params, d = api.snapshot_pass(b, scaling=True)
     n = nv * nx
     rng = np.random.default_rng(5)
     probes = np.sort(rng.choice(n, size=n_probes, replace=False))
@@ -93,12 +93,19 @@ def run_c5(ctx, out, rs, n_probes=1000):
         t0 = time.perf_counter()
         rows = api.basis_rows(b, tr, probes)
         t_probe = time.perf_counter() - t0
+        # the probes' series over the 2K horizon from a ROM trajectory (reconstruct_probes)
+        qt = np.random.default_rng(r).standard_normal((2 * K, r)) * 1e-2
+        plist = [api.Probe(int(p) // nx, int(p) % nx) for p in probes]
+        t0 = time.perf_counter()
+        series = api.reconstruct_probes(b, tr, qt, plist, params)
+        t_series = time.perf_counter() - t0
         emit({"config": "c5", "n": n, "K": K, "r": r, "basis_ms": round(best, 3),
               "tflops": round(flops / best / 1e9, 3), "gbs": round(byts / best / 1e6, 1),
               "frac_fp64": round(flops / best / 1e9 / PEAK_FP64, 4), "frac_hbm": round(byts / best / 1e6 / PEAK_HBM, 4),
               "roofline_ms": round(max(flops / PEAK_FP64 / 1e9, byts / PEAK_HBM / 1e6), 3),
               "probe_rows": n_probes, "probe_basis_rows_wall_ms": round(t_probe * 1e3, 3),
-              "probe_rows_shape": list(rows.shape)}, out)
+              "probe_rows_shape": list(rows.shape), "probe_series_nt_p": 2 * K,
+              "reconstruct_probes_wall_ms": round(t_series * 1e3, 3), "probe_series": len(series)}, out)
     b.close()
 
 
