@@ -99,7 +99,19 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ a, const 
     const int nb8 = n / 8;
     const bool four = n - 8 * nb8 >= 4;
     double acc = 0.0;
-    for (int blk = 0; blk < nb8; ++blk) acc = __fma_rn(a[8 * blk + l], b[8 * blk + l], acc);
+    int blk = 0;
+    // eight loads in flight ahead of each eight-long stretch of the FMA chain
+    for (; blk + 8 <= nb8; blk += 8) {
+        double x[8], y[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            x[u] = __ldg(a + 8 * (blk + u) + l);
+            y[u] = b[8 * (blk + u) + l];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __fma_rn(x[u], y[u], acc);
+    }
+    for (; blk < nb8; ++blk) acc = __fma_rn(__ldg(a + 8 * blk + l), b[8 * blk + l], acc);
     if (four && l < 4) acc = __fma_rn(a[8 * nb8 + l], b[8 * nb8 + l], acc);
     // v_l = acc0_l + acc1_l (lanes l and l + 4)
     const double hi = __shfl_down_sync(gmask, acc, 4, 8);
