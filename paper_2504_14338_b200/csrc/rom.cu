@@ -18,6 +18,8 @@
 // unfused). Eight threads run the eight chains of one output. The scores
 // follow training_error / growth_ratio (rom_search.cpp:94-145) in the
 // reference's (unfused) order.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -105,13 +107,13 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ a, const 
         double x[8], y[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            x[u] = __ldg(a + 8 * (blk + u) + l);
+            x[u] = a[8 * (blk + u) + l];  // global or shared (generic load)
             y[u] = b[8 * (blk + u) + l];
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc = __fma_rn(x[u], y[u], acc);
     }
-    for (; blk < nb8; ++blk) acc = __fma_rn(__ldg(a + 8 * blk + l), b[8 * blk + l], acc);
+    for (; blk < nb8; ++blk) acc = __fma_rn(a[8 * blk + l], b[8 * blk + l], acc);
     if (four && l < 4) acc = __fma_rn(a[8 * nb8 + l], b[8 * nb8 + l], acc);
     // v_l = acc0_l + acc1_l (lanes l and l + 4)
     const double hi = __shfl_down_sync(gmask, acc, 4, 8);
@@ -178,6 +180,69 @@ __global__ void __launch_bounds__(1024)
             }
         }
         __syncthreads();
+    }
+}
+
+// The same integration with each pair's operators resident in shared memory:
+// a cluster of CL CTAs per pair, CTA k holding the operator columns of outputs
+// [k·rpc, (k+1)·rpc) (rpc·d doubles). Every CTA forms quad(q) itself, computes
+// its outputs from shared memory, and writes them into every cluster member's
+// next-state buffer (distributed shared memory); one cluster barrier per step.
+// Same arithmetic, same order as integrate_kernel (group_dot), so the same bits.
+__global__ void __launch_bounds__(1024)
+    integrate_cluster_kernel(const double* __restrict__ ops, int r, const double* __restrict__ q0, int n_steps,
+                             int rpc, double* __restrict__ traj) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) double smc[];
+    const int s = r * (r + 1) / 2;
+    const int d = r + s + 1;
+    const int CL = static_cast<int>(cluster.num_blocks());
+    const int cr = static_cast<int>(cluster.block_rank());
+    const int p = blockIdx.x / CL;
+    const int i0 = cr * rpc, i1 = min(r, i0 + rpc);
+    const double* x = ops + static_cast<size_t>(p) * d * r;
+    double* tp = traj + static_cast<size_t>(p) * n_steps * r;
+    double* cols = smc;                                     // rpc × d: this CTA's operator columns
+    double* qb = cols + static_cast<size_t>(rpc) * d;       // 2 × r: state, double-buffered
+    double* feat = qb + 2 * r;                              // s
+    int* pi = reinterpret_cast<int*>(feat + s);             // s
+    const int g = threadIdx.x / 8, l = threadIdx.x % 8;
+    const unsigned gmask = 0xFFu << (8 * ((threadIdx.x % 32) / 8));
+    for (size_t e = threadIdx.x; e < static_cast<size_t>(i1 - i0) * d; e += blockDim.x) {
+        cols[e] = x[static_cast<size_t>(i0) * d + e];
+    }
+    for (int i = 0, pos = 0; i < r; ++i) {
+        for (int j = i; j < r; ++j, ++pos) {
+            if (pos % blockDim.x == static_cast<int>(threadIdx.x)) pi[pos] = (i << 16) | j;
+        }
+    }
+    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+        qb[i] = q0[i];
+        if (cr == 0) tp[i] = q0[i];
+    }
+    cluster.sync();
+    int cur = 0;
+    for (int k = 0; k + 1 < n_steps; ++k) {
+        const double* q = qb + cur * r;
+        for (int pos = threadIdx.x; pos < s; pos += blockDim.x) {
+            const int e = pi[pos];
+            feat[pos] = __dmul_rn(q[e >> 16], q[e & 0xFFFF]);
+        }
+        __syncthreads();
+        const int i = i0 + g;
+        if (i < i1) {
+            const double* col = cols + static_cast<size_t>(g) * d;
+            const double da = group_dot(col, q, r, l, gmask);
+            const double df = group_dot(col + r, feat, s, l, gmask);
+            const double v = __dadd_rn(__dadd_rn(col[r + s], da), df);  // c_i + dot(A_i, q) + dot(F_i, feat)
+            if (l == 0) {
+                for (int m = 0; m < CL; ++m) cluster.map_shared_rank(qb + (cur ^ 1) * r, m)[i] = v;
+                tp[static_cast<size_t>(k + 1) * r + i] = v;
+            }
+        }
+        cluster.sync();  // next state complete everywhere; q and feat no longer read
+        cur ^= 1;
     }
 }
 
@@ -304,12 +369,42 @@ cudaError_t launch_integrate(const double* ops, int r, const double* q0, int n_s
                              cudaStream_t stream) {
     if (n_pairs <= 0) return cudaSuccess;
     const int s = r * (r + 1) / 2;
+    const int d = r + s + 1;
+    constexpr size_t kSmemCap = 200 * 1024;
+    // Operators that fit L1 stay there (one CTA per pair, the plain kernel);
+    // larger ones are held in shared memory by the smallest cluster (2..8
+    // CTAs) whose slices of operator columns fit.
+    const bool l1_resident = static_cast<size_t>(r) * d * sizeof(double) <= 160 * 1024;
+    for (int CL = 2; !l1_resident && CL <= 8; CL *= 2) {
+        const int rpc = (r + CL - 1) / CL;
+        if (rpc > 128) continue;  // ≤ 1024 threads: 8 per output
+        const size_t smem = (static_cast<size_t>(rpc) * d + 2 * r + s) * sizeof(double) + s * sizeof(int);
+        if (smem > kSmemCap) continue;
+        cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(integrate_cluster_kernel), kSmemCap);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(n_pairs * CL);
+        cfg.blockDim = dim3(std::max(32, (8 * rpc + 31) / 32 * 32));
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, integrate_cluster_kernel, ops, r, q0, n_steps, rpc, traj);
+        note_launch();
+        return e != cudaSuccess ? e : cudaGetLastError();
+    }
+    // operators in L1 (or too large even for a cluster's shared memory: L2)
     const int threads = std::min(1024, std::max(32, ((8 * r + 31) / 32) * 32));
     const int groups = threads / 8;
     if ((r + groups - 1) / groups > 8) return cudaErrorInvalidValue;  // outputs per group
     const size_t smem = static_cast<size_t>(r + s) * sizeof(double) + static_cast<size_t>(s) * sizeof(int);
-    if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(integrate_kernel), 200 * 1024);
+    if (smem > kSmemCap) return cudaErrorInvalidValue;
+    cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(integrate_kernel), kSmemCap);
     if (e != cudaSuccess) return e;
     integrate_kernel<<<n_pairs, threads, smem, stream>>>(ops, r, q0, n_steps, traj);
     note_launch();

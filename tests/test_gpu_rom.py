@@ -47,7 +47,10 @@ def _qhat(oracle, r, nt, seed, decay=0.05):
 
 
 @pytest.mark.parametrize("r,nt,steps", [(1, 20, 50), (3, 40, 80), (4, 40, 80), (5, 30, 400), (9, 60, 120),
-                                        (12, 50, 100)])
+                                        (12, 50, 100),
+                                        # operators beyond L1: the shared-memory cluster kernel (2 / 4 CTAs,
+                                        # uneven slices)
+                                        (40, 120, 60), (45, 120, 40), (61, 150, 25)])
 def test_integrate_bit_identical(ctx, oracle, reference, r, nt, steps):
     a = api()
     q = _qhat(oracle, r, nt, seed=r)
