@@ -89,7 +89,13 @@ GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r
     double* rhs = c->rom_rhs.get<double>(static_cast<size_t>(D) * r, "rhs");
     ck(rom::launch_assemble(dq, R, NT, dhat, ldd, q2t, c->stream), "assemble");
     ck(rom::launch_transpose(dq, R, NT, qrows, c->stream), "transpose");
-    rom_gram(c, dhat, ldd, KK, D, g);
+    // DhatᵀDhat: bit-identical to linalg::gram (FMA chains) up to d = 2048;
+    // larger systems on the tensor-pipe Gram kernel
+    if (D <= 2048) {
+        ck(rom::launch_gram_exact(dhat, ldd, KK, D, g, c->stream), "dhat gram");
+    } else {
+        rom_gram(c, dhat, ldd, KK, D, g);
+    }
     ck(rom::launch_rhs(dhat, ldd, q2t, KK, D, R, rhs, c->stream), "rhs");
 
     // this rank's candidates, solved / integrated / scored in batches that fit
@@ -132,7 +138,15 @@ GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r
         ck(rom::launch_systems(g, D, R, betas, betas + nb, static_cast<int>(nb), rhs, lhs, rhsb, c->stream),
            "systems");
         ck(cudaMemsetAsync(info, 0, 2 * nb * sizeof(int), c->stream), "memset");
-        if (c->solver.spd_solve(lhs, D, static_cast<int>(nb), rhsb, R, info, c->stream, &err) != cudaSuccess) {
+        // Cholesky factors over concurrent cuSOLVER lanes, then every pair's
+        // triangular solves in one launch (shared-memory substitution); systems
+        // beyond the shared-memory solve use cuSOLVER's potrs per pair
+        if (D <= 1760) {
+            if (c->solver.cholesky(lhs, D, static_cast<int>(nb), info, c->stream, &err) != cudaSuccess) {
+                fail(DOPINF_B200_ERR_DEVICE, err);
+            }
+            ck(rom::launch_chol_solve(lhs, D, static_cast<int>(nb), rhsb, R, c->stream), "cholesky solve");
+        } else if (c->solver.spd_solve(lhs, D, static_cast<int>(nb), rhsb, R, info, c->stream, &err) != cudaSuccess) {
             fail(DOPINF_B200_ERR_DEVICE, err);
         }
         ck(cudaEventRecord(ev[0], c->stream), "event");

@@ -233,8 +233,8 @@ Solver::CholLane::~CholLane() {
     if (work) cudaFree(work);
 }
 
-cudaError_t Solver::spd_solve(double* a, int n, int batch, double* b, int nrhs, int* info_dev, cudaStream_t stream,
-                              std::string* err) {
+cudaError_t Solver::chol_lanes(double* a, int n, int batch, double* b, int nrhs, int* info_dev, cudaStream_t stream,
+                               std::string* err) {
     if (!ensure_handle(err)) return cudaErrorNotSupported;
     const Api& x = api();
     const int lanes = std::min(kCholLanes, std::max(batch, 1));
@@ -273,14 +273,14 @@ cudaError_t Solver::spd_solve(double* a, int n, int batch, double* b, int nrhs, 
         CholLane& ln = lanes_[i % lanes];
         auto h = static_cast<cusolverDnHandle_t>(ln.handle);
         double* ai = a + static_cast<size_t>(i) * n * n;
-        double* bi = b + static_cast<size_t>(i) * n * nrhs;
+        double* bi = b ? b + static_cast<size_t>(i) * n * nrhs : nullptr;
         if (x.potrf(h, CUBLAS_FILL_MODE_LOWER, n, ai, n, static_cast<double*>(ln.work),
                     static_cast<int>(ln.work_doubles), info_dev + i) != CUSOLVER_STATUS_SUCCESS) {
             *err = "cusolverDnDpotrf failed";
             return cudaErrorUnknown;
         }
-        if (x.potrs(h, CUBLAS_FILL_MODE_LOWER, n, nrhs, ai, n, bi, n, info_dev + batch + i) !=
-            CUSOLVER_STATUS_SUCCESS) {
+        if (b && x.potrs(h, CUBLAS_FILL_MODE_LOWER, n, nrhs, ai, n, bi, n, info_dev + batch + i) !=
+                     CUSOLVER_STATUS_SUCCESS) {
             *err = "cusolverDnDpotrs failed";
             return cudaErrorUnknown;
         }
@@ -290,6 +290,15 @@ cudaError_t Solver::spd_solve(double* a, int n, int batch, double* b, int nrhs, 
         if ((e = cudaStreamWaitEvent(stream, lanes_[l].done, 0)) != cudaSuccess) return e;
     }
     return cudaGetLastError();
+}
+
+cudaError_t Solver::spd_solve(double* a, int n, int batch, double* b, int nrhs, int* info_dev, cudaStream_t stream,
+                              std::string* err) {
+    return chol_lanes(a, n, batch, b, nrhs, info_dev, stream, err);
+}
+
+cudaError_t Solver::cholesky(double* a, int n, int batch, int* info_dev, cudaStream_t stream, std::string* err) {
+    return chol_lanes(a, n, batch, nullptr, 0, info_dev, stream, err);
 }
 
 cudaError_t launch_reduced_map(const double* v, const double* lambda, int n, int r, double* tr, cudaStream_t stream) {

@@ -28,6 +28,8 @@ public:
     // potrf infos, then potrs.
     cudaError_t spd_solve(double* a, int n, int batch, double* b, int nrhs, int* info_dev, cudaStream_t stream,
                           std::string* err);
+    // Only the factorisations (lower Cholesky in place), info_dev[batch].
+    cudaError_t cholesky(double* a, int n, int batch, int* info_dev, cudaStream_t stream, std::string* err);
 
 private:
     static constexpr int kCholLanes = 8;
@@ -40,6 +42,8 @@ private:
         ~CholLane();
     };
     bool ensure_handle(std::string* err);
+    cudaError_t chol_lanes(double* a, int n, int batch, double* b, int nrhs, int* info_dev, cudaStream_t stream,
+                           std::string* err);
     void* handle_ = nullptr;
     cudaEvent_t start_ = nullptr;
     CholLane lanes_[kCholLanes];

@@ -70,6 +70,20 @@ __global__ void matmul_tn_cm_kernel(const double* __restrict__ a, size_t lda, co
     out[e] = acc;
 }
 
+// G = DhatᵀDhat in linalg::gram's order (linalg.cpp:50-58: c.row(i) +=
+// a(l, i)·a.row(l) by axpy → G(i, j) an FMA chain over l), so G is
+// bit-identical to the reference's (and bitwise symmetric: the products
+// commute). One thread per (i, j ≥ i); the CTA's warp runs along j.
+__global__ void gram_exact_kernel(const double* __restrict__ a, size_t lda, int K, int d, double* __restrict__ g) {
+    const int i = blockIdx.y;
+    const int j = i + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= d) return;
+    double acc = 0.0;
+    for (int l = 0; l < K; ++l) acc = __fma_rn(a[static_cast<size_t>(l) * lda + i], a[static_cast<size_t>(l) * lda + j], acc);
+    g[static_cast<size_t>(i) * d + j] = acc;
+    g[static_cast<size_t>(j) * d + i] = acc;
+}
+
 // Pair p's system: lhs_p = G + diag(γ_p) (opinf.cpp:76-77; build_regularizer
 // opinf.cpp:60-67: β1 on the r state columns and the ones column, β2 on the s
 // quadratic ones), rhs_p = rhs.
@@ -246,6 +260,59 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
+// X = L⁻ᵀ L⁻¹ B for one pair's Cholesky factor (column-major, lower: L[i + j·d])
+// and a chunk of kSolveCols right-hand sides held in shared memory: forward
+// substitution column by column (right-looking: each solved y_j updates the
+// rows below it from L's contiguous column j), then backward substitution
+// row by row (left-looking: x_j needs column j of L below the diagonal dotted
+// with the solved x below, a 16-lane reduction per right-hand side).
+constexpr int kSolveCols = 16;
+constexpr int kSolveThreads = 256;
+
+__global__ void __launch_bounds__(kSolveThreads)
+    chol_solve_kernel(const double* __restrict__ lbatch, int d, double* __restrict__ bbatch, int r) {
+    extern __shared__ double xs[];  // d × kSolveCols, column c at xs[c·d]
+    const int p = blockIdx.y;
+    const int c0 = blockIdx.x * kSolveCols;
+    const int nc = min(kSolveCols, r - c0);
+    const double* L = lbatch + static_cast<size_t>(p) * d * d;
+    double* B = bbatch + static_cast<size_t>(p) * d * r;
+    for (int e = threadIdx.x; e < d * nc; e += blockDim.x) {
+        const int c = e / d, i = e % d;
+        xs[c * d + i] = B[static_cast<size_t>(c0 + c) * d + i];
+    }
+    __syncthreads();
+    // forward: L y = b
+    for (int j = 0; j < d; ++j) {
+        const double* col = L + static_cast<size_t>(j) * d;
+        if (threadIdx.x < nc) xs[threadIdx.x * d + j] /= col[j];
+        __syncthreads();
+        const int rows = d - 1 - j;
+        for (int e = threadIdx.x; e < rows * nc; e += blockDim.x) {
+            const int c = e / rows, i = j + 1 + e % rows;
+            xs[c * d + i] = fma(-col[i], xs[c * d + j], xs[c * d + i]);
+        }
+        __syncthreads();
+    }
+    // backward: Lᵀ x = y; 16 lanes per right-hand side
+    const int c = threadIdx.x / 16, lane = threadIdx.x % 16;
+    for (int j = d - 1; j >= 0; --j) {
+        const double* col = L + static_cast<size_t>(j) * d;
+        double part = 0.0;
+        if (c < nc) {
+            for (int i = j + 1 + lane; i < d; i += 16) part = fma(col[i], xs[c * d + i], part);
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) part += __shfl_down_sync(0xFFFFFFFFu, part, o, 16);
+        if (c < nc && lane == 0) xs[c * d + j] = (xs[c * d + j] - part) / col[j];
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < d * nc; e += blockDim.x) {
+        const int cc = e / d, i = e % d;
+        B[static_cast<size_t>(c0 + cc) * d + i] = xs[cc * d + i];
+    }
+}
+
 // Scores of one pair per CTA: finite (integrate's check), training_error over
 // the first nt rows against qhat_rows (nt × r), growth_ratio; flags a zero-norm
 // reference row / constant training data the way the reference throws.
@@ -347,6 +414,12 @@ cudaError_t launch_assemble(const double* qhat, int r, int nt, double* dhat, siz
     return cudaGetLastError();
 }
 
+cudaError_t launch_gram_exact(const double* dhat, size_t ldd, int K, int d, double* g, cudaStream_t stream) {
+    gram_exact_kernel<<<dim3((d + 127) / 128, d), 128, 0, stream>>>(dhat, ldd, K, d, g);
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rhs(const double* dhat, size_t ldd, const double* q2t, int K, int d, int r, double* rhs_cm,
                        cudaStream_t stream) {
     const long long total = static_cast<long long>(d) * r;
@@ -407,6 +480,17 @@ cudaError_t launch_integrate(const double* ops, int r, const double* q0, int n_s
     cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(integrate_kernel), kSmemCap);
     if (e != cudaSuccess) return e;
     integrate_kernel<<<n_pairs, threads, smem, stream>>>(ops, r, q0, n_steps, traj);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chol_solve(const double* l, int d, int batch, double* b, int r, cudaStream_t stream) {
+    if (batch <= 0) return cudaSuccess;
+    const size_t smem = static_cast<size_t>(d) * kSolveCols * sizeof(double);
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(chol_solve_kernel), 220 * 1024);
+    if (e != cudaSuccess) return e;
+    chol_solve_kernel<<<dim3((r + kSolveCols - 1) / kSolveCols, batch), kSolveThreads, smem, stream>>>(l, d, b, r);
     note_launch();
     return cudaGetLastError();
 }
