@@ -148,3 +148,17 @@ def test_grid_search_errors(ctx, oracle, reference):
     assert str(got.value) == want.value.msg
     with pytest.raises(a.InvalidArgumentError, match="need at least one step"):
         a.rom_integrate(ctx, np.eye(2), np.zeros((2, 3)), np.zeros(2), np.ones(2), 0)
+
+
+def test_grid_search_large_system_fallback(ctx, oracle, reference):
+    # r = 60: d = 1891 exceeds the shared-memory triangular solve (d <= 1760) and
+    # the exact-order Gram still applies; cuSOLVER potrs per pair, same pair as the reference
+    a = api()
+    r, nt = 60, 120
+    q = _qhat(oracle, r, nt, seed=60)
+    b1, b2 = np.array([1e-2, 1e-1]), np.array([1e-1, 1.0])
+    traj_w, pair_w, err_w = reference.grid_search(q, b1, b2, 1.2, 2 * nt)
+    out = a.grid_search(q, a.SearchConfig(list(b1), list(b2), 1.2, 2 * nt), ctx)
+    assert out.pair_opt == pair_w
+    assert err_close(out.train_err, err_w)
+    assert rel(out.trajectory, traj_w) <= ROM_TOL
