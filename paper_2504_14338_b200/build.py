@@ -129,7 +129,23 @@ def build_parity_harness() -> Path | None:
     return out
 
 
+def build_c_smoke() -> Path:
+    """tests/c/_build/abi_smoke: the C ABI exercised from plain C11 (gcc)."""
+    out = ROOT / "tests" / "c" / "_build" / "abi_smoke"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    src = ROOT / "tests" / "c" / "abi_smoke.c"
+    if not _stale(out, [src, LIB, ROOT / "include" / "dopinf_b200.h"]):
+        return out
+    cmd = ["gcc", "-std=c11", "-O2", "-Wall", "-Wextra", "-Werror", f"-I{ROOT / 'include'}", str(src), f"-L{PKG}",
+           "-ldopinf_b200", "-Wl,-rpath,$ORIGIN/../../../paper_2504_14338_b200", "-lm", "-o", str(out)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"C smoke build failed:\n{res.stderr}")
+    return out
+
+
 if __name__ == "__main__":
     print(build_extension(verbose=True))
     build_oracle()
     print(build_parity_harness())
+    print(build_c_smoke())

@@ -19,3 +19,17 @@ def test_cpp_dropin_parity():
     print(res.stdout)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "FAIL" not in res.stdout
+
+
+C_BIN = Path(__file__).resolve().parent / "c" / "_build" / "abi_smoke"
+
+
+def test_c_abi_from_plain_c():
+    # tests/c/abi_smoke.c: the ABI from C11 (no C++ anywhere on the caller's side)
+    if not C_BIN.exists():
+        from paper_2504_14338_b200 import build
+
+        build.build_c_smoke()
+    res = subprocess.run([str(C_BIN)], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "all checks passed" in res.stdout
