@@ -261,50 +261,84 @@ __global__ void __launch_bounds__(1024)
 }
 
 // X = L⁻ᵀ L⁻¹ B for one pair's Cholesky factor (column-major, lower: L[i + j·d])
-// and a chunk of kSolveCols right-hand sides held in shared memory: forward
-// substitution column by column (right-looking: each solved y_j updates the
-// rows below it from L's contiguous column j), then backward substitution
-// row by row (left-looking: x_j needs column j of L below the diagonal dotted
-// with the solved x below, a 16-lane reduction per right-hand side).
+// and a chunk of kSolveCols right-hand sides held in shared memory, in blocks
+// of kSolveBlock unknowns (two CTA barriers per block instead of per unknown):
+//  forward  — the block's small triangle solved by one lane per right-hand
+//             side, then every row below updated with the block's solutions
+//             (8-term FMA sums along L's contiguous columns);
+//  backward — each warp forms, for one unknown of the block, the dots of its
+//             L column below the block with the solved x (two lanes per
+//             right-hand side), then the block's triangle is solved upward.
 constexpr int kSolveCols = 16;
 constexpr int kSolveThreads = 256;
+constexpr int kSolveBlock = 8;
 
 __global__ void __launch_bounds__(kSolveThreads)
     chol_solve_kernel(const double* __restrict__ lbatch, int d, double* __restrict__ bbatch, int r) {
     extern __shared__ double xs[];  // d × kSolveCols, column c at xs[c·d]
+    __shared__ double part[kSolveBlock][kSolveCols];
     const int p = blockIdx.y;
     const int c0 = blockIdx.x * kSolveCols;
     const int nc = min(kSolveCols, r - c0);
     const double* L = lbatch + static_cast<size_t>(p) * d * d;
     double* B = bbatch + static_cast<size_t>(p) * d * r;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (int e = threadIdx.x; e < d * nc; e += blockDim.x) {
         const int c = e / d, i = e % d;
         xs[c * d + i] = B[static_cast<size_t>(c0 + c) * d + i];
     }
     __syncthreads();
-    // forward: L y = b
-    for (int j = 0; j < d; ++j) {
-        const double* col = L + static_cast<size_t>(j) * d;
-        if (threadIdx.x < nc) xs[threadIdx.x * d + j] /= col[j];
+    // ---- forward: L y = b ----
+    for (int j0 = 0; j0 < d; j0 += kSolveBlock) {
+        const int nb = min(kSolveBlock, d - j0);
+        if (threadIdx.x < nc) {
+            double* x = xs + threadIdx.x * d;
+            for (int jj = 0; jj < nb; ++jj) {
+                const int j = j0 + jj;
+                const double y = x[j] / L[static_cast<size_t>(j) * d + j];
+                x[j] = y;
+                for (int kk = jj + 1; kk < nb; ++kk) x[j0 + kk] = fma(-L[static_cast<size_t>(j) * d + j0 + kk], y, x[j0 + kk]);
+            }
+        }
         __syncthreads();
-        const int rows = d - 1 - j;
+        const int rows = d - j0 - nb;
         for (int e = threadIdx.x; e < rows * nc; e += blockDim.x) {
-            const int c = e / rows, i = j + 1 + e % rows;
-            xs[c * d + i] = fma(-col[i], xs[c * d + j], xs[c * d + i]);
+            const int c = e / rows, i = j0 + nb + e % rows;
+            double acc = xs[c * d + i];
+#pragma unroll
+            for (int jj = 0; jj < kSolveBlock; ++jj) {
+                if (jj < nb) acc = fma(-L[static_cast<size_t>(j0 + jj) * d + i], xs[c * d + j0 + jj], acc);
+            }
+            xs[c * d + i] = acc;
         }
         __syncthreads();
     }
-    // backward: Lᵀ x = y; 16 lanes per right-hand side
-    const int c = threadIdx.x / 16, lane = threadIdx.x % 16;
-    for (int j = d - 1; j >= 0; --j) {
-        const double* col = L + static_cast<size_t>(j) * d;
-        double part = 0.0;
-        if (c < nc) {
-            for (int i = j + 1 + lane; i < d; i += 16) part = fma(col[i], xs[c * d + i], part);
+    // ---- backward: Lᵀ x = y ----
+    const int nblk = (d + kSolveBlock - 1) / kSolveBlock;
+    for (int blk = nblk - 1; blk >= 0; --blk) {
+        const int j0 = blk * kSolveBlock, nb = min(kSolveBlock, d - j0);
+        // warp w: unknown j0 + w; lanes (c, half): dot of L column j below the block with x
+        if (warp < nb) {
+            const int j = j0 + warp, c = lane / 2, h = lane % 2;
+            double acc = 0.0;
+            if (c < nc) {
+                const double* col = L + static_cast<size_t>(j) * d;
+                for (int i = j0 + nb + h; i < d; i += 2) acc = fma(col[i], xs[c * d + i], acc);
+            }
+            acc += __shfl_down_sync(0xFFFFFFFFu, acc, 1);
+            if (h == 0 && c < kSolveCols) part[warp][c] = acc;
         }
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) part += __shfl_down_sync(0xFFFFFFFFu, part, o, 16);
-        if (c < nc && lane == 0) xs[c * d + j] = (xs[c * d + j] - part) / col[j];
+        __syncthreads();
+        if (threadIdx.x < nc) {
+            const int c = threadIdx.x;
+            double* x = xs + c * d;
+            for (int jj = nb - 1; jj >= 0; --jj) {
+                const int j = j0 + jj;
+                double v = x[j] - part[jj][c];
+                for (int kk = jj + 1; kk < nb; ++kk) v = fma(-L[static_cast<size_t>(j) * d + j0 + kk], x[j0 + kk], v);
+                x[j] = v / L[static_cast<size_t>(j) * d + j];
+            }
+        }
         __syncthreads();
     }
     for (int e = threadIdx.x; e < d * nc; e += blockDim.x) {
