@@ -291,6 +291,10 @@ int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* ctx, const char* path, size_
  * pair_opt[2] = {beta1, beta2}, train_err, owner, rom_seconds (device time of
  * the integration launch), trajectory nt_p x r. Errors as the reference:
  * InvalidArgumentError, SolveError, NoAdmissiblePairError (same messages). */
+/* rom_search::distribute_pairs (rom_search.cpp:147-160): the contiguous slice
+ * [*begin, *end) of n_reg candidates owned by `rank` of `size` (remainder to
+ * the last rank; ranks beyond n_reg get empty slices). Host only. */
+int dopinf_b200_distribute_pairs(size_t n_reg, int rank, int size, size_t* begin, size_t* end);
 int dopinf_b200_grid_search(dopinf_b200_ctx* ctx, const double* qhat, size_t r, size_t nt, const double* b1,
                             size_t n1, const double* b2, size_t n2, double max_growth, size_t nt_p,
                             double* pair_opt, double* train_err, int* owner, double* rom_seconds,

@@ -82,6 +82,7 @@ SIGNATURES = {
                                                  C.c_int, C.c_double, C.c_double, _dp, C.c_int, _dp, _dp, _dp]),
     "dopinf_b200_snp1_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t,
                                           C.POINTER(C.c_size_t)]),
+    "dopinf_b200_distribute_pairs": (C.c_int, [C.c_size_t, C.c_int, C.c_int, _sp, _sp]),
     "dopinf_b200_grid_search": (C.c_int, [_vp, _dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp, C.c_size_t,
                                           C.c_double, C.c_size_t, _dp, _dp, C.POINTER(C.c_int), _dp, _dp]),
     "dopinf_b200_rom_integrate": (C.c_int, [_vp, _dp, _dp, _dp, C.c_size_t, _dp, C.c_size_t, _dp,

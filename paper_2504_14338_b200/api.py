@@ -600,6 +600,13 @@ def default_b2() -> list:
     return logspace(1e-4, 1e4, 8)
 
 
+def distribute_pairs(n_reg: int, rank: int, size: int) -> RowRange:
+    """rom_search::distribute_pairs (rom_search.cpp:147-160) through the ABI."""
+    b, e = C.c_size_t(), C.c_size_t()
+    _check(_lib.load().dopinf_b200_distribute_pairs(n_reg, rank, size, C.byref(b), C.byref(e)))
+    return RowRange(b.value, e.value)
+
+
 @dataclass
 class SearchConfig:
     """rom_search::SearchConfig (rom_search.hpp:19-24)."""

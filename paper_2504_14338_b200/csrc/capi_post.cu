@@ -18,14 +18,6 @@ void host_allreduce(dopinf_b200_ctx* c, double* data, size_t count, ncclRedOp_t 
     c->sync("allreduce");
 }
 
-// rom_search::distribute_pairs (rom_search.cpp:147-160).
-std::pair<size_t, size_t> distribute_pairs(size_t n_reg, int rank, int size) {
-    const size_t ranks = static_cast<size_t>(size), rk = static_cast<size_t>(rank);
-    if (ranks > n_reg) return rk < n_reg ? std::make_pair(rk, rk + 1) : std::make_pair(n_reg, n_reg);
-    const size_t base = n_reg / ranks;
-    return {rk * base, (rk + 1 == ranks) ? n_reg : (rk + 1) * base};
-}
-
 // G = DhatᵀDhat (d × d, full, bitwise symmetric) with the Gram kernel on the
 // grid search's own plan/tiles (the snapshot pass's cached plan stays intact).
 void rom_gram(dopinf_b200_ctx* c, const double* dhat, size_t ldd, int K, int d, double* g) {
@@ -100,7 +92,11 @@ GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r
 
     // this rank's candidates, solved / integrated / scored in batches that fit
     const size_t n_reg = n1 * n2;
-    const auto mine = distribute_pairs(n_reg, c->rank, c->size);
+    size_t pb = 0, pe = 0;
+    if (dopinf_b200_distribute_pairs(n_reg, c->rank, c->size, &pb, &pe) != DOPINF_B200_OK) {
+        fail(DOPINF_B200_ERR_INVALID_ARGUMENT, g_thread_err);
+    }
+    const std::pair<size_t, size_t> mine(pb, pe);
     const size_t np = mine.second - mine.first;
     const size_t per_pair = static_cast<size_t>(D) * D + static_cast<size_t>(D) * r + nt_p * r;
     const size_t batch = std::max<size_t>(1, std::min<size_t>(std::max<size_t>(np, 1),
@@ -436,6 +432,23 @@ bool pwrite_parallel(int fd, const void* src, size_t bytes, uint64_t off) {
 }  // namespace dopinf_b200
 
 extern "C" {
+
+int dopinf_b200_distribute_pairs(size_t n_reg, int rank, int size, size_t* begin, size_t* end) {
+    return guarded_free([&] {
+        if (n_reg < 1) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "distribute_pairs: no candidates");
+        if (size < 1 || rank < 0 || rank >= size) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "distribute_pairs: bad rank/size");
+        require(begin && end, "distribute_pairs: null outputs");
+        const size_t ranks = static_cast<size_t>(size), rk = static_cast<size_t>(rank);
+        if (ranks > n_reg) {
+            *begin = rk < n_reg ? rk : n_reg;
+            *end = rk < n_reg ? rk + 1 : n_reg;
+            return;
+        }
+        const size_t base = n_reg / ranks;
+        *begin = rk * base;
+        *end = (rk + 1 == ranks) ? n_reg : (rk + 1) * base;
+    });
+}
 
 int dopinf_b200_grid_search(dopinf_b200_ctx* c, const double* qhat, size_t r, size_t nt, const double* b1,
                             size_t n1, const double* b2, size_t n2, double max_growth, size_t nt_p,

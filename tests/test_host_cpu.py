@@ -158,3 +158,20 @@ def test_two_rank_gloo_matches_reference_order(tmp_path):
     assert uid == bytes(range(128))
     _, _, _, d_ref = oracle_pass(o, q, nv, nx, 2)
     assert np.array_equal(d, d_ref)  # ascending-rank sum = the reference's in-process order
+
+
+def test_distribute_pairs_known_answers():
+    # test_rom_search.cpp:178-191, through the ABI (host only, no GPU)
+    from paper_2504_14338_b200 import api
+
+    for rank in range(8):
+        rr = api.distribute_pairs(64, rank, 8)
+        assert rr.begin == 8 * rank and rr.count() == 8
+    assert api.distribute_pairs(10, 0, 3) == api.RowRange(0, 3)
+    assert api.distribute_pairs(10, 1, 3) == api.RowRange(3, 6)
+    assert api.distribute_pairs(10, 2, 3) == api.RowRange(6, 10)
+    assert [api.distribute_pairs(2, r, 4).count() for r in range(4)] == [1, 1, 0, 0]
+    with pytest.raises(api.InvalidArgumentError, match="no candidates"):
+        api.distribute_pairs(0, 0, 1)
+    with pytest.raises(api.InvalidArgumentError, match="bad rank/size"):
+        api.distribute_pairs(4, 4, 4)
