@@ -10,14 +10,17 @@
 //     atomic queue, so the CTAs running at any moment read the same rows of
 //     Q (L2 reuse across the ~tiles CTAs that need them).
 //   * Each persistent CTA = 1 TMA producer warp + 16 consumer warps. The
-//     producer streams BK×128 row-slabs of the I and J column blocks (8 boxes
-//     of 16 columns, 128-byte swizzle) through a 6-stage mbarrier ring
+//     producer streams 40×128 row-slabs of the I and J column blocks (8 boxes
+//     of 16 columns, 128-byte swizzle; boxes wholly beyond column K are not
+//     loaded) through a double-buffered mbarrier ring
 //     (cp.async.bulk.tensor, OOB rows/cols zero-filled); consumers run
 //     mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) on 32×32 warp tiles with
 //     fragments read as conflict-free 128-bit shared loads.
 //   * Diagonal tiles skip warp tiles / mma tiles strictly below the diagonal
-//     and edge tiles skip columns >= K; the remaining warp tiles are balanced
-//     over the 4 SM sub-partitions on the host (LPT).
+//     and edge tiles skip columns >= K — through compile-time mma masks (the
+//     few partial shapes that occur), never predicated DMMA; the remaining
+//     warp tiles are balanced over the 4 SM sub-partitions on the host (exact
+//     min-max assignment).
 //   * Each item's partial goes to a workspace in fragment order; a second
 //     kernel sums the S partials of every tile in split order s = 0..S-1 —
 //     fixed order, no atomics on data, bitwise reproducible — and writes the
