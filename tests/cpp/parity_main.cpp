@@ -12,6 +12,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
 #include <functional>
 #include <string>
 #include <vector>
@@ -20,6 +21,7 @@
 #include "dopinf/data.hpp"
 #include "dopinf/errors.hpp"
 #include "dopinf/linalg.hpp"
+#include "dopinf/pipeline.hpp"
 #include "dopinf/pod.hpp"
 #include "dopinf/postprocess.hpp"
 #include "dopinf/rom_search.hpp"
@@ -430,6 +432,104 @@ int main() {
         report(probes_same, "reconstruct_probes bit-identical to postprocess::reconstruct_probes", "11 probes, both runs");
         report(field_same <= 1e-10 && field_chain <= 1e-8, "reconstruct_field vs postprocess::reconstruct_field",
                "same inputs rel " + fmt(field_same) + " <= 1e-10; whole chain rel " + fmt(field_chain) + " <= 1e-8");
+    }
+
+    // 5. Steps I–V from a snapshot file: the reference's own pipeline::run
+    //    (pipeline.cpp:229-398) against the B200 chain on the same SNP1 file —
+    //    file → device (streamed pass) → reference eig → device projection →
+    //    device grid search → device probes → streamed field file.
+    {
+        namespace fs = std::filesystem;
+        const fs::path dir = fs::temp_directory_path() / "dopinf_b200_pipeline";
+        fs::remove_all(dir);
+        fs::create_directories(dir / "ref");
+        fs::create_directories(dir / "b200");
+        synth::QuadraticSpec spec;
+        spec.n_vars = 2;
+        spec.nx = 600;
+        spec.r_true = 3;
+        spec.nt = 200;
+        spec.nt_p = 400;
+        spec.seed = 12;
+        const std::string data = (dir / "data.snp1").string();
+        synth::generate_quadratic(spec, data, (dir / "truth.bin").string());
+
+        pipeline::PipelineConfig cfg;
+        cfg.data_path = data;
+        cfg.workers = 1;
+        cfg.scaling = true;
+        cfg.b1 = rom_search::default_b1();
+        cfg.b2 = rom_search::default_b2();
+        cfg.nt_p = spec.nt_p;
+        cfg.probes = {{0, 5}, {1, 300}, {0, 599}};
+        cfg.out_dir = (dir / "ref").string();
+        const pipeline::RunResult refrun = pipeline::run(cfg);
+
+        // B200: the same stages on the same file
+        const auto hdr = dopinf_b200::data::read_header<data::SnapshotHeader>(data);
+        const std::size_t nx = hdr.nx, nt = hdr.nt, nv = hdr.n_vars, rows = nv * nx;
+        std::vector<double> means(rows), scales(nv);
+        Matrix d(nt, nt);
+        dopinf_b200_block* blk = nullptr;
+        bool ok = dopinf_b200_snapshot_pass_file(g_gpu->handle(), data.c_str(), 0, nx, 1, &blk, means.data(),
+                                                 scales.data(), d.data()) == DOPINF_B200_OK;
+        const pod::EigenSpectrum sp = pod::eig_sym_desc(d);
+        const std::size_t r = pod::select_rank(sp.eigenvalues, cfg.energy).r;
+        const Matrix tr = pod::reduced_map(sp, r);
+        const Matrix qhat = dopinf_b200::pod::project(tr, d);
+        rom_search::SearchOutcome out;
+        comm::run_on_workers(1, [&](comm::Comm& c) {
+            dopinf_b200::Bind bind(*g_gpu);
+            out = dopinf_b200::rom_search::grid_search<rom_search::SearchOutcome>(
+                qhat, rom_search::SearchConfig{cfg.b1, cfg.b2, cfg.max_growth, spec.nt_p}, c);
+        });
+        ok = ok && r == refrun.r && out.pair_opt == refrun.pair_opt;
+        const double err_gap = std::abs(out.train_err - refrun.train_err) / std::max(refrun.train_err, 1e-4);
+        // probes (files <probe>.bin written by the reference: raw doubles)
+        std::vector<std::size_t> pv, pi;
+        for (const auto& p : cfg.probes) {
+            pv.push_back(p.var);
+            pi.push_back(p.index);
+        }
+        std::vector<double> series(cfg.probes.size() * spec.nt_p);
+        std::vector<int> owned(cfg.probes.size());
+        ok = ok && dopinf_b200_reconstruct_probes(blk, tr.data(), r, out.trajectory.data(), spec.nt_p, pv.data(),
+                                                  pi.data(), pv.size(), means.data(), scales.data(), 1,
+                                                  series.data(), owned.data()) == DOPINF_B200_OK;
+        // field file (pipeline.cpp:330-350) streamed by the device
+        std::string names;
+        for (const auto& n : hdr.var_names) names += n + std::string(1, '\0');
+        const std::string field_b200 = (dir / "b200" / "field_rank0.snp1").string();
+        ok = ok && dopinf_b200_write_field(blk, tr.data(), r, out.trajectory.data(), spec.nt_p, means.data(),
+                                           scales.data(), 1, names.data(), field_b200.c_str()) == DOPINF_B200_OK;
+        dopinf_b200_block_destroy(blk);
+        const data::SnapshotHeader fh_ref = data::read_header((dir / "ref" / "field_rank0.snp1").string());
+        const data::SnapshotHeader fh_b200 = data::read_header(field_b200);
+        ok = ok && fh_ref.n_vars == fh_b200.n_vars && fh_ref.nx == fh_b200.nx && fh_ref.nt == fh_b200.nt &&
+             fh_ref.var_names == fh_b200.var_names;
+        const data::PartitionPlan one = data::partition_rows(fh_ref.nx, 1);
+        const Matrix fr = data::read_block((dir / "ref" / "field_rank0.snp1").string(), one, 0, fh_ref).values;
+        const Matrix fg = data::read_block(field_b200, one, 0, fh_b200).values;
+        const double field_gap = rel_frob(fg, fr);
+        // device probe series against the reference field's rows (the numbers its probe files hold)
+        double probe_gap = 0.0;
+        {
+            for (std::size_t k = 0; k < cfg.probes.size(); ++k) {
+                const std::size_t row = cfg.probes[k].var * nx + cfg.probes[k].index;
+                double num = 0.0, den = 0.0;
+                for (std::size_t t = 0; t < spec.nt_p; ++t) {
+                    const double a = series[k * spec.nt_p + t], b = fr(row, t);
+                    num += (a - b) * (a - b);
+                    den += b * b;
+                }
+                probe_gap = std::max(probe_gap, std::sqrt(num / den));
+            }
+        }
+        ok = ok && err_gap <= 1e-8 && field_gap <= 1e-8 && probe_gap <= 1e-8;
+        report(ok, "Steps I-V from a snapshot file vs pipeline::run",
+               "r = " + std::to_string(r) + ", same pair; train_err gap " + fmt(err_gap) + ", field file rel " +
+                   fmt(field_gap) + ", probes rel " + fmt(probe_gap) + " <= 1e-8");
+        fs::remove_all(dir);
     }
 
     std::printf("parity: %s\n", g_fail == 0 ? "all checks passed" : "FAILURES");
