@@ -99,8 +99,12 @@ GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r
     const std::pair<size_t, size_t> mine(pb, pe);
     const size_t np = mine.second - mine.first;
     const size_t per_pair = static_cast<size_t>(D) * D + static_cast<size_t>(D) * r + nt_p * r;
-    const size_t batch = std::max<size_t>(1, std::min<size_t>(std::max<size_t>(np, 1),
-                                                               (size_t(8) << 30) / (per_pair * sizeof(double))));
+    size_t batch = std::max<size_t>(1, std::min<size_t>(std::max<size_t>(np, 1),
+                                                         (size_t(8) << 30) / (per_pair * sizeof(double))));
+    if (const char* env = std::getenv("DOPINF_B200_GRID_BATCH")) {  // test knob: pairs per batch
+        const long long v = std::atoll(env);
+        if (v > 0) batch = std::min<size_t>(batch, static_cast<size_t>(v));
+    }
     std::string err;
     int* info = c->rom_info.get<int>(2 * batch, "potrf info");
     double* betas = c->rom_betas.get<double>(2 * batch, "betas");

@@ -162,3 +162,16 @@ def test_grid_search_large_system_fallback(ctx, oracle, reference):
     assert out.pair_opt == pair_w
     assert err_close(out.train_err, err_w)
     assert rel(out.trajectory, traj_w) <= ROM_TOL
+
+
+def test_grid_search_batches_agree(ctx, oracle, monkeypatch):
+    # pairs solved / integrated / scored in several batches (8 GB cap at large r;
+    # forced here with the DOPINF_B200_GRID_BATCH knob): same winner, same bits
+    a = api()
+    q = _qhat(oracle, 5, 60, seed=77)
+    cfg = a.SearchConfig(list(np.logspace(-8, 0, 4)), list(np.logspace(-3, 3, 3)), 1.2, 120)
+    one = a.grid_search(q, cfg, ctx)
+    monkeypatch.setenv("DOPINF_B200_GRID_BATCH", "5")
+    five = a.grid_search(q, cfg, ctx)
+    assert five.pair_opt == one.pair_opt and five.train_err == one.train_err
+    assert np.array_equal(five.trajectory, one.trajectory)
