@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from conftest import rel_frob
+from _helpers import oracle_pass
 
 pytestmark = pytest.mark.gpu
 
@@ -335,3 +336,32 @@ def test_external_stream_context(ctx):
     assert np.array_equal(p1.local_means, p2.local_means) and np.array_equal(d1, d2)
     ext.close()
     s.synchronize()  # the caller's stream outlives the context
+
+
+@pytest.mark.parametrize("case", list(range(30)))
+def test_random_shapes_against_oracle(ctx, oracle, case):
+    # seeded random shapes around the tile / chunk / warp-tile boundaries: the fused
+    # pass (transform bit-identical, Gram <= 1e-12) and the projection (bit-identical)
+    a = api()
+    rng = np.random.default_rng(1000 + case)
+    nv = int(rng.integers(1, 5))
+    nx = int(rng.choice([1, 2, 7, 63, 64, 65, 127, 129, 500, 4097]))
+    nt = int(rng.choice([2, 3, 8, 15, 16, 17, 33, 127, 128, 129, 200, 257]))
+    if nt == 1 or nx * nv == 0:
+        return
+    scaling = bool(rng.integers(2))
+    q = rng.standard_normal((nv * nx, nt)) * rng.uniform(1e-3, 1e3) + rng.uniform(-10, 10)
+    if scaling and nt >= 2:
+        q[:, 0] += 1.0  # no variable constant in time
+    b = a.LocalBlock(ctx, nv, a.RowRange(0, nx), nt, values=q)
+    params, d = a.snapshot_pass(b, scaling)
+    full, means, scales, od = oracle_pass(oracle, q, nv, nx, 1, scaling)
+    assert np.array_equal(params.local_means, means)
+    if scaling:
+        assert np.array_equal(params.scales, scales)
+    assert np.array_equal(b.values, full)
+    assert rel_frob(d, od) <= GRAM_TOL
+    assert np.array_equal(d, d.T)
+    r = int(rng.integers(1, nt + 1))
+    tr = rng.standard_normal((nt, r))
+    assert np.array_equal(a.project(tr, d, ctx), oracle.project(tr, d))
