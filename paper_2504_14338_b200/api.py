@@ -3,14 +3,20 @@
 Same names, argument meaning and error behaviour as the reference functions
 (paths relative to /root/reference/proj):
 
-  data::partition_rows            data.hpp:47,  data.cpp:86-103
+  data::partition_rows / read_header / read_block / write_snapshots
+                                  data.hpp:47-55,      data.cpp:86-202
   transform::center_in_place      transform.hpp:27,    transform.cpp:10-20
   transform::compute_global_scales transform.hpp:32-34, transform.cpp:22-41
   transform::scale_in_place       transform.hpp:37,    transform.cpp:43-49
   pod::local_gram / global_gram   pod.hpp:28-31,       pod.cpp:11-18
+  pod::eig_sym_desc / reduced_map pod.hpp:34-47,       pod.cpp:20-101 (device)
   pod::project                    pod.hpp:49,          pod.cpp:103-105
+  rom_search::grid_search / integrate / distribute_pairs
+                                  rom_search.hpp:45-91, rom_search.cpp:60-262
   postprocess::basis_rows         postprocess.hpp:25,  postprocess.cpp:12-34
-  reconstruct_field's Φ_r         postprocess.cpp:66
+  postprocess::reconstruct_probes / reconstruct_field
+                                  postprocess.hpp:37-45, postprocess.cpp:36-70
+  (fused) snapshot_pass / snapshot_pass_host / snapshot_pass_file / write_field
 
 Blocks live on the GPU (`LocalBlock` is device resident; `.values` downloads).
 The reference's comm::Comm argument is the per-rank `DeviceContext`, whose
