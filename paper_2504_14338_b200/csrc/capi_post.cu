@@ -256,7 +256,8 @@ struct FieldOperands {
     const double* means = nullptr;
     const double* scales = nullptr;
     size_t nt_p = 0;
-    int r_pad = 0;
+    int r_pad = 0;  // pitch of Φ_r and Q̃ on the device
+    int k_ext = 0;  // contraction extent: r rounded up to the DMMA k-step of 4 (columns ≥ r are zero)
 };
 
 FieldOperands field_operands(dopinf_b200_block* b, const double* qtilde, size_t r, size_t nt_p, int r_pad,
@@ -265,6 +266,7 @@ FieldOperands field_operands(dopinf_b200_block* b, const double* qtilde, size_t 
     FieldOperands f;
     f.nt_p = nt_p;
     f.r_pad = r_pad;
+    f.k_ext = static_cast<int>((r + 3) / 4 * 4);
     double* dqt = c->field_qt.get<double>(nt_p * r_pad, "qtilde");
     ck(cudaMemsetAsync(dqt, 0, nt_p * r_pad * sizeof(double), c->stream), "memset");
     ck(cudaMemcpy2DAsync(dqt, r_pad * sizeof(double), qtilde, r * sizeof(double), r * sizeof(double), nt_p,
@@ -293,9 +295,9 @@ void do_field_rows(dopinf_b200_block* b, const FieldOperands& f, long long row0,
     auto* c = b->ctx;
     const int slab = field::max_r_pad();
     const double* phi = static_cast<const double*>(b->phi.p) + static_cast<size_t>(row0) * f.r_pad;
-    for (int k0 = 0; k0 < f.r_pad; k0 += slab) {
-        const int w = std::min(slab, f.r_pad - k0);
-        const bool last = k0 + w == f.r_pad;
+    for (int k0 = 0; k0 < f.k_ext; k0 += slab) {
+        const int w = std::min(slab, f.k_ext - k0);
+        const bool last = k0 + w == f.k_ext;
         ck(field::launch_field(phi + k0, f.r_pad, f.qt + k0, f.r_pad, nrows, static_cast<int>(f.nt_p), w,
                                last && f.means ? f.means + row0 : nullptr, last ? f.scales : nullptr,
                                static_cast<long long>(b->nx_i), row0, out, ldo, k0 > 0 ? 1 : 0, c->num_sms,

@@ -14,7 +14,9 @@
 // CTA tile 128 rows × 64 times, 8 warps of 32×32. The CTA's Φ_r tile (128 × r)
 // stays in shared memory while the CTA walks its group of 64-wide time chunks;
 // the chunks of Q̃ (64 × r, L2-resident: nt_p·r·8 bytes) stream through a
-// two-slot cp.async ring. Operand rows are padded to a pitch P ≡ 8 (mod 16)
+// TMA ring. The kernel is instantiated per contraction extent RP = r rounded
+// up to 4 (a last k-step of four when RP ≡ 4 mod 8), so no DMMA multiplies
+// padding. Operand rows are padded to a pitch P ≡ 8 (mod 16)
 // doubles so each quarter-warp's 128-bit fragment loads hit 8 distinct 16-byte
 // bank groups (conflict-free). Work items = (row tile, chunk group), strided
 // over a persistent grid.
@@ -30,7 +32,16 @@ namespace {
 constexpr int THREADS = 256;  // 8 warps: 4 (rows) × 2 (times), 32×32 each
 constexpr int kMaxPitch = 104;  // r_pad ≤ 96 keeps Φ tile + 2 Q̃ slots ≤ 213 KB
 
-__host__ __device__ constexpr int pitch_for(int r_pad) { return r_pad % 16 == 8 ? r_pad : r_pad + 8; }
+// Shared-memory pitch of a row of RP doubles: the smallest P ≥ RP with
+// P ≡ 8 (mod 16), so each quarter-warp's 128-bit fragment loads hit 8
+// distinct 16-byte bank groups.
+__host__ __device__ constexpr int pitch_for(int rp) { return rp + ((8 - rp % 16) + 16) % 16; }
+
+__device__ __forceinline__ double lds64(uint32_t saddr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(saddr));
+    return v;
+}
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
@@ -153,7 +164,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
 #pragma unroll
-                for (int k8 = 0; k8 < RP; k8 += 8) {
+                for (int k8 = 0; k8 + 8 <= RP; k8 += 8) {
                     const uint32_t ko = static_cast<uint32_t>(k8 * sizeof(double));
                     double2 a[4], b[2];
 #pragma unroll
@@ -172,6 +183,21 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
                         for (int j = 0; j < 2; ++j)
                             dmma_8x8x4(acc[mi][2 * h + j][0], acc[mi][2 * h + j][1], a[mi].y, b[j].y);
+                }
+                if constexpr (RP % 8 == 4) {  // a last k-step of four: lane (g, t) takes k = RP − 4 + t
+                    const uint32_t at = as_u + static_cast<uint32_t>(((wm * 32 + g) * P + RP - 4 + t) * sizeof(double));
+                    const uint32_t bt = bs_u + slot * kSlotBytes +
+                                        static_cast<uint32_t>(((wn * 32 + g) * P + RP - 4 + t) * sizeof(double));
+                    double a[4], b[2];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) a[i] = lds64(at + i * step8);
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) b[j] = lds64(bt + (2 * h + j) * step8);
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            dmma_8x8x4(acc[mi][2 * h + j][0], acc[mi][2 * h + j][1], a[mi], b[j]);
                 }
             }
             // every DMMA above consumed its shared-memory operands (scoreboard), so
@@ -274,28 +300,40 @@ cudaError_t launch_rp(const double* phi, size_t ldphi, const double* qt, size_t 
 }  // namespace
 
 cudaError_t launch_field(const double* phi, size_t ldphi, const double* qt, size_t ldq, long long rows, int nt_p,
-                         int r_pad, const double* means, const double* scales, long long nx_i, long long row_base,
+                         int k_ext, const double* means, const double* scales, long long nx_i, long long row_base,
                          double* out, size_t ldo, int accumulate, int num_sms, cudaStream_t stream) {
     if (rows <= 0 || nt_p <= 0) return cudaSuccess;
-    if (r_pad % 8 != 0 || r_pad < 8 || r_pad > max_r_pad() || ldo % 2 != 0 || ldphi % 2 != 0 || ldq % 2 != 0) {
+    if (k_ext % 4 != 0 || k_ext < 4 || k_ext > max_r_pad() || ldo % 2 != 0 || ldphi % 2 != 0 || ldq % 2 != 0) {
         return cudaErrorInvalidValue;
     }
 #define DOPINF_FIELD(RP) \
-    case RP / 8:         \
+    case RP / 4:         \
         return launch_rp<RP>(phi, ldphi, qt, ldq, rows, nt_p, means, scales, nx_i, row_base, out, ldo, accumulate, \
                              num_sms, stream)
-    switch (r_pad / 8) {
+    switch (k_ext / 4) {
+        DOPINF_FIELD(4);
         DOPINF_FIELD(8);
+        DOPINF_FIELD(12);
         DOPINF_FIELD(16);
+        DOPINF_FIELD(20);
         DOPINF_FIELD(24);
+        DOPINF_FIELD(28);
         DOPINF_FIELD(32);
+        DOPINF_FIELD(36);
         DOPINF_FIELD(40);
+        DOPINF_FIELD(44);
         DOPINF_FIELD(48);
+        DOPINF_FIELD(52);
         DOPINF_FIELD(56);
+        DOPINF_FIELD(60);
         DOPINF_FIELD(64);
+        DOPINF_FIELD(68);
         DOPINF_FIELD(72);
+        DOPINF_FIELD(76);
         DOPINF_FIELD(80);
+        DOPINF_FIELD(84);
         DOPINF_FIELD(88);
+        DOPINF_FIELD(92);
         default: DOPINF_FIELD(96);
     }
 #undef DOPINF_FIELD
