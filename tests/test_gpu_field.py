@@ -62,6 +62,25 @@ def test_field_matches_reference(ctx, oracle, reference, nv, nx, nt, r, nt_p, sc
     assert rel(phi, oracle.matmul(b.values, tr)) <= 1e-12
 
 
+def test_field_every_contraction_extent(ctx, oracle):
+    """r = 1…200: every kernel instantiation (extents 4…96 in steps of 4, the
+    4-wide k tail for extents ≡ 4 mod 8) and every k-slab split, against the
+    C oracle's restatement of reconstruct_field."""
+    a = api()
+    nv, nx, nt, nt_p = 2, 150, 208, 70
+    rng = oracle.rng(5)
+    raw = rng.matrix(nv * nx, nt) * np.repeat(10.0 ** np.arange(nv), nx)[:, None] + 1.5
+    b = a.LocalBlock(ctx, nv, a.RowRange(0, nx), nt, values=raw)
+    params, _ = a.snapshot_pass(b, True)
+    q = b.values
+    trs, qts = rng.matrix(nt, 200) * 0.1, rng.matrix(nt_p, 200)
+    for r in list(range(1, 101)) + [131, 157, 192, 200]:
+        tr, qt = np.ascontiguousarray(trs[:, :r]), np.ascontiguousarray(qts[:, :r])
+        field = a.reconstruct_field(b, tr, qt, params)
+        want = oracle.reconstruct_field(q, tr, qt, params.local_means, params.scales, nx, True)
+        assert rel(field, want) <= FIELD_TOL, r
+
+
 def test_field_device_t_r_and_device_output(ctx, oracle, reference):
     a = api()
     nv, nx, nt, r, nt_p = 2, 3000, 128, 12, 256
