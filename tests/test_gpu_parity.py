@@ -365,3 +365,42 @@ def test_random_shapes_against_oracle(ctx, oracle, case):
     r = int(rng.integers(1, nt + 1))
     tr = rng.standard_normal((nt, r))
     assert np.array_equal(a.project(tr, d, ctx), oracle.project(tr, d))
+
+
+# ---- acceptance.cpp:351-419 (criterion 2): partition invariance on the device ------------
+@pytest.mark.parametrize("p", [1, 2, 4, 7])
+def test_partition_invariance(ctx, oracle, p):
+    """The p ranks of partition_rows run one after another on this GPU through
+    the stage API (center_in_place → compute_global_scales → scale_in_place →
+    local_gram); the MAX and SUM collectives are done on the host in ascending
+    rank order (comm_inprocess.cpp:101-112). Transformed rows are bit-identical
+    to the unpartitioned oracle's, the summed Gram within the Gram tolerance."""
+    a = api()
+    nv, nx, nt = 3, 1001, 72
+    rng = np.random.default_rng(23)
+    q = rng.standard_normal((nv * nx, nt)) * np.repeat([1e-3, 1.0, 1e4], nx)[:, None] + 5.0
+    oq, _ = oracle.center(q)
+    os_, _ = oracle.reduce_scales(oracle.local_maxabs(oq, nv, nx)[None, :])
+    oq = oracle.scale(oq, nv, nx, os_)
+    header = a.SnapshotHeader(nv, nx, nt, ["a", "b", "c"])
+    blocks, local_scales = [], []
+    for rr in a.partition_rows(nx, p):
+        rows = np.concatenate([q[v * nx + rr.begin:v * nx + rr.end] for v in range(nv)])
+        b = a.LocalBlock(ctx, nv, rr, nt, values=rows)
+        a.center_in_place(b)
+        local_scales.append(a.compute_global_scales(b, header))
+        blocks.append((rr, b))
+    scales = np.max(np.stack(local_scales), axis=0)
+    assert np.array_equal(scales, os_)
+    d = None
+    for rr, b in blocks:
+        a.scale_in_place(b, scales)
+        got = b.values
+        for v in range(nv):
+            want = oq[v * nx + rr.begin:v * nx + rr.end]
+            assert np.array_equal(got[v * rr.count():(v + 1) * rr.count()], want)
+        g = a.local_gram(b)
+        d = g if d is None else d + g
+        b.close()
+    assert np.array_equal(d, d.T)
+    assert rel_frob(d, oracle.gram(oq)) <= GRAM_TOL
