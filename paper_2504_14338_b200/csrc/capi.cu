@@ -68,12 +68,20 @@ void run_stats(dopinf_b200_block* b, bool center) {
     c->record(DOPINF_B200_STAGE_STATS, 1);
 }
 
-void do_center(dopinf_b200_block* b, double* means_host) {
+void do_center(dopinf_b200_block* b, double* means_host, bool side_copy) {
     materialize(b);  // a second centering acts on centered values, as in the reference
     run_stats(b, true);
     b->pending_center = true;
     b->stats_valid = true;
-    if (means_host) {
+    if (means_host && side_copy && is_pinned(means_host)) {
+        // the means leave on the copy stream while the scales, apply and Gram
+        // run; the caller joins the copy stream before returning
+        auto* c = b->ctx;
+        ck(cudaStreamWaitEvent(c->copy_stream, c->ev[DOPINF_B200_STAGE_STATS][1], 0), "wait stats");
+        ck(cudaMemcpyAsync(means_host, b->means.get<double>(b->rows, "means"), b->rows * sizeof(double),
+                           cudaMemcpyDeviceToHost, c->copy_stream),
+           "means D2H");
+    } else if (means_host) {
         ck(cudaMemcpyAsync(means_host, b->means.get<double>(b->rows, "means"), b->rows * sizeof(double),
                            cudaMemcpyDeviceToHost, b->ctx->stream),
            "means D2H");
@@ -852,13 +860,16 @@ int dopinf_b200_snapshot_pass(dopinf_b200_block* b, int scaling, double* means, 
     if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
     auto* c = b->ctx;
     return guarded(c, [&] {
-        if (b->rows > 0) do_center(b, means);
+        struct JoinCopies {  // also on failure: no copy into the caller's means outlives the call
+            cudaStream_t s;
+            ~JoinCopies() { cudaStreamSynchronize(s); }
+        } join{c->copy_stream};
+        if (b->rows > 0) do_center(b, means, true);
+        std::vector<double> s(b->n_vars);  // outlives the async scales upload (synced below)
         if (scaling) {
-            std::vector<double> s(b->n_vars);
             do_global_scales(b, s.data(), nullptr);
             if (scales) std::memcpy(scales, s.data(), s.size() * sizeof(double));
             if (b->rows > 0) do_scale(b, s.data());
-            c->sync("snapshot_pass");  // host scales must outlive the async upload
         }
         do_local_gram(b, nullptr);
         do_global_gram(c, d);

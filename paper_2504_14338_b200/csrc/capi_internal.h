@@ -322,7 +322,7 @@ struct Fd {
 // ---- helpers defined in capi.cu / capi_io.cu --------------------------------
 void materialize(dopinf_b200_block* b);
 void run_stats(dopinf_b200_block* b, bool center);
-void do_center(dopinf_b200_block* b, double* means_host);
+void do_center(dopinf_b200_block* b, double* means_host, bool side_copy = false);
 void do_global_scales(dopinf_b200_block* b, double* scales_host, size_t* degenerate);
 void do_scale(dopinf_b200_block* b, const double* scales_host);
 void copy_d_out(dopinf_b200_ctx* c, double* d_host);

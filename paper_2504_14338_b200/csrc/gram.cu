@@ -270,8 +270,23 @@ __global__ void __launch_bounds__(512)
     const size_t item_stride = static_cast<size_t>(n_tiles) * CONSUMERS * kWarpFragDoubles;
     const double* p = w + static_cast<size_t>(tile) * CONSUMERS * kWarpFragDoubles;
     double2 sum = __ldcg(reinterpret_cast<const double2*>(p));
-    for (int sp = 1; sp < n_splits; ++sp) {
-        const double2 v = __ldcg(reinterpret_cast<const double2*>(p + sp * item_stride));
+    // kReduceBatch loads in flight per thread, then the adds in split order
+    // (the summation order, hence the bits, do not depend on the batching)
+    constexpr int kReduceBatch = 8;
+    int sp = 1;
+    for (; sp + kReduceBatch <= n_splits; sp += kReduceBatch) {
+        double2 v[kReduceBatch];
+#pragma unroll
+        for (int u = 0; u < kReduceBatch; ++u)
+            v[u] = __ldcs(reinterpret_cast<const double2*>(p + (sp + u) * item_stride));
+#pragma unroll
+        for (int u = 0; u < kReduceBatch; ++u) {
+            sum.x += v[u].x;
+            sum.y += v[u].y;
+        }
+    }
+    for (; sp < n_splits; ++sp) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(p + sp * item_stride));
         sum.x += v.x;
         sum.y += v.y;
     }
