@@ -200,7 +200,11 @@ void do_local_gram(dopinf_b200_block* b, double* d_host) {
         ck(gram::launch_gram(c->plan, b->gram_map, tiles, work, counters, c->stream), "gram");
         c->record(DOPINF_B200_STAGE_GRAM, 1);
         c->record(DOPINF_B200_STAGE_GRAM_REDUCE, 0);
-        ck(gram::launch_reduce(c->plan, tiles, work, packed, c->stream), "gram reduce");
+        const int groups = gram::reduce_groups(c->plan, c->num_sms);
+        double* scratch = groups > 1 ? c->reduce_scratch.get<double>(gram::reduce_scratch_doubles(c->plan, groups),
+                                                                     "reduce scratch")
+                                     : nullptr;
+        ck(gram::launch_reduce(c->plan, tiles, work, packed, c->stream, groups, scratch), "gram reduce");
         c->record(DOPINF_B200_STAGE_GRAM_REDUCE, 1);
     }
     unpack(c);

@@ -199,7 +199,7 @@ struct dopinf_b200_ctx {
     long long plan_rows = -1;
     gram::Plan plan;
     int tiles_K = -1;
-    DBuf tiles, work, counters, packed, gather, dmat, dhost_in;
+    DBuf tiles, work, counters, packed, gather, dmat, dhost_in, reduce_scratch;
     bool counters_zeroed = false;
     // scratch
     DBuf scales, tr, trt, qhat, sel, rows_out, span;

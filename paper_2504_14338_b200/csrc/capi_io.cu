@@ -166,7 +166,13 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
         ck(gram::launch_gram(plan, map, tiles, work, counters, c->stream, !ch.first_of_var), "gram");
         c->gram_event_pair();
         if (ch.last_of_var) {
-            ck(gram::launch_reduce(first_plan, tiles, work, gv + static_cast<size_t>(ch.var) * count, c->stream),
+            const int groups = gram::reduce_groups(first_plan, c->num_sms);
+            double* scratch =
+                groups > 1 ? c->reduce_scratch.get<double>(gram::reduce_scratch_doubles(first_plan, groups),
+                                                           "reduce scratch")
+                           : nullptr;
+            ck(gram::launch_reduce(first_plan, tiles, work, gv + static_cast<size_t>(ch.var) * count, c->stream,
+                                   groups, scratch),
                "gram reduce");
             if (scaling) {
                 if (c->size > 1) {

@@ -254,11 +254,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-// Fixed-order split-n reduction: block = (tile, warp slot), thread = (mma, lane).
+// Fixed-order split-n reduction: block = (split group, tile, warp slot),
+// thread = (mma, lane). With one group the S partials of a tile are summed in
+// split order and scattered into the packed triangle; with several (few tiles,
+// many splits: the tiles alone cannot fill the GPU) each group's consecutive
+// splits are summed in order into group_out, whose layout is the workspace's
+// with "split" = group, and a second launch with one group sums those in group
+// order. Either way the order is fixed: bitwise reproducible.
 __global__ void __launch_bounds__(512)
     gram_reduce_kernel(const TileInfo* __restrict__ tiles, int n_tiles, int n_splits, int K,
-                       const double* __restrict__ work, double* __restrict__ packed) {
-    const int tile = blockIdx.x / CONSUMERS;
+                       const double* __restrict__ work, double* __restrict__ packed, int n_groups,
+                       double* __restrict__ group_out) {
+    const int per_group_blocks = n_tiles * CONSUMERS;
+    const int grp = blockIdx.x / per_group_blocks;
+    const int tile = (blockIdx.x % per_group_blocks) / CONSUMERS;
     const int slot = blockIdx.x % CONSUMERS;
     int wm, wn;
     bool diag;
@@ -266,15 +275,18 @@ __global__ void __launch_bounds__(512)
     decode(tiles[tile].warp[slot], wm, wn, diag, mask);
     const int mma = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
     if (!((mask >> mma) & 1u)) return;
-    const double* w = work + static_cast<size_t>(slot) * kWarpFragDoubles + mma * 64 + lane * 2;
+    const int per = (n_splits + n_groups - 1) / n_groups;
+    const int sp0 = grp * per, sp1 = min(n_splits, sp0 + per);
+    if (sp0 >= sp1) return;
+    const size_t frag = static_cast<size_t>(slot) * kWarpFragDoubles + mma * 64 + lane * 2;
     const size_t item_stride = static_cast<size_t>(n_tiles) * CONSUMERS * kWarpFragDoubles;
-    const double* p = w + static_cast<size_t>(tile) * CONSUMERS * kWarpFragDoubles;
-    double2 sum = __ldcg(reinterpret_cast<const double2*>(p));
+    const double* p = work + static_cast<size_t>(tile) * CONSUMERS * kWarpFragDoubles + frag;
+    double2 sum = __ldcg(reinterpret_cast<const double2*>(p + sp0 * item_stride));
     // kReduceBatch loads in flight per thread, then the adds in split order
     // (the summation order, hence the bits, do not depend on the batching)
     constexpr int kReduceBatch = 8;
-    int sp = 1;
-    for (; sp + kReduceBatch <= n_splits; sp += kReduceBatch) {
+    int sp = sp0 + 1;
+    for (; sp + kReduceBatch <= sp1; sp += kReduceBatch) {
         double2 v[kReduceBatch];
 #pragma unroll
         for (int u = 0; u < kReduceBatch; ++u)
@@ -285,10 +297,16 @@ __global__ void __launch_bounds__(512)
             sum.y += v[u].y;
         }
     }
-    for (; sp < n_splits; ++sp) {
+    for (; sp < sp1; ++sp) {
         const double2 v = __ldcs(reinterpret_cast<const double2*>(p + sp * item_stride));
         sum.x += v.x;
         sum.y += v.y;
+    }
+    if (n_groups > 1) {
+        __stcg(reinterpret_cast<double2*>(group_out + grp * item_stride +
+                                          static_cast<size_t>(tile) * CONSUMERS * kWarpFragDoubles + frag),
+               sum);
+        return;
     }
     const int g = lane >> 2, t = lane & 3;
     const int mi = mma >> 2, ni = mma & 3;
@@ -520,11 +538,34 @@ cudaError_t launch_combine_vars(const double* gv, int n_vars, size_t count, cons
     return cudaGetLastError();
 }
 
+int reduce_groups(const Plan& plan, int num_sms) {
+    const long long blocks = static_cast<long long>(plan.n_tiles) * CONSUMERS;
+    const long long want = 4LL * num_sms;
+    if (blocks >= want || plan.n_splits < 16) return 1;
+    const long long g = std::max<long long>(1, std::min<long long>((want + blocks - 1) / blocks, plan.n_splits / 8));
+    // no empty group: ceil(S / ceil(S / g)) groups of ceil(S / g) splits
+    const long long per = (plan.n_splits + g - 1) / g;
+    return static_cast<int>((plan.n_splits + per - 1) / per);
+}
+
+size_t reduce_scratch_doubles(const Plan& plan, int groups) {
+    return groups > 1 ? static_cast<size_t>(groups) * plan.n_tiles * kItemDoubles : 0;
+}
+
 cudaError_t launch_reduce(const Plan& plan, const TileInfo* d_tiles, const double* work,
-                          double* packed, cudaStream_t stream) {
-    gram_reduce_kernel<<<plan.n_tiles * CONSUMERS, 512, 0, stream>>>(d_tiles, plan.n_tiles,
-                                                                      plan.n_splits, plan.K, work,
-                                                                      packed);
+                          double* packed, cudaStream_t stream, int groups, double* scratch) {
+    if (groups > 1 && scratch) {
+        gram_reduce_kernel<<<groups * plan.n_tiles * CONSUMERS, 512, 0, stream>>>(
+            d_tiles, plan.n_tiles, plan.n_splits, plan.K, work, packed, groups, scratch);
+        note_launch();
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        gram_reduce_kernel<<<plan.n_tiles * CONSUMERS, 512, 0, stream>>>(d_tiles, plan.n_tiles, groups, plan.K,
+                                                                          scratch, packed, 1, nullptr);
+    } else {
+        gram_reduce_kernel<<<plan.n_tiles * CONSUMERS, 512, 0, stream>>>(d_tiles, plan.n_tiles, plan.n_splits,
+                                                                          plan.K, work, packed, 1, nullptr);
+    }
     note_launch();
     return cudaGetLastError();
 }

@@ -51,8 +51,12 @@ Plan make_stream_plan(long long chunk_rows, int K, int num_sms, long long split_
 // D = Σ_v gv[v] / scales[v]² (scales == nullptr: Σ_v gv[v]), variables in order.
 cudaError_t launch_combine_vars(const double* gv, int n_vars, size_t count, const double* scales,
                                 double* out, cudaStream_t stream);
+// Split groups for the fixed-order reduction (1 = one pass over all splits;
+// more when the tiles alone would leave most SMs idle) and the scratch they need.
+int reduce_groups(const Plan& plan, int num_sms);
+size_t reduce_scratch_doubles(const Plan& plan, int groups);
 cudaError_t launch_reduce(const Plan& plan, const TileInfo* d_tiles, const double* work,
-                          double* packed, cudaStream_t stream);
+                          double* packed, cudaStream_t stream, int groups = 1, double* scratch = nullptr);
 cudaError_t launch_unpack(const double* packed, int K, double* d, cudaStream_t stream);
 cudaError_t launch_ordered_sum(const double* parts, int p, size_t count, double* out,
                                cudaStream_t stream);

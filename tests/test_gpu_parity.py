@@ -404,3 +404,19 @@ def test_partition_invariance(ctx, oracle, p):
         b.close()
     assert np.array_equal(d, d.T)
     assert rel_frob(d, oracle.gram(oq)) <= GRAM_TOL
+
+
+@pytest.mark.parametrize("rows,nt", [(210003, 7), (150001, 128), (120007, 300)])
+def test_gram_grouped_reduce(ctx, oracle, rows, nt):
+    """Few tiles, many splits: the split-n reduction runs in two fixed-order
+    levels (groups of consecutive splits, then the groups); odd split counts
+    leave a short last group."""
+    a = api()
+    q = np.random.default_rng(rows).standard_normal((rows, nt)) + 1.0
+    b = make_block(ctx, q)
+    _, d = a.snapshot_pass(b, scaling=False)
+    oq, _ = oracle.center(q)
+    assert rel_frob(d, oracle.gram(oq)) <= GRAM_TOL
+    b.upload(q)
+    _, d2 = a.snapshot_pass(b, scaling=False)
+    assert np.array_equal(d, d2) and np.array_equal(d, d.T)
