@@ -80,7 +80,9 @@ __device__ __forceinline__ void decode(uint32_t e, int& wm, int& wn, bool& diag,
 // time so skipped tiles cost nothing (a predicated-off DMMA still occupies
 // the tensor pipe). The partial masks that occur for any K are few:
 // diagonal 0xCCFF, column edge 0x1111/0x3333/0x7777, and their combinations
-// 0x0001/0x0033/0x0477 (enumerated by plan_tiles; kPartialMasks below).
+// 0x0001/0x0033/0x0477; plus the halves plan_tiles cuts from warp tiles of
+// tiles with fewer than 16 active warp tiles (0x3333/0xCCCC, 0x3333/0x4444
+// by columns; 0x0033/0x3300, 0x00CC/0xCC00 by rows).
 template <uint32_t MASK>
 __device__ __forceinline__ void stage_mma(double (&acc)[16][2], const double* __restrict__ as,
                                           const double* __restrict__ bs, int xg0, int xg1, uint32_t mask) {
@@ -116,6 +118,11 @@ __device__ __forceinline__ void stage_mma_any(double (&acc)[16][2], const double
         case 0x0477u: stage_mma<0x0477u>(acc, as, bs, xg0, xg1, mask); break;
         case 0x0033u: stage_mma<0x0033u>(acc, as, bs, xg0, xg1, mask); break;
         case 0x0001u: stage_mma<0x0001u>(acc, as, bs, xg0, xg1, mask); break;
+        case 0xCCCCu: stage_mma<0xCCCCu>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x4444u: stage_mma<0x4444u>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x3300u: stage_mma<0x3300u>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x00CCu: stage_mma<0x00CCu>(acc, as, bs, xg0, xg1, mask); break;
+        case 0xCC00u: stage_mma<0xCC00u>(acc, as, bs, xg0, xg1, mask); break;
         default: stage_mma<0u>(acc, as, bs, xg0, xg1, mask); break;
     }
 }
@@ -394,6 +401,31 @@ std::vector<TileInfo> plan_tiles(int K) {
                     }
                     if (mask) entries.push_back({wm, wn, __builtin_popcount(mask), mask});
                 }
+            }
+            // Diagonal and edge tiles leave warps idle (10 or fewer of 16 active),
+            // and 2-3 warps per SM sub-partition hide the fragment-load latency
+            // poorly: cut the largest warp tiles (≥ 8 mma) into column halves
+            // (mma columns {0,1} / {2,3}; rows {0,1} / {2,3} when no column cut
+            // applies) until every consumer warp has work. Each half is its own
+            // warp slot; the reduction scatters per mma, so halves need nothing else.
+            while (entries.size() < static_cast<size_t>(kConsumerWarps)) {
+                int best = -1;
+                for (int pass = 0; pass < 2 && best < 0; ++pass) {
+                    const uint32_t lo = pass == 0 ? 0x3333u : 0x00FFu, hi = pass == 0 ? 0xCCCCu : 0xFF00u;
+                    for (size_t k = 0; k < entries.size(); ++k) {
+                        const uint32_t m = entries[k].mask;
+                        if (entries[k].cost >= 8 && (m & lo) && (m & hi) &&
+                            (best < 0 || entries[k].cost > entries[best].cost)) {
+                            best = static_cast<int>(k);
+                        }
+                    }
+                    if (best >= 0) {
+                        const Entry e = entries[best];
+                        entries[best] = {e.wm, e.wn, __builtin_popcount(e.mask & lo), e.mask & lo};
+                        entries.push_back({e.wm, e.wn, __builtin_popcount(e.mask & hi), e.mask & hi});
+                    }
+                }
+                if (best < 0) break;
             }
             // Balance the warp tiles over the 4 SM sub-partitions (warp w runs
             // on SMSP w % 4, at most 4 each): exact min-max assignment by a
