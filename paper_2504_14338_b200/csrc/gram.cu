@@ -30,6 +30,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -374,7 +376,7 @@ __global__ void ordered_sum_kernel(const double* __restrict__ parts, int p, size
 // ---------------------------------------------------------------------------
 // Host planning.
 
-std::vector<TileInfo> plan_tiles(int K) {
+std::vector<TileInfo> plan_tiles_uncached(int K) {
     const int nb = (K + BT - 1) / BT;
     std::vector<TileInfo> out;
     for (int I = 0; I < nb; ++I) {
@@ -437,8 +439,23 @@ std::vector<TileInfo> plan_tiles(int K) {
             std::vector<int> cur(n, 0), best_assign(n, 0);
             int load[4] = {0, 0, 0, 0}, used[4] = {0, 0, 0, 0};
             int best_max = 1 << 30;
+            int total = 0;
+            for (const Entry& e : entries) total += e.cost;
+            const int bound = (total + 3) / 4;  // no assignment beats an even split
+            {  // LPT start (at most 4 per SMSP): the search only has to beat it
+                int l[4] = {0, 0, 0, 0}, u[4] = {0, 0, 0, 0};
+                for (int k = 0; k < n; ++k) {
+                    int c = -1;
+                    for (int q = 0; q < 4; ++q)
+                        if (u[q] < 4 && (c < 0 || l[q] < l[c])) c = q;
+                    l[c] += entries[k].cost;
+                    ++u[c];
+                    best_assign[k] = c;
+                }
+                best_max = std::max(std::max(l[0], l[1]), std::max(l[2], l[3]));
+            }
             std::function<void(int, int)> dfs = [&](int k, int cur_max) {
-                if (cur_max >= best_max) return;
+                if (cur_max >= best_max || best_max <= bound) return;
                 if (k == n) {
                     best_max = cur_max;
                     best_assign = cur;
@@ -470,6 +487,17 @@ std::vector<TileInfo> plan_tiles(int K) {
         }
     }
     return out;
+}
+
+// The tile table depends on K only: planned once per K per process (the
+// streamed passes re-plan every chunk).
+std::vector<TileInfo> plan_tiles(int K) {
+    static std::mutex mu;
+    static std::map<int, std::vector<TileInfo>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(K);
+    if (it == cache.end()) it = cache.emplace(K, plan_tiles_uncached(K)).first;
+    return it->second;
 }
 
 Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes) {
