@@ -17,6 +17,7 @@ namespace {
 // into a two-slot ring — the block is never resident (config 4: 403 GB/GPU).
 constexpr long long kStreamChunkRows = 32768;   // rows per H2D chunk (315 MB at K = 1200)
 
+constexpr long long kTailChunkRows = 8192;     // the pass's final chunk is cut to this size
 constexpr long long kStreamSplitRows = 2048;    // rows per Gram item inside a host chunk
 
 constexpr long long kSynthChunkRows = 262144;   // rows per generated chunk (3.1 GB at K = 1500)
@@ -27,6 +28,13 @@ struct StreamChunk {
     int var;
     long long r0, rows;
     bool first_of_var, last_of_var;
+};
+
+// Joins the copy stream when an entry point leaves (also on failure): work a
+// streamed pass left there (the last variable's scaling) is done by then.
+struct SideJoin {
+    cudaStream_t s;
+    ~SideJoin() { cudaStreamSynchronize(s); }
 };
 
 struct StreamSource {
@@ -70,6 +78,17 @@ std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b, long long chu
         for (long long r0 = v0; r0 < v1; r0 += chunk_rows) {
             const long long rows = std::min(chunk_rows, v1 - r0);
             out.push_back({static_cast<int>(v), r0, rows, r0 == v0, r0 + rows == v1});
+        }
+    }
+    // The pass cannot finish before the last chunk has landed and been
+    // processed: cut the final chunk finer so little work trails the last copy.
+    if (!out.empty() && out.back().rows > kTailChunkRows) {
+        const StreamChunk last = out.back();
+        out.pop_back();
+        for (long long r0 = last.r0; r0 < last.r0 + last.rows; r0 += kTailChunkRows) {
+            const long long rows = std::min(kTailChunkRows, last.r0 + last.rows - r0);
+            out.push_back({last.var, r0, rows, last.first_of_var && r0 == last.r0,
+                           last.last_of_var && r0 + rows == last.r0 + last.rows});
         }
     }
     return out;
@@ -185,9 +204,18 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
                 }
                 if (!src.synth) {
                     const long long v0 = static_cast<long long>(ch.var) * static_cast<long long>(b->nx_i);
+                    // the last variable's scaling runs on the copy stream (its copies are all
+                    // done) beside the Gram combine and the downloads; the entry point joins it
+                    cudaStream_t s = c->stream;
+                    if (ch.var + 1 == static_cast<int>(b->n_vars)) {
+                        cudaEvent_t ev = c->chunk_events[chunks.size()];
+                        ck(cudaEventRecord(ev, c->stream), "event");
+                        ck(cudaStreamWaitEvent(c->copy_stream, ev, 0), "event wait");
+                        s = c->copy_stream;
+                    }
                     ck(transform::launch_apply(b->q + v0 * b->ld, b->ld, static_cast<long long>(b->nx_i), K,
                                                static_cast<long long>(b->nx_i), nullptr, ds + ch.var, c->num_sms,
-                                               c->stream),
+                                               s),
                        "scale");
                 }
             }
@@ -393,6 +421,7 @@ int dopinf_b200_snapshot_pass_host(dopinf_b200_block* b, const double* host, siz
     auto* c = b->ctx;
     return guarded(c, [&] {
         require(host_ld >= b->nt && (b->rows == 0 || host), "snapshot_pass_host: bad host buffer");
+        SideJoin join{c->copy_stream};
         StreamSource src;
         src.host = host;
         src.host_ld = host_ld;
@@ -434,6 +463,7 @@ int dopinf_b200_block_read(dopinf_b200_ctx* c, const char* path, size_t row_begi
     *out = nullptr;
     dopinf_b200_block* b = nullptr;
     const int rc = guarded(c, [&] {
+        SideJoin join{c->copy_stream};
         Fd f;
         Snp1 h;
         b = open_file_block(c, path, row_begin, row_end, f, h);
@@ -460,6 +490,7 @@ int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* c, const char* path, size_t 
     *out = nullptr;
     dopinf_b200_block* b = nullptr;
     const int rc = guarded(c, [&] {
+        SideJoin join{c->copy_stream};
         Fd f;
         Snp1 h;
         b = open_file_block(c, path, row_begin, row_end, f, h);
