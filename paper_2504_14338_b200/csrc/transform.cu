@@ -134,9 +134,9 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
 }
 
 // x ← (x − mean[row]) / scale[var]  (or x − mean when scales == nullptr).
-// Warp per row; each lane issues kApplyBatch independent 16-byte loads before
+// Warp per row; each lane issues kApplyBatch (8) independent 16-byte loads before
 // any store (streaming hints: the block is touched once per pass).
-constexpr int kApplyBatch = 4;
+constexpr int kApplyBatch = 8;
 
 template <bool kScale>
 __global__ void __launch_bounds__(256)
