@@ -420,3 +420,44 @@ def test_gram_grouped_reduce(ctx, oracle, rows, nt):
     b.upload(q)
     _, d2 = a.snapshot_pass(b, scaling=False)
     assert np.array_equal(d, d2) and np.array_equal(d, d.T)
+
+
+def test_contexts_in_concurrent_threads(oracle):
+    """The reference runs its ranks as threads (comm_inprocess.cpp:159-178):
+    independent contexts driven from concurrent host threads (ctypes releases
+    the GIL) give the same bits as the same passes run one after another."""
+    import threading
+
+    a = api()
+    rng = np.random.default_rng(77)
+    qs = [rng.standard_normal((2 * 20000, 96)) * (k + 1) + k for k in range(3)]
+    seq = []
+    with a.DeviceContext(0) as c:
+        for q in qs:
+            b = make_block(c, q, 2)
+            p, d = a.snapshot_pass(b, True)
+            seq.append((p.local_means.copy(), p.scales.copy(), d, b.values))
+            b.close()
+    out = [None] * len(qs)
+    errors = []
+
+    def worker(k):
+        try:
+            with a.DeviceContext(0) as c:
+                for _ in range(3):
+                    b = make_block(c, qs[k], 2)
+                    p, d = a.snapshot_pass(b, True)
+                    out[k] = (p.local_means.copy(), p.scales.copy(), d, b.values)
+                    b.close()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(len(qs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for got, want in zip(out, seq):
+        for x, y in zip(got, want):
+            assert np.array_equal(x, y)
