@@ -177,6 +177,12 @@ int dopinf_b200_center(dopinf_b200_block* block, double* means);
  * MAX all-reduced over the ranks. DEGENERATE_VARIABLE when a scale is 0, with
  * *degenerate_var set to the first such variable. scales: host [n_vars]. */
 int dopinf_b200_global_scales(dopinf_b200_block* block, double* scales, size_t* degenerate_var);
+/* The rank-local half of compute_global_scales (transform.cpp:28-31: the
+ * per-variable kernels::max_abs over this block's centered rows) with no
+ * collective and no zero check: for callers that reduce over their own
+ * comm::Comm (transform.cpp:32) — e.g. several in-process ranks sharing one
+ * GPU, each with a size-1 context. maxabs: host [n_vars]. */
+int dopinf_b200_local_maxabs(dopinf_b200_block* block, double* maxabs);
 /* scale_in_place (transform.cpp:43-49): q /= scales[var] (IEEE division). */
 int dopinf_b200_scale(dopinf_b200_block* block, const double* scales);
 

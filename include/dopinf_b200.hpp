@@ -39,6 +39,9 @@
 #include <string>
 #include <type_traits>
 #include <vector>
+#if __cplusplus >= 202002L
+#include <span>
+#endif
 
 #include "dopinf_b200.h"
 
@@ -167,6 +170,37 @@ public:
 private:
     Context* prev_;
 };
+
+namespace detail {
+#if __cplusplus >= 202002L
+// comm::ReduceOp of the caller's Comm (comm.hpp:9: Sum, Max, Min), deduced from
+// its allreduce(std::span<double>, ReduceOp) (comm.hpp:24).
+template <class C, class Op>
+Op reduce_op_of(void (C::*)(std::span<double>, Op));
+template <class CommT>
+using ReduceOpT = decltype(reduce_op_of(&CommT::allreduce));
+constexpr int kSum = 0, kMax = 1;
+
+// Which collectives a stage uses. The bound Context's own (NCCL) when it spans
+// the caller's ranks; the caller's Comm when every rank binds a size-1
+// Context — the reference's in-process ranks (comm_inprocess.cpp:159-178) or
+// MPI ranks sharing fewer GPUs than ranks: each rank runs its local half on
+// the device and the reduction is the reference's own.
+template <class CommT>
+bool host_collectives(CommT& comm, const char* what) {
+    Context& c = ctx();
+    if (comm.size() == c.size() && comm.rank() == c.rank()) return false;
+    if (c.size() == 1) return true;
+    throw CollectiveError(std::string(what) + ": comm does not match the bound device context");
+}
+#else
+template <class CommT>
+bool host_collectives(CommT& comm, const char* what) {
+    if (comm.size() == ctx().size() && comm.rank() == ctx().rank()) return false;
+    throw CollectiveError(std::string(what) + ": comm does not match the bound device context");
+}
+#endif
+}  // namespace detail
 
 // Device mirror of one host LocalBlock (data.hpp:38-42).
 class DeviceBlock {
@@ -305,14 +339,28 @@ std::vector<double> center_in_place(LocalBlockT& block) {
 // transform.cpp:22-41 (MAX all-reduce over NCCL; `comm` must be this rank's).
 template <class LocalBlockT, class HeaderT, class CommT>
 std::vector<double> compute_global_scales(const LocalBlockT& block, const HeaderT& header, CommT& comm) {
-    if (comm.size() != detail::ctx().size() || comm.rank() != detail::ctx().rank()) {
-        throw CollectiveError("compute_global_scales: comm does not match the bound device context");
-    }
+    const bool host = detail::host_collectives(comm, "compute_global_scales");
     const std::size_t n_vars = static_cast<std::size_t>(header.n_vars);
     DeviceBlock d = detail::uploaded(block, n_vars);
     std::vector<double> scales(n_vars);
     std::size_t bad = 0;
-    const int rc = dopinf_b200_global_scales(d.handle(), scales.data(), &bad);
+    int rc = DOPINF_B200_OK;
+    if (host) {
+#if __cplusplus >= 202002L
+        // transform.cpp:28-39: local max-abs, MAX over the caller's Comm, zero check
+        Context::check(dopinf_b200_local_maxabs(d.handle(), scales.data()), d.context().handle(),
+                       "compute_global_scales");
+        comm.allreduce(std::span<double>(scales), static_cast<detail::ReduceOpT<CommT>>(detail::kMax));
+        for (std::size_t j = 0; j < n_vars && rc == DOPINF_B200_OK; ++j) {
+            if (scales[j] == 0.0) {
+                rc = DOPINF_B200_ERR_DEGENERATE_VARIABLE;
+                bad = j;
+            }
+        }
+#endif
+    } else {
+        rc = dopinf_b200_global_scales(d.handle(), scales.data(), &bad);
+    }
     if (rc == DOPINF_B200_ERR_DEGENERATE_VARIABLE) {
         throw DegenerateVariableError("variable '" + header.var_names[bad] +
                                       "' is constant in time; max-abs scaling is undefined");
@@ -345,7 +393,14 @@ auto local_gram(const LocalBlockT& block) -> std::decay_t<decltype(block.values)
 // pod.cpp:15-18: reduces the device copy of the last local Gram of this rank.
 template <class MatrixT, class CommT>
 MatrixT global_gram(MatrixT local, CommT& comm) {
-    if (comm.size() != detail::ctx().size()) throw CollectiveError("global_gram: comm size mismatch");
+    if (detail::host_collectives(comm, "global_gram")) {
+#if __cplusplus >= 202002L
+        // pod.cpp:15-18 verbatim: the caller's Comm sums the local Grams
+        comm.allreduce(std::span<double>(local.data(), local.rows() * local.cols()),
+                       static_cast<detail::ReduceOpT<CommT>>(detail::kSum));
+#endif
+        return local;
+    }
     Context::check(dopinf_b200_global_gram(detail::ctx().handle(), local.data()), detail::ctx().handle(),
                    "global_gram");
     return local;
@@ -396,7 +451,11 @@ namespace rom_search {
 // Context's ranks share the candidates as distribute_pairs does (the comm
 // argument is the reference's and unused: the Context carries the ranks).
 template <class OutcomeT, class MatrixT, class ConfigT, class CommT>
-OutcomeT grid_search(const MatrixT& qhat, const ConfigT& config, CommT& /*comm*/) {
+OutcomeT grid_search(const MatrixT& qhat, const ConfigT& config, CommT& comm) {
+    // With size-1 Contexts under a wider Comm every rank evaluates all pairs
+    // (same winner: the first minimum, as the reference's lowest-rank claim over
+    // contiguous pair ranges) and reports the owner distribute_pairs gives it.
+    const bool host = detail::host_collectives(comm, "grid_search");
     Context& c = detail::ctx();
     std::vector<double> traj(config.nt_p * qhat.rows());
     double pair[2] = {0.0, 0.0}, err = 0.0, secs = 0.0;
@@ -406,6 +465,19 @@ OutcomeT grid_search(const MatrixT& qhat, const ConfigT& config, CommT& /*comm*/
                                                  config.max_growth, config.nt_p, pair, &err, &owner, &secs,
                                                  traj.data()),
                          c.handle());
+    if (host) {  // rom_search.cpp:207 / 236-240: the rank whose pair range holds the winner
+        const std::size_t n2 = config.b2.size(), n_reg = config.b1.size() * n2;
+        std::size_t idx = 0;
+        while (idx < n_reg && !(config.b1[idx / n2] == pair[0] && config.b2[idx % n2] == pair[1])) ++idx;
+        for (int r = 0; r < comm.size(); ++r) {
+            std::size_t b = 0, e = 0;
+            Context::check(dopinf_b200_distribute_pairs(n_reg, r, comm.size(), &b, &e), nullptr, "grid_search");
+            if (idx >= b && idx < e) {
+                owner = r;
+                break;
+            }
+        }
+    }
     OutcomeT out;
     out.pair_opt = {pair[0], pair[1]};
     out.owner_rank = owner;

@@ -65,6 +65,7 @@ SIGNATURES = {
     "dopinf_b200_block_synth_lowrank": (C.c_int, [_vp, C.c_uint64, C.c_int, C.c_double]),
     "dopinf_b200_center": (C.c_int, [_vp, _dp]),
     "dopinf_b200_global_scales": (C.c_int, [_vp, _dp, _sp]),
+    "dopinf_b200_local_maxabs": (C.c_int, [_vp, _dp]),
     "dopinf_b200_scale": (C.c_int, [_vp, _dp]),
     "dopinf_b200_local_gram": (C.c_int, [_vp, _dp]),
     "dopinf_b200_global_gram": (C.c_int, [_vp, _dp]),

@@ -461,6 +461,14 @@ def compute_global_scales(block: LocalBlock, header: SnapshotHeader, comm: Devic
     return scales
 
 
+def local_maxabs(block: LocalBlock) -> np.ndarray:
+    """transform.cpp:28-31: this block's per-variable max |centered q|, no
+    collective and no zero check (the caller reduces over its own comm)."""
+    out = np.empty(block.n_vars, dtype=np.float64)
+    _check(_lib.load().dopinf_b200_local_maxabs(block._h, _lib.dptr(out)), block.ctx, "local_maxabs")
+    return out
+
+
 def scale_in_place(block: LocalBlock, scales) -> None:
     """transform.cpp:43-49: divide each variable's rows by its scale."""
     s = _f64(scales, (block.n_vars,))

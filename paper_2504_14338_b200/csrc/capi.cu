@@ -671,6 +671,24 @@ int dopinf_b200_global_scales(dopinf_b200_block* b, double* scales, size_t* dege
     return guarded(b->ctx, [&] { do_global_scales(b, scales, degenerate_var); });
 }
 
+int dopinf_b200_local_maxabs(dopinf_b200_block* b, double* maxabs) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    return guarded(b->ctx, [&] {
+        require(maxabs != nullptr, "local_maxabs: null output");
+        if (!b->stats_valid) {
+            run_stats(b, false);
+            b->stats_valid = true;
+        }
+        auto* c = b->ctx;
+        std::vector<double> host(b->n_vars);
+        ck(cudaMemcpyAsync(host.data(), b->varmax.get<double>(b->n_vars, "varmax"), b->n_vars * sizeof(double),
+                           cudaMemcpyDeviceToHost, c->stream),
+           "maxabs D2H");
+        c->sync("local_maxabs");
+        std::memcpy(maxabs, host.data(), host.size() * sizeof(double));
+    });
+}
+
 int dopinf_b200_scale(dopinf_b200_block* b, const double* scales) {
     if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
     return guarded(b->ctx, [&] {

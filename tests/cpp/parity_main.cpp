@@ -147,6 +147,59 @@ PassOut pass_b200(const Matrix& raw, std::size_t nv, std::size_t nx, bool scalin
     return o;
 }
 
+// Steps II–III over p in-process ranks (comm::run_on_workers, the reference's
+// own Comm). B200: every rank thread binds its own size-1 device Context on the
+// one GPU; MAX and SUM go over the reference Comm (dopinf_b200.hpp host
+// collectives). Returns each rank's transformed block and rank 0's D.
+struct RanksOut {
+    std::vector<Matrix> q;
+    Matrix d;
+    std::vector<double> scales;
+};
+
+data::LocalBlock rank_block(const Matrix& raw, std::size_t nv, std::size_t nx, const data::RowRange& rr) {
+    data::LocalBlock b;
+    b.row_range = rr;
+    b.values = Matrix(nv * rr.count(), raw.cols());
+    for (std::size_t j = 0; j < nv; ++j)
+        for (std::size_t k = 0; k < rr.count(); ++k)
+            std::copy(raw.row(j * nx + rr.begin + k), raw.row(j * nx + rr.begin + k) + raw.cols(),
+                      b.values.row(j * rr.count() + k));
+    return b;
+}
+
+RanksOut ranks_pass(const Matrix& raw, std::size_t nv, std::size_t nx, int p, bool device) {
+    RanksOut o;
+    o.q.resize(static_cast<std::size_t>(p));
+    const data::PartitionPlan plan = data::partition_rows(nx, p);
+    const data::SnapshotHeader h = header_for(nv, nx, raw.cols());
+    comm::run_on_workers(p, [&](comm::Comm& c) {
+        const std::size_t rank = static_cast<std::size_t>(c.rank());
+        data::LocalBlock b = rank_block(raw, nv, nx, plan[rank]);
+        Matrix d;
+        std::vector<double> scales;
+        if (device) {
+            dopinf_b200::Context ctx(0);  // size 1: the reference Comm carries the ranks
+            dopinf_b200::Bind bind(ctx);
+            dopinf_b200::transform::center_in_place(b);
+            scales = dopinf_b200::transform::compute_global_scales(b, h, c);
+            dopinf_b200::transform::scale_in_place(b, scales);
+            d = dopinf_b200::pod::global_gram(dopinf_b200::pod::local_gram(b), c);
+        } else {
+            transform::center_in_place(b);
+            scales = transform::compute_global_scales(b, h, c);
+            transform::scale_in_place(b, scales);
+            d = pod::global_gram(pod::local_gram(b), c);
+        }
+        o.q[rank] = b.values;
+        if (rank == 0) {
+            o.d = d;
+            o.scales = scales;
+        }
+    });
+    return o;
+}
+
 }  // namespace
 
 int main() {
@@ -171,6 +224,27 @@ int main() {
             detail += "seed " + std::to_string(seed) + " gram " + fmt(e) + "; ";
         }
         report(ok, "transform bit-identical, Gram rel <= 1e-12", detail + "means/scales/block bitwise");
+    }
+
+    // 1b. acceptance.cpp:351-419 (criterion 2) with the reference's own in-process
+    //     Comm: p rank threads on one GPU, each with a size-1 device Context.
+    {
+        bool ok = true;
+        double worst = 0.0;
+        synth::Rng rng(12);
+        const std::size_t nv = 3, nx = 1001, nt = 48;
+        Matrix raw = random_matrix(rng, nv * nx, nt);
+        for (std::size_t i = 0; i < raw.rows(); ++i) raw(i, 0) += static_cast<double>(1 + i / nx) * 10.0;
+        for (int p : {1, 2, 3, 4, 7}) {
+            const RanksOut r = ranks_pass(raw, nv, nx, p, false);
+            const RanksOut g = ranks_pass(raw, nv, nx, p, true);
+            ok = ok && r.scales == g.scales;
+            for (std::size_t k = 0; k < r.q.size(); ++k) ok = ok && r.q[k] == g.q[k];
+            worst = std::max(worst, rel_frob(g.d, r.d));
+        }
+        ok = ok && worst <= 1e-12;
+        report(ok, "in-process ranks p in {1,2,3,4,7} on size-1 contexts (reference Comm)",
+               "scales and every rank's block bitwise; Gram rel " + fmt(worst) + " <= 1e-12");
     }
 
     // 2. Degenerate variable throws the reference class naming it (test_transform.cpp:115-128).

@@ -382,13 +382,12 @@ def test_partition_invariance(ctx, oracle, p):
     oq, _ = oracle.center(q)
     os_, _ = oracle.reduce_scales(oracle.local_maxabs(oq, nv, nx)[None, :])
     oq = oracle.scale(oq, nv, nx, os_)
-    header = a.SnapshotHeader(nv, nx, nt, ["a", "b", "c"])
     blocks, local_scales = [], []
     for rr in a.partition_rows(nx, p):
         rows = np.concatenate([q[v * nx + rr.begin:v * nx + rr.end] for v in range(nv)])
         b = a.LocalBlock(ctx, nv, rr, nt, values=rows)
         a.center_in_place(b)
-        local_scales.append(a.compute_global_scales(b, header))
+        local_scales.append(a.local_maxabs(b))  # the rank-local half; MAX below (transform.cpp:28-32)
         blocks.append((rr, b))
     scales = np.max(np.stack(local_scales), axis=0)
     assert np.array_equal(scales, os_)
@@ -461,3 +460,14 @@ def test_contexts_in_concurrent_threads(oracle):
     for got, want in zip(out, seq):
         for x, y in zip(got, want):
             assert np.array_equal(x, y)
+
+
+def test_local_maxabs_no_zero_check(ctx):
+    """A rank whose rows of a variable are constant in time reports 0 for it
+    (the zero check belongs after the MAX, transform.cpp:33-39)."""
+    a = api()
+    q = np.vstack([np.full((10, 5), 3.0), np.arange(50.0).reshape(10, 5)])
+    b = make_block(ctx, q, 2)
+    a.center_in_place(b)
+    m = a.local_maxabs(b)
+    assert m[0] == 0.0 and m[1] == 2.0
