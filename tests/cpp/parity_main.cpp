@@ -416,7 +416,8 @@ int main() {
             for (std::size_t i = 0; i < spec.nx; ++i)
                 for (std::size_t t = 0; t < spec.nt; ++t) raw(v * spec.nx + i, t) = made.variables[v](i, t);
         double traj_gap = 0, err_gap = 0, lam_gap = 0, field_same = 0, field_chain = 0, grid_err = 0, grid_traj = 0;
-        bool grid_pair = true, probes_same = true;
+        bool grid_pair = true, probes_same = true, grid_ranks = true;
+        std::string grid_ranks_detail;
         std::string err_detail;
         bool pair_same = true;
         std::size_t r_ref = 0, r_gpu = 0;
@@ -444,6 +445,24 @@ int main() {
             });
             // the device grid search against the reference's on the same Q̂
             grid_pair = grid_pair && dgp.pair_opt == ogp.pair_opt && dgp.owner_rank == ogp.owner_rank;
+            // and over p in-process ranks sharing the GPU (size-1 contexts, reference Comm):
+            // same pair and the same owner rank as the reference's distribute_pairs split
+            for (int p : {3, 8}) {
+                rom_search::SearchOutcome ref_p, dev_p;
+                comm::run_on_workers(p, [&](comm::Comm& c) {
+                    rom_search::SearchOutcome o = rom_search::grid_search(qg, cfg, c);
+                    if (c.rank() == 0) ref_p = o;
+                });
+                comm::run_on_workers(p, [&](comm::Comm& c) {
+                    dopinf_b200::Context ctx(0);
+                    dopinf_b200::Bind bind(ctx);
+                    rom_search::SearchOutcome o =
+                        dopinf_b200::rom_search::grid_search<rom_search::SearchOutcome>(qg, cfg, c);
+                    if (c.rank() == 0) dev_p = o;
+                });
+                grid_ranks = grid_ranks && dev_p.pair_opt == ref_p.pair_opt && dev_p.owner_rank == ref_p.owner_rank;
+                grid_ranks_detail += "p=" + std::to_string(p) + " owner " + std::to_string(ref_p.owner_rank) + "; ";
+            }
             // train_err is itself a relative error: when it is tiny (1e-5 on the scaled run) its own
             // relative precision is trajectory-rounding / train_err, so it is held to 1e-8
             // relative or 1e-12 absolute, whichever is looser
@@ -500,6 +519,8 @@ int main() {
         report(err_gap <= 1e-10, "pipeline training error (acceptance criterion-2 run)",
                err_detail + "centered run rel <= 1e-10");
         report(traj_gap <= 1e-8, "ROM prediction over 2x horizon", "rel " + fmt(traj_gap) + " <= 1e-8");
+        report(grid_ranks, "device grid_search over in-process ranks p in {3,8}: pair and owner",
+               grid_ranks_detail + "as the reference's distribute_pairs split");
         report(grid_pair && grid_err <= 1e-8 && grid_traj <= 1e-8, "device grid_search vs rom_search::grid_search",
                "same pair and owner; train_err gap / max(err, 1e-4) " + fmt(grid_err) + ", trajectory rel " +
                    fmt(grid_traj) + " <= 1e-8");
