@@ -71,7 +71,7 @@ void file_chunk_h2d(dopinf_b200_block* b, const StreamSource& src, const std::ve
     ck(cudaEventRecord(c->chunk_events[k], c->copy_stream), "event");
 }
 
-std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b, long long chunk_rows) {
+std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b, long long chunk_rows, bool split_tail) {
     std::vector<StreamChunk> out;
     for (size_t v = 0; v < b->n_vars; ++v) {
         const long long v0 = static_cast<long long>(v * b->nx_i), v1 = v0 + static_cast<long long>(b->nx_i);
@@ -80,9 +80,9 @@ std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b, long long chu
             out.push_back({static_cast<int>(v), r0, rows, r0 == v0, r0 + rows == v1});
         }
     }
-    // The pass cannot finish before the last chunk has landed and been
+    // A copied pass cannot finish before the last chunk has landed and been
     // processed: cut the final chunk finer so little work trails the last copy.
-    if (!out.empty() && out.back().rows > kTailChunkRows) {
+    if (split_tail && !out.empty() && out.back().rows > kTailChunkRows) {
         const StreamChunk last = out.back();
         out.pop_back();
         for (long long r0 = last.r0; r0 < last.r0 + last.rows; r0 += kTailChunkRows) {
@@ -110,7 +110,7 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
     b->stats_valid = false;
     c->have_gram = false;
     c->K = K;
-    const std::vector<StreamChunk> chunks = stream_chunks(b, chunk_rows);
+    const std::vector<StreamChunk> chunks = stream_chunks(b, chunk_rows, !src.synth);
     while (c->chunk_events.size() < chunks.size() + 1) {
         cudaEvent_t e;
         ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
@@ -259,7 +259,7 @@ void do_block_read(dopinf_b200_block* b, const StreamSource& src) {
     auto* c = b->ctx;
     b->pending_center = false;
     b->stats_valid = false;
-    const std::vector<StreamChunk> chunks = stream_chunks(b, kStreamChunkRows);
+    const std::vector<StreamChunk> chunks = stream_chunks(b, kStreamChunkRows, false);
     if (chunks.empty()) return;
     while (c->chunk_events.size() < chunks.size() + 1) {
         cudaEvent_t e;
