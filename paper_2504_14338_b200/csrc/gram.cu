@@ -5,8 +5,9 @@
 // kernels::axpy. Here:
 //   * Q (rows × K, row-major, pitch ld) is cut into 128-column blocks; only
 //     output tiles (I, J) with I <= J are computed (K(K+1)/2 useful entries).
-//   * The contraction dimension (rows) is split into S equal chunks; a work
-//     item is (split s, tile). Items are handed out s-major from a global
+//   * The contraction dimension (rows) is split into S chunks (4K rows, the
+//     last ones quartered so the final wave ends together); a work item is
+//     (split s, tile). Items are handed out s-major from a global
 //     atomic queue, so the CTAs running at any moment read the same rows of
 //     Q (L2 reuse across the ~tiles CTAs that need them).
 //   * Each persistent CTA = 1 TMA producer warp + 16 consumer warps. The
@@ -18,13 +19,15 @@
 //     fragments read as conflict-free 128-bit shared loads.
 //   * Diagonal tiles skip warp tiles / mma tiles strictly below the diagonal
 //     and edge tiles skip columns >= K — through compile-time mma masks (the
-//     few partial shapes that occur), never predicated DMMA; the remaining
-//     warp tiles are balanced over the 4 SM sub-partitions on the host (exact
-//     min-max assignment).
+//     few partial shapes that occur), never predicated DMMA; tiles with fewer
+//     than 16 active warp tiles have their largest ones cut in halves so every
+//     consumer warp works, and the warp tiles are balanced over the 4 SM
+//     sub-partitions on the host (exact min-max assignment, planned once per K).
 //   * Each item's partial goes to a workspace in fragment order; a second
-//     kernel sums the S partials of every tile in split order s = 0..S-1 —
-//     fixed order, no atomics on data, bitwise reproducible — and writes the
-//     packed upper triangle. A third kernel expands it to the symmetric K×K
+//     kernel sums the S partials of every tile in split order s = 0..S-1 (in
+//     two fixed levels — groups of consecutive splits, then the groups — when
+//     the tiles alone cannot fill the GPU) — fixed order, no atomics on data,
+//     bitwise reproducible — and writes the packed upper triangle. A third kernel expands it to the symmetric K×K
 //     D (bitwise symmetric, as linalg.hpp:17 promises for the reference).
 #include <algorithm>
 #include <cstdio>
