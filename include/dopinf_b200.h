@@ -28,7 +28,7 @@
  *   pipeline::run_rank read + Steps II-III (pipeline.cpp:254-280)
  *                                                            dopinf_b200_snapshot_pass_file
  *   rom_search::grid_search (rom_search.cpp:185-262)        dopinf_b200_grid_search
- *   rom_search::integrate (rom_search.cpp:60-85)            dopinf_b200_rom_integrate
+ *   rom_search::integrate (rom_search.cpp:62-87)            dopinf_b200_rom_integrate
  *   postprocess::reconstruct_probes (postprocess.cpp:36-61)  dopinf_b200_reconstruct_probes
  *   postprocess::reconstruct_field (postprocess.cpp:63-70)   dopinf_b200_reconstruct_field
  *   Step V field_rank<r>.snp1 output (pipeline.cpp:330-350) dopinf_b200_write_field
@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define DOPINF_B200_ABI_VERSION 1
+#define DOPINF_B200_ABI_VERSION 2
 #define DOPINF_B200_UNIQUE_ID_BYTES 128
 
 typedef enum dopinf_b200_status {
@@ -74,11 +74,13 @@ typedef enum dopinf_b200_reduce_op {
 } dopinf_b200_reduce_op;
 
 /* How the K×K Gram partials of the ranks are combined (pod.cpp:15-18).
- * ORDERED: ncclAllGather of the packed upper triangles, then a device sum in
+ * NCCL (default): one ncclAllReduce(Sum) of the packed upper triangle over
+ * NVLink — the north star's single all-reduce, and the reference's MPI
+ * backend (comm_mpi.cpp:44-47, MPI_Allreduce); identical on every rank.
+ * ORDERED: ncclAllGather of the packed triangles, then a device sum in
  * ascending rank order — the reduction order of the reference's in-process
  * backend (comm_inprocess.cpp:101-112), bitwise reproducible for a fixed rank
- * count regardless of NCCL's algorithm choice. NCCL: ncclAllReduce(Sum) of
- * the packed triangle (half the bytes of ORDERED at p=2, fewer beyond). */
+ * count regardless of NCCL's algorithm choice. */
 typedef enum dopinf_b200_gram_reduce {
     DOPINF_B200_GRAM_REDUCE_ORDERED = 0,
     DOPINF_B200_GRAM_REDUCE_NCCL = 1
@@ -103,6 +105,15 @@ typedef enum dopinf_b200_stage {
     DOPINF_B200_STAGE_COUNT = 14
 } dopinf_b200_stage;
 
+/* dopinf_b200_ctx_create_ex flags. */
+#define DOPINF_B200_CTX_NCCL 1u /* an NCCL communicator even at size 1: the collective
+                                 * code paths run (and are testable) on one GPU */
+
+/* dopinf_b200_debug_inject faults (test support). */
+#define DOPINF_B200_INJECT_STALL 1 /* the next collective is followed on the stream by a
+                                    * device stall the library releases only when it
+                                    * aborts: drives the timeout → abort → poison path */
+
 typedef struct dopinf_b200_ctx dopinf_b200_ctx;
 typedef struct dopinf_b200_block dopinf_b200_block;
 
@@ -126,14 +137,48 @@ int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* 
  * Rank and size come from the communicator. Neither is destroyed with the
  * context; the caller keeps them alive until dopinf_b200_ctx_destroy. */
 int dopinf_b200_ctx_create_external(int device, void* nccl_comm, void* stream, dopinf_b200_ctx** out);
+/* ctx_create with flags (DOPINF_B200_CTX_NCCL: create the communicator from
+ * `id` even when size == 1). */
+int dopinf_b200_ctx_create_ex(int device, int rank, int size, const unsigned char* id, unsigned flags,
+                              dopinf_b200_ctx** out);
 void dopinf_b200_ctx_destroy(dopinf_b200_ctx* ctx);
 int dopinf_b200_ctx_rank(const dopinf_b200_ctx* ctx);
 int dopinf_b200_ctx_size(const dopinf_b200_ctx* ctx);
 const char* dopinf_b200_last_error(const dopinf_b200_ctx* ctx);
 int dopinf_b200_set_gram_reduce(dopinf_b200_ctx* ctx, int mode);
-/* Comm::allreduce / barrier (comm.hpp:20-30) on a HOST span, over NCCL. */
+/* Comm::allreduce / barrier (comm.hpp:20-30) on a HOST span, over NCCL;
+ * SUM in ascending rank order (all-gather + ordered device sum). */
 int dopinf_b200_allreduce(dopinf_b200_ctx* ctx, double* data, size_t count, int op);
 int dopinf_b200_barrier(dopinf_b200_ctx* ctx);
+/* Group failure semantics (comm_inprocess.cpp:41-87). Waiting for a queued
+ * collective is bounded by `seconds` (default 60, the reference's kTimeout);
+ * an NCCL asynchronous error or the deadline aborts the communicator
+ * (ncclCommAbort) and poisons the context: that call and every later
+ * collective fail with COLLECTIVE ("collective timed out waiting for peer
+ * ranks"). A rank-local failure inside a fused call (snapshot_pass, the grid
+ * search) is carried to the peers in the collective that follows, which then
+ * fail with COLLECTIVE "rank r aborted" while the failing rank reports its own
+ * error. */
+int dopinf_b200_set_collective_timeout(dopinf_b200_ctx* ctx, double seconds);
+/* verify_uniform (comm_inprocess.cpp:139-151): when enabled, every collective
+ * is preceded by an all-gather of (sequence, count, op) and all ranks fail
+ * with the same COLLECTIVE verdict on a mismatch (debugging aid: one extra
+ * small collective each). */
+int dopinf_b200_set_collective_checks(dopinf_b200_ctx* ctx, int enabled);
+/* 1 when a collective failure has poisoned the context. */
+int dopinf_b200_ctx_poisoned(const dopinf_b200_ctx* ctx);
+/* The agreement rule itself, host only: `table` holds p rows of
+ * (sequence, count, tag) as all-gathered; COLLECTIVE with the reference's
+ * message ("<what>: rank R passed count X, rank S passed count Y") written to
+ * msg when rank `rank` sees a disagreement. */
+int dopinf_b200_check_uniform(const long long* table, int p, int rank, const char* what, char* msg,
+                              size_t msg_cap);
+/* Fault injection for tests (DOPINF_B200_INJECT_*; 0 clears). */
+int dopinf_b200_debug_inject(dopinf_b200_ctx* ctx, int what);
+/* The combine step of the ORDERED reduction on the device: out = parts[0] +
+ * parts[1] + ... + parts[p-1] element-wise, left to right (kernels::add in
+ * ascending rank order, comm_inprocess.cpp:101-112). parts: host p x count. */
+int dopinf_b200_ordered_sum(dopinf_b200_ctx* ctx, const double* parts, int p, size_t count, double* out);
 /* Device milliseconds of `stage` in the most recent call that ran it. */
 int dopinf_b200_stage_ms(const dopinf_b200_ctx* ctx, int stage, double* ms);
 /* The context's CUDA stream (cudaStream_t), for callers that interoperate. */
@@ -191,9 +236,12 @@ int dopinf_b200_scale(dopinf_b200_block* block, const double* scales);
  * tensor pipe, split-n partials reduced in fixed order; kept on the device
  * and, when d != NULL, written to the host as the full symmetric nt x nt. */
 int dopinf_b200_local_gram(dopinf_b200_block* block, double* d);
-/* global_gram (pod.cpp:15-18): reduces the context's local Gram over the
- * ranks (identical on every rank) and optionally writes it to the host. */
-int dopinf_b200_global_gram(dopinf_b200_ctx* ctx, double* d);
+/* global_gram (pod.cpp:15-18): the SUM over the ranks of the context's last
+ * local Gram (its device copy; nt must be its size, else INVALID_ARGUMENT),
+ * identical on every rank, optionally written to the host (d: nt x nt). Like
+ * the reference's pure function it can be repeated: each call reduces the
+ * same local partial. Fails after set_gram (no local partial). */
+int dopinf_b200_global_gram(dopinf_b200_ctx* ctx, double* d, size_t nt);
 /* project (pod.cpp:103-105): Q̂ = T_rᵀ D with the context's device D;
  * tr is host nt x r (NULL: the device T_r of dopinf_b200_reduced_map),
  * qhat host r x nt. */
@@ -297,7 +345,7 @@ int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* ctx, const char* path, size_
  * pair_opt[2] = {beta1, beta2}, train_err, owner, rom_seconds (device time of
  * the integration launch), trajectory nt_p x r. Errors as the reference:
  * InvalidArgumentError, SolveError, NoAdmissiblePairError (same messages). */
-/* rom_search::distribute_pairs (rom_search.cpp:147-160): the contiguous slice
+/* rom_search::distribute_pairs (rom_search.cpp:136-149): the contiguous slice
  * [*begin, *end) of n_reg candidates owned by `rank` of `size` (remainder to
  * the last rank; ranks beyond n_reg get empty slices). Host only. */
 int dopinf_b200_distribute_pairs(size_t n_reg, int rank, int size, size_t* begin, size_t* end);
@@ -305,7 +353,7 @@ int dopinf_b200_grid_search(dopinf_b200_ctx* ctx, const double* qhat, size_t r, 
                             size_t n1, const double* b2, size_t n2, double max_growth, size_t nt_p,
                             double* pair_opt, double* train_err, int* owner, double* rom_seconds,
                             double* trajectory);
-/* rom_search::integrate (rom_search.cpp:60-85): q_{k+1} = A q_k + F quad(q_k) + c
+/* rom_search::integrate (rom_search.cpp:62-87): q_{k+1} = A q_k + F quad(q_k) + c
  * from q0 for n_steps rows (row 0 = q0), bit-identical to the reference for
  * the same operators. a: r x r, f: r x r(r+1)/2, c: r, q0: r (host);
  * traj: host n_steps x r; finite: 1 iff every entry is finite. */

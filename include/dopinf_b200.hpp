@@ -401,8 +401,9 @@ MatrixT global_gram(MatrixT local, CommT& comm) {
 #endif
         return local;
     }
-    Context::check(dopinf_b200_global_gram(detail::ctx().handle(), local.data()), detail::ctx().handle(),
-                   "global_gram");
+    if (local.rows() != local.cols()) throw InvalidArgumentError("global_gram: local Gram is not square");
+    Context::check(dopinf_b200_global_gram(detail::ctx().handle(), local.data(), local.rows()),
+                   detail::ctx().handle(), "global_gram");
     return local;
 }
 

@@ -26,6 +26,8 @@ ERR_DATA_FORMAT = 10
 ERR_NO_ADMISSIBLE_PAIR = 11
 
 SUM, MAX, MIN = 0, 1, 2
+CTX_NCCL = 1
+INJECT_STALL = 1
 GRAM_REDUCE_ORDERED, GRAM_REDUCE_NCCL = 0, 1
 
 STAGES = ["upload", "stats", "scales", "apply", "gram", "gram_reduce", "allreduce", "unpack",
@@ -44,6 +46,14 @@ SIGNATURES = {
     "dopinf_b200_get_unique_id": (C.c_int, [C.c_char_p]),
     "dopinf_b200_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
     "dopinf_b200_ctx_create_external": (C.c_int, [C.c_int, _vp, _vp, C.POINTER(_vp)]),
+    "dopinf_b200_ctx_create_ex": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_uint, C.POINTER(_vp)]),
+    "dopinf_b200_set_collective_timeout": (C.c_int, [_vp, C.c_double]),
+    "dopinf_b200_set_collective_checks": (C.c_int, [_vp, C.c_int]),
+    "dopinf_b200_ctx_poisoned": (C.c_int, [_vp]),
+    "dopinf_b200_check_uniform": (C.c_int, [C.POINTER(C.c_longlong), C.c_int, C.c_int, C.c_char_p, C.c_char_p,
+                                            C.c_size_t]),
+    "dopinf_b200_debug_inject": (C.c_int, [_vp, C.c_int]),
+    "dopinf_b200_ordered_sum": (C.c_int, [_vp, _dp, C.c_int, C.c_size_t, _dp]),
     "dopinf_b200_ctx_destroy": (None, [_vp]),
     "dopinf_b200_ctx_rank": (C.c_int, [_vp]),
     "dopinf_b200_ctx_size": (C.c_int, [_vp]),
@@ -68,7 +78,7 @@ SIGNATURES = {
     "dopinf_b200_local_maxabs": (C.c_int, [_vp, _dp]),
     "dopinf_b200_scale": (C.c_int, [_vp, _dp]),
     "dopinf_b200_local_gram": (C.c_int, [_vp, _dp]),
-    "dopinf_b200_global_gram": (C.c_int, [_vp, _dp]),
+    "dopinf_b200_global_gram": (C.c_int, [_vp, _dp, C.c_size_t]),
     "dopinf_b200_project": (C.c_int, [_vp, _dp, C.c_size_t, C.c_size_t, _dp]),
     "dopinf_b200_project_host": (C.c_int, [_vp, _dp, _dp, C.c_size_t, C.c_size_t, _dp]),
     "dopinf_b200_eig_sym_desc": (C.c_int, [_vp, _dp, _dp]),

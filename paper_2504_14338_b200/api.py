@@ -139,6 +139,21 @@ class SnapshotHeader:
             self.var_names = [f"var{j}" for j in range(self.n_vars)]
 
 
+def check_uniform(table, rank: int, what: str = "allreduce") -> None:
+    """verify_uniform's rule (comm_inprocess.cpp:139-151) on an all-gathered
+    table of (sequence, count, tag) rows, through the library: raises
+    CollectiveError with the reference's message on a disagreement."""
+    t = np.ascontiguousarray(table, dtype=np.int64)
+    if t.ndim != 2 or t.shape[1] != 3:
+        raise InvalidArgumentError("check_uniform: table must be p x 3")
+    msg = C.create_string_buffer(512)
+    rc = _lib.load().dopinf_b200_check_uniform(t.ctypes.data_as(C.POINTER(C.c_longlong)), t.shape[0], rank,
+                                               what.encode(), msg, 512)
+    if rc == _lib.ERR_COLLECTIVE:
+        raise CollectiveError(msg.value.decode())
+    _check(rc)
+
+
 def partition_rows(nx: int, p: int) -> list:
     """data.cpp:86-103: floor(nx/p) rows per rank, remainder on the last rank."""
     lib = _lib.load()
@@ -162,15 +177,20 @@ class DeviceContext:
     SUM, MAX, MIN = _lib.SUM, _lib.MAX, _lib.MIN
 
     def __init__(self, device: int = 0, rank: int = 0, size: int = 1, unique_id: bytes | None = None,
-                 gram_reduce: str = "ordered"):
+                 gram_reduce: str = "nccl", nccl: bool = False):
+        """`nccl=True` gives a size-1 context an NCCL communicator too (its own
+        unique id unless one is passed), so every collective code path runs on
+        one GPU."""
         lib = _lib.load()
         h = C.c_void_p()
         uid = None
-        if size > 1:
+        if size > 1 or nccl:
+            if unique_id is None and size == 1:
+                unique_id = DeviceContext.unique_id()
             if unique_id is None or len(unique_id) != _lib.UNIQUE_ID_BYTES:
                 raise InvalidArgumentError("size > 1 needs the rank-0 unique id bytes")
             uid = C.create_string_buffer(bytes(unique_id), _lib.UNIQUE_ID_BYTES)
-        rc = lib.dopinf_b200_ctx_create(device, rank, size, uid, C.byref(h))
+        rc = lib.dopinf_b200_ctx_create_ex(device, rank, size, uid, _lib.CTX_NCCL if nccl else 0, C.byref(h))
         if rc != _lib.OK:
             raise _STATUS.get(rc, Error)(f"ctx_create(device={device}, rank={rank}, size={size}) failed: "
                                          f"{lib.dopinf_b200_status_string(rc).decode()}")
@@ -181,7 +201,7 @@ class DeviceContext:
 
     @classmethod
     def external(cls, device: int = 0, nccl_comm: int | None = None, stream: int | None = None,
-                 gram_reduce: str = "ordered") -> "DeviceContext":
+                 gram_reduce: str = "nccl") -> "DeviceContext":
         """A context on the caller's NCCL communicator / CUDA stream (raw handle
         values; None: one rank / own stream). Rank and size come from the
         communicator; neither handle is destroyed with the context."""
@@ -223,6 +243,29 @@ class DeviceContext:
 
     def barrier(self) -> None:
         _check(_lib.load().dopinf_b200_barrier(self._h), self, "barrier")
+
+    def set_collective_timeout(self, seconds: float) -> None:
+        """Deadline for a queued collective (comm_inprocess.cpp kTimeout = 60 s)."""
+        _check(_lib.load().dopinf_b200_set_collective_timeout(self._h, float(seconds)), self)
+
+    def set_collective_checks(self, enabled: bool) -> None:
+        """verify_uniform (comm_inprocess.cpp:139-151) before every collective."""
+        _check(_lib.load().dopinf_b200_set_collective_checks(self._h, 1 if enabled else 0), self)
+
+    def poisoned(self) -> bool:
+        return bool(_lib.load().dopinf_b200_ctx_poisoned(self._h))
+
+    def debug_inject(self, fault: int) -> None:
+        _check(_lib.load().dopinf_b200_debug_inject(self._h, fault), self)
+
+    def ordered_sum(self, parts) -> np.ndarray:
+        """Device ascending-rank sum of p partials (the ORDERED combine step)."""
+        parts = _f64(parts)
+        p, count = parts.shape
+        out = np.empty(count, dtype=np.float64)
+        _check(_lib.load().dopinf_b200_ordered_sum(self._h, _lib.dptr(parts), p, count, _lib.dptr(out)), self,
+               "ordered_sum")
+        return out
 
     def stage_ms(self, stage: str) -> float:
         v = C.c_double()
@@ -491,7 +534,7 @@ def global_gram(local: np.ndarray | None, comm: DeviceContext) -> np.ndarray:
     d = np.empty((nt, nt), dtype=np.float64) if nt is not None else None
     if d is None:
         raise InvalidArgumentError("global_gram: pass the local Gram returned by local_gram")
-    _check(_lib.load().dopinf_b200_global_gram(comm._h, _lib.dptr(d)), comm, "global_gram")
+    _check(_lib.load().dopinf_b200_global_gram(comm._h, _lib.dptr(d), nt), comm, "global_gram")
     return d
 
 
@@ -615,7 +658,7 @@ def default_b2() -> list:
 
 
 def distribute_pairs(n_reg: int, rank: int, size: int) -> RowRange:
-    """rom_search::distribute_pairs (rom_search.cpp:147-160) through the ABI."""
+    """rom_search::distribute_pairs (rom_search.cpp:136-149) through the ABI."""
     b, e = C.c_size_t(), C.c_size_t()
     _check(_lib.load().dopinf_b200_distribute_pairs(n_reg, rank, size, C.byref(b), C.byref(e)))
     return RowRange(b.value, e.value)
@@ -666,7 +709,7 @@ def grid_search(qhat, config: SearchConfig, comm: DeviceContext, r: int | None =
 
 
 def rom_integrate(ctx: DeviceContext, a, f, c, q0, n_steps: int):
-    """rom_search::integrate (rom_search.cpp:60-85) on the device -> (trajectory, finite)."""
+    """rom_search::integrate (rom_search.cpp:62-87) on the device -> (trajectory, finite)."""
     a, f, c, q0 = _f64(a), _f64(f), _f64(c), _f64(q0)
     r = a.shape[0]
     traj = np.empty((max(n_steps, 0), r), dtype=np.float64)

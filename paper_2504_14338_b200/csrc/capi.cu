@@ -57,7 +57,7 @@ void materialize(dopinf_b200_block* b) {
 
 void run_stats(dopinf_b200_block* b, bool center) {
     auto* c = b->ctx;
-    double* vm = b->varmax.get<double>(b->n_vars, "varmax");
+    double* vm = b->varmax.get<double>(b->n_vars + 1, "varmax");
     double* mn = b->means.get<double>(b->rows, "means");
     c->record(DOPINF_B200_STAGE_STATS, 0);
     ck(cudaMemsetAsync(vm, 0, b->n_vars * sizeof(double), c->stream), "memset");
@@ -88,26 +88,40 @@ void do_center(dopinf_b200_block* b, double* means_host, bool side_copy) {
     }
 }
 
-void do_global_scales(dopinf_b200_block* b, double* scales_host, size_t* degenerate) {
+void do_global_scales(dopinf_b200_block* b, double* scales_host, size_t* degenerate,
+                      const std::optional<Fail>& earlier) {
     auto* c = b->ctx;
-    if (!b->stats_valid) {
-        run_stats(b, false);
-        b->stats_valid = true;
+    const size_t nv = b->n_vars;
+    // varmax carries one status slot after the n_vars maxima: MAX of
+    // (size - rank) over the failed ranks, so the lowest failed rank is size - max
+    double* vm = b->varmax.get<double>(nv + 1, "varmax");
+    double* red = c->scales.get<double>(nv + 1, "scales");
+    std::optional<Fail> own = earlier;
+    if (!own) {
+        own = attempt(c, [&] {
+            if (!b->stats_valid) {
+                run_stats(b, false);
+                b->stats_valid = true;
+            }
+        });
     }
-    double* vm = b->varmax.get<double>(b->n_vars, "varmax");
-    double* red = c->scales.get<double>(b->n_vars, "scales");
     c->record(DOPINF_B200_STAGE_SCALES, 0);
-    if (c->size > 1) {
-        ckn(ncclAllReduce(vm, red, b->n_vars, ncclFloat64, ncclMax, c->comm, c->stream), "allreduce(MAX)");
+    if (coll(c)) {
+        const double flag = own ? static_cast<double>(c->size - c->rank) : 0.0;
+        ck(cudaMemcpyAsync(vm + nv, &flag, sizeof(double), cudaMemcpyHostToDevice, c->stream), "status H2D");
+        coll_allreduce(c, vm, red, nv + 1, ncclFloat64, ncclMax, "allreduce(MAX)");
     } else {
-        ck(cudaMemcpyAsync(red, vm, b->n_vars * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
+        ck(cudaMemcpyAsync(red, vm, nv * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
     }
     c->record(DOPINF_B200_STAGE_SCALES, 1);
-    std::vector<double> host(b->n_vars);
-    ck(cudaMemcpyAsync(host.data(), red, b->n_vars * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+    double* pin = c->small_pinned<double>(nv + 1);
+    pin[nv] = 0.0;
+    ck(cudaMemcpyAsync(pin, red, (coll(c) ? nv + 1 : nv) * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
        "scales D2H");
     c->sync("global_scales");
-    if (scales_host) std::memcpy(scales_host, host.data(), b->n_vars * sizeof(double));
+    const std::vector<double> host(pin, pin + nv + 1);
+    settle(own, host[nv] > 0.0 ? c->size - static_cast<int>(host[nv]) : -1);
+    if (scales_host) std::memcpy(scales_host, host.data(), nv * sizeof(double));
     for (size_t j = 0; j < b->n_vars; ++j) {
         if (host[j] == 0.0) {
             if (degenerate) *degenerate = j;
@@ -119,7 +133,7 @@ void do_global_scales(dopinf_b200_block* b, double* scales_host, size_t* degener
 
 void do_scale(dopinf_b200_block* b, const double* scales_host) {
     auto* c = b->ctx;
-    double* ds = c->scales.get<double>(b->n_vars, "scales");
+    double* ds = c->scales.get<double>(b->n_vars + 1, "scales");
     ck(cudaMemcpyAsync(ds, scales_host, b->n_vars * sizeof(double), cudaMemcpyHostToDevice, c->stream),
        "scales H2D");
     c->record(DOPINF_B200_STAGE_APPLY, 0);
@@ -141,11 +155,10 @@ void copy_d_out(dopinf_b200_ctx* c, double* d_host) {
     c->record(DOPINF_B200_STAGE_DOWNLOAD, 1);
 }
 
-void unpack(dopinf_b200_ctx* c) {
+void unpack(dopinf_b200_ctx* c, const double* packed) {
     const int K = c->K;
     c->record(DOPINF_B200_STAGE_UNPACK, 0);
-    ck(gram::launch_unpack(c->packed.get<double>(gram::packed_count(K), "packed"), K,
-                           c->dmat.get<double>(static_cast<size_t>(K) * K, "D"), c->stream),
+    ck(gram::launch_unpack(packed, K, c->dmat.get<double>(static_cast<size_t>(K) * K, "D"), c->stream),
        "unpack");
     c->record(DOPINF_B200_STAGE_UNPACK, 1);
 }
@@ -173,9 +186,13 @@ void do_local_gram(dopinf_b200_block* b, double* d_host) {
     materialize(b);
     const int K = static_cast<int>(b->nt);
     const long long rows = static_cast<long long>(b->rows);
+    require(rows < (1LL << 31), "local_gram: blocks of 2^31 rows or more are not supported (TMA row coordinate)");
     c->have_gram = false;
+    c->local_valid = false;
     c->K = K;
-    double* packed = c->packed.get<double>(gram::packed_count(K), "packed");
+    // packed triangle + one status slot (0: this rank's partial is valid)
+    double* packed = c->packed.get<double>(gram::packed_count(K) + 1, "packed");
+    ck(cudaMemsetAsync(packed + gram::packed_count(K), 0, sizeof(double), c->stream), "memset");
     if (rows == 0) {
         ck(cudaMemsetAsync(packed, 0, gram::packed_count(K) * sizeof(double), c->stream), "memset");
     } else {
@@ -207,29 +224,59 @@ void do_local_gram(dopinf_b200_block* b, double* d_host) {
         ck(gram::launch_reduce(c->plan, tiles, work, packed, c->stream, groups, scratch), "gram reduce");
         c->record(DOPINF_B200_STAGE_GRAM_REDUCE, 1);
     }
-    unpack(c);
+    unpack(c, packed);
     c->have_gram = true;
+    c->dmat_local = true;
+    c->local_valid = true;
     copy_d_out(c, d_host);
 }
 
-void do_global_gram(dopinf_b200_ctx* c, double* d_host) {
-    if (!c->have_gram) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "global_gram: no local Gram on this context");
+// pod::global_gram: SUM over the ranks of the local partial in `packed` into
+// `gpacked` (the partial stays, so a repeated call gives the same D). A rank
+// whose local step failed (local_failure) still enters the reduction with its
+// status slot set: every rank learns the lowest failed rank from the summed
+// slot and raises (settle) instead of leaving its peers to the deadline.
+void do_global_gram(dopinf_b200_ctx* c, double* d_host, const std::optional<Fail>& local_failure) {
+    if (!local_failure && !c->local_valid) {
+        fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "global_gram: no local Gram on this context");
+    }
     const int K = c->K;
     const size_t count = gram::packed_count(K);
-    if (c->size > 1) {
-        double* packed = c->packed.get<double>(count, "packed");
-        c->record(DOPINF_B200_STAGE_ALLREDUCE, 0);
-        if (c->gram_reduce == DOPINF_B200_GRAM_REDUCE_NCCL) {
-            ckn(ncclAllReduce(packed, packed, count, ncclFloat64, ncclSum, c->comm, c->stream),
-                "allreduce(SUM)");
-        } else {
-            double* parts = c->gather.get<double>(count * c->size, "gather");
-            ckn(ncclAllGather(packed, parts, count, ncclFloat64, c->comm, c->stream), "allgather");
-            ck(gram::launch_ordered_sum(parts, c->size, count, packed, c->stream), "ordered sum");
-        }
-        c->record(DOPINF_B200_STAGE_ALLREDUCE, 1);
-        unpack(c);
+    if (!coll(c)) {
+        if (local_failure) throw *local_failure;
+        if (!c->dmat_local) unpack(c, c->packed.get<double>(count + 1, "packed"));
+        c->have_gram = true;
+        c->dmat_local = true;
+        copy_d_out(c, d_host);
+        return;
     }
+    double* packed = c->packed.get<double>(count + 1, "packed");
+    if (local_failure) {
+        const double bit = failure_bit(c, true);
+        ck(cudaMemsetAsync(packed, 0, count * sizeof(double), c->stream), "memset");
+        ck(cudaMemcpyAsync(packed + count, &bit, sizeof(double), cudaMemcpyHostToDevice, c->stream), "status H2D");
+    } else {
+        // status slot 0 (set by do_local_gram / the streamed pass)
+    }
+    double* out = c->gpacked.get<double>(count + 1, "reduced Gram");
+    c->record(DOPINF_B200_STAGE_ALLREDUCE, 0);
+    if (c->gram_reduce == DOPINF_B200_GRAM_REDUCE_NCCL) {
+        coll_allreduce(c, packed, out, count + 1, ncclFloat64, ncclSum, "allreduce(SUM)");
+    } else {
+        double* parts = c->gather.get<double>((count + 1) * static_cast<size_t>(c->size), "gather");
+        coll_allgather(c, packed, parts, count + 1, ncclFloat64, "allgather");
+        ck(gram::launch_ordered_sum(parts, c->size, count + 1, count + 1, out, c->stream), "ordered sum");
+    }
+    c->record(DOPINF_B200_STAGE_ALLREDUCE, 1);
+    double* pin = c->small_pinned<double>(1);
+    ck(cudaMemcpyAsync(pin, out + count, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "status D2H");
+    c->sync("global_gram");
+    const double status = *pin;
+    c->have_gram = false;
+    settle(local_failure, lowest_failed(status));
+    unpack(c, out);
+    c->have_gram = true;
+    c->dmat_local = false;
     copy_d_out(c, d_host);
 }
 
@@ -378,7 +425,13 @@ extern "C" {
 
 int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* id,
                            dopinf_b200_ctx** out) {
-    if (!out || size < 1 || rank < 0 || rank >= size || (size > 1 && !id)) {
+    return dopinf_b200_ctx_create_ex(device, rank, size, id, 0u, out);
+}
+
+int dopinf_b200_ctx_create_ex(int device, int rank, int size, const unsigned char* id, unsigned flags,
+                              dopinf_b200_ctx** out) {
+    const bool nccl = size > 1 || (flags & DOPINF_B200_CTX_NCCL) != 0;
+    if (!out || size < 1 || rank < 0 || rank >= size || (nccl && !id) || (flags & ~DOPINF_B200_CTX_NCCL)) {
         return DOPINF_B200_ERR_INVALID_ARGUMENT;
     }
     *out = nullptr;
@@ -389,7 +442,7 @@ int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* 
     c->size = size;
     const int rc = guarded(c, [&] {
         init_ctx(c, device, nullptr);
-        if (size > 1) {
+        if (nccl) {
             ncclUniqueId uid;
             std::memcpy(&uid, id, sizeof uid);
             ckn(ncclCommInitRank(&c->comm, size, uid, rank), "ncclCommInitRank");
@@ -421,13 +474,14 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
-    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->stream) join_stream(c, c->stream);
     if (c->comm && c->owns_comm) ncclCommDestroy(c->comm);
+    if (c->stall_flag) cudaFreeHost(c->stall_flag);
     for (auto& pair : c->ev) {
         if (pair[0]) cudaEventDestroy(pair[0]);
         if (pair[1]) cudaEventDestroy(pair[1]);
     }
-    for (DBuf* b : {&c->tiles, &c->work, &c->counters, &c->packed, &c->gather, &c->dmat, &c->dhost_in,
+    for (DBuf* b : {&c->tiles, &c->work, &c->counters, &c->packed, &c->gpacked, &c->coll_scratch, &c->gather, &c->dmat, &c->dhost_in,
                     &c->scales, &c->tr, &c->trt, &c->qhat, &c->sel, &c->rows_out, &c->span, &c->eig_a,
                     &c->eig_w, &c->eig_work, &c->eig_info, &c->eig_v, &c->eig_lambda, &c->tr_dev, &c->field_qt,
                     &c->field_means, &c->field_scales, &c->field_ring, &c->rom_qhat, &c->rom_dhat, &c->rom_q2t,
@@ -437,6 +491,7 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
         b->release();
     }
     c->staging.release();
+    c->coll_host.release();
     c->file_ring.release();
     c->gv.release();
     c->ring.release();
@@ -444,7 +499,7 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
     for (cudaEvent_t e : c->chunk_events2) cudaEventDestroy(e);
     for (cudaEvent_t e : c->timing_events) cudaEventDestroy(e);
     if (c->copy_stream) {
-        cudaStreamSynchronize(c->copy_stream);
+        join_stream(c, c->copy_stream);
         cudaStreamDestroy(c->copy_stream);
     }
     if (c->stream && c->owns_stream) cudaStreamDestroy(c->stream);
@@ -472,21 +527,22 @@ int dopinf_b200_allreduce(dopinf_b200_ctx* c, double* data, size_t count, int op
     return guarded(c, [&] {
         require(op >= DOPINF_B200_SUM && op <= DOPINF_B200_MIN, "allreduce: unknown op");
         require(count == 0 || data, "allreduce: null data");
-        if (c->size == 1 || count == 0) return;
+        if (!coll(c) || count == 0) return;
         double* buf = c->span.get<double>(count * (op == DOPINF_B200_SUM ? c->size + 1 : 1), "span");
         ck(cudaMemcpyAsync(buf, data, count * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
         if (op == DOPINF_B200_SUM) {
             // Ascending-rank order, as the reference's in-process backend sums.
             double* parts = buf + count;
-            ckn(ncclAllGather(buf, parts, count, ncclFloat64, c->comm, c->stream), "allgather");
-            ck(gram::launch_ordered_sum(parts, c->size, count, buf, c->stream), "ordered sum");
+            coll_allgather(c, buf, parts, count, ncclFloat64, "allreduce");
+            ck(gram::launch_ordered_sum(parts, c->size, count, count, buf, c->stream), "ordered sum");
         } else {
-            ckn(ncclAllReduce(buf, buf, count, ncclFloat64, op == DOPINF_B200_MAX ? ncclMax : ncclMin,
-                              c->comm, c->stream),
-                "allreduce");
+            coll_allreduce(c, buf, buf, count, ncclFloat64, op == DOPINF_B200_MAX ? ncclMax : ncclMin,
+                           "allreduce");
         }
-        ck(cudaMemcpyAsync(data, buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        double* pin = c->small_pinned<double>(count);
+        ck(cudaMemcpyAsync(pin, buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
         c->sync("allreduce");
+        std::memcpy(data, pin, count * sizeof(double));
     });
 }
 
@@ -541,13 +597,15 @@ int dopinf_b200_block_create(dopinf_b200_ctx* c, size_t n_vars, size_t nx_i, siz
         b->nt = nt;
         b->ld = (nt + 1) / 2 * 2;  // 16-byte rows for TMA and 128-bit accesses
         b->rows = n_vars * nx_i;
+        require(b->rows < (size_t(1) << 31), "block_create: blocks of 2^31 rows or more are not supported "
+                                             "(TMA row coordinates are 32-bit); shard over more ranks");
         if (b->rows > 0) {
             ck(cudaMalloc(&b->q, b->rows * b->ld * sizeof(double)), "block values");
             if (b->ld != nt) {
                 ck(cudaMemsetAsync(b->q, 0, b->rows * b->ld * sizeof(double), c->stream), "memset");
             }
         }
-        b->varmax.get<double>(n_vars, "varmax");
+        b->varmax.get<double>(n_vars + 1, "varmax");  // + the status slot of the MAX collective
         c->sync("block_create");
     });
     if (rc != DOPINF_B200_OK) {
@@ -681,7 +739,7 @@ int dopinf_b200_local_maxabs(dopinf_b200_block* b, double* maxabs) {
         }
         auto* c = b->ctx;
         std::vector<double> host(b->n_vars);
-        ck(cudaMemcpyAsync(host.data(), b->varmax.get<double>(b->n_vars, "varmax"), b->n_vars * sizeof(double),
+        ck(cudaMemcpyAsync(host.data(), b->varmax.get<double>(b->n_vars + 1, "varmax"), b->n_vars * sizeof(double),
                            cudaMemcpyDeviceToHost, c->stream),
            "maxabs D2H");
         c->sync("local_maxabs");
@@ -706,8 +764,12 @@ int dopinf_b200_local_gram(dopinf_b200_block* b, double* d) {
     });
 }
 
-int dopinf_b200_global_gram(dopinf_b200_ctx* c, double* d) {
+int dopinf_b200_global_gram(dopinf_b200_ctx* c, double* d, size_t nt) {
     return guarded(c, [&] {
+        require(c->local_valid, "global_gram: no local Gram on this context");
+        require(nt == static_cast<size_t>(c->K),
+                "global_gram: local Gram is " + std::to_string(c->K) + " x " + std::to_string(c->K) +
+                    ", caller passed nt = " + std::to_string(nt));
         do_global_gram(c, d);
         c->sync("global_gram");
     });
@@ -742,6 +804,8 @@ int dopinf_b200_set_gram(dopinf_b200_ctx* c, const double* d, size_t nt) {
            "D H2D");
         c->K = static_cast<int>(nt);
         c->have_gram = true;
+        c->local_valid = false;  // D is the caller's: no local partial to reduce
+        c->dmat_local = false;
         c->eig_K = 0;
         c->tr_dev_r = 0;
         c->sync("set_gram");
@@ -883,18 +947,27 @@ int dopinf_b200_snapshot_pass(dopinf_b200_block* b, int scaling, double* means, 
     auto* c = b->ctx;
     return guarded(c, [&] {
         struct JoinCopies {  // also on failure: no copy into the caller's means outlives the call
-            cudaStream_t s;
-            ~JoinCopies() { cudaStreamSynchronize(s); }
-        } join{c->copy_stream};
-        if (b->rows > 0) do_center(b, means, true);
+            dopinf_b200_ctx* c;
+            ~JoinCopies() { join_stream(c, c->copy_stream); }
+        } join{c};
+        // Rank-local steps that fail still enter the collective that follows,
+        // whose status slot tells the peers (attempt / settle).
+        std::optional<Fail> own = attempt(c, [&] {
+            if (b->rows > 0) do_center(b, means, true);
+        });
         std::vector<double> s(b->n_vars);  // outlives the async scales upload (synced below)
         if (scaling) {
-            do_global_scales(b, s.data(), nullptr);
+            do_global_scales(b, s.data(), nullptr, own);  // settles `own` across the ranks
             if (scales) std::memcpy(scales, s.data(), s.size() * sizeof(double));
-            if (b->rows > 0) do_scale(b, s.data());
+            own.reset();
         }
-        do_local_gram(b, nullptr);
-        do_global_gram(c, d);
+        if (!own) {
+            own = attempt(c, [&] {
+                if (scaling && b->rows > 0) do_scale(b, s.data());
+                do_local_gram(b, nullptr);
+            });
+        }
+        do_global_gram(c, d, own);
         c->sync("snapshot_pass");
     });
 }

@@ -1,0 +1,268 @@
+// capi_coll.cu — the collective layer of the C ABI: every NCCL call of the
+// library goes through here, so the reference group semantics hold for all of
+// them (paths relative to /root/reference/proj):
+//
+//   * a deadline on every wait for a queued collective (comm_inprocess.cpp:
+//     50-63, kTimeout = 60 s): while the stream holds an unfinished
+//     collective, sync() polls it together with ncclCommGetAsyncError; an
+//     asynchronous NCCL error or the deadline aborts the communicator
+//     (ncclCommAbort) and poisons the context, so this and every later
+//     collective call fails with CollectiveError (comm_inprocess.cpp:66-78);
+//   * optional (count, op) agreement before each collective
+//     (verify_uniform, comm_inprocess.cpp:139-151): the ranks all-gather
+//     (sequence, count, tag) and every rank reaches the same verdict and
+//     message;
+//   * rank-local failures ahead of a collective ride in a status slot of the
+//     collective's own buffer (attempt/settle in capi_internal.h), so peers
+//     raise CollectiveError "rank r aborted" instead of waiting out the
+//     deadline (comm_inprocess.cpp:171).
+#include "capi_internal.h"
+
+#include <chrono>
+
+namespace dopinf_b200 {
+namespace capi {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+// Debug stall behind an injected collective: spins until the host releases
+// the flag (the abort path does) or `max_ns` passes, so it can never outlive
+// its test by more than the bound.
+__global__ void stall_kernel(volatile int* flag, unsigned long long max_ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(20000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (*flag == 0 && t - t0 < max_ns);
+}
+
+// Tags of verify_uniform: the op for an all-reduce, the root for a broadcast.
+constexpr long long kTagAllgather = 100, kTagBroadcast = 200;
+
+long long reduce_tag(ncclRedOp_t op, ncclDataType_t type) {
+    return static_cast<long long>(op) + 16LL * static_cast<long long>(type);
+}
+
+[[noreturn]] void poison_and_fail(dopinf_b200_ctx* c, const std::string& msg) {
+    if (!c->poisoned) {
+        c->poisoned = true;
+        c->poison_msg = msg;
+    }
+    fail(DOPINF_B200_ERR_COLLECTIVE, msg);
+}
+
+// ncclCommAbort: NCCL kernels waiting on absent peers exit, the communicator
+// is gone (also one handed in by ctx_create_external — it is unusable after a
+// hang); the stream then drains (bounded wait).
+void abort_comm(dopinf_b200_ctx* c) {
+    // an injected stall is not an NCCL kernel: release it first, since the
+    // abort waits for the device work NCCL cannot flag
+    if (c->stall_flag) *reinterpret_cast<volatile int*>(c->stall_flag) = 1;
+    if (c->comm) {
+        ncclCommAbort(c->comm);
+        c->comm = nullptr;
+    }
+    const auto t0 = Clock::now();
+    while (cudaStreamQuery(c->stream) == cudaErrorNotReady &&
+           Clock::now() - t0 < std::chrono::seconds(20)) {
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+    cudaGetLastError();
+    c->coll_pending = false;
+}
+
+void before(dopinf_b200_ctx* c, size_t count, long long tag, const char* what);
+
+void issued(dopinf_b200_ctx* c) {
+    c->coll_pending = true;
+    ++c->coll_seq;
+    if (c->inject == DOPINF_B200_INJECT_STALL) {
+        c->inject = 0;
+        if (!c->stall_flag) {
+            void* p = nullptr;
+            ck(cudaHostAlloc(&p, sizeof(int), cudaHostAllocMapped), "stall flag");
+            c->stall_flag = static_cast<int*>(p);
+        }
+        *reinterpret_cast<volatile int*>(c->stall_flag) = 0;
+        int* dflag = nullptr;
+        ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dflag), c->stall_flag, 0), "stall flag");
+        const double bound_s = c->coll_timeout_s + 30.0;
+        stall_kernel<<<1, 1, 0, c->stream>>>(dflag, static_cast<unsigned long long>(bound_s * 1e9));
+        note_launch();
+        ck(cudaGetLastError(), "stall");
+    }
+}
+
+// comm_inprocess.cpp:139-151 over NCCL: all-gather (sequence, count, tag).
+void before(dopinf_b200_ctx* c, size_t count, long long tag, const char* what) {
+    if (c->poisoned) fail(DOPINF_B200_ERR_COLLECTIVE, c->poison_msg);
+    if (!c->coll_checks) return;
+    const int p = c->size;
+    long long mine[3] = {c->coll_seq, static_cast<long long>(count), tag};
+    auto* dev = c->coll_scratch.get<long long>(3 * (static_cast<size_t>(p) + 1), "collective check");
+    long long* pin = c->small_pinned<long long>(3 * static_cast<size_t>(p) + 3);
+    std::memcpy(pin, mine, sizeof mine);
+    ck(cudaMemcpyAsync(dev, pin, sizeof mine, cudaMemcpyHostToDevice, c->stream), "check H2D");
+    const ncclResult_t r = ncclAllGather(dev, dev + 3, 3, ncclInt64, c->comm, c->stream);
+    if (r != ncclSuccess) poison_and_fail(c, std::string(what) + ": " + ncclGetErrorString(r));
+    c->coll_pending = true;
+    ck(cudaMemcpyAsync(pin + 3, dev + 3, 3 * static_cast<size_t>(p) * sizeof(long long), cudaMemcpyDeviceToHost,
+                       c->stream),
+       "check D2H");
+    c->sync(what);
+    const std::vector<long long> table(pin + 3, pin + 3 + 3 * static_cast<size_t>(p));
+    char msg[512];
+    if (dopinf_b200_check_uniform(table.data(), p, c->rank, what, msg, sizeof msg) != DOPINF_B200_OK) {
+        // every rank holds the same table, so every rank poisons with the same verdict
+        if (!c->poisoned) {
+            c->poisoned = true;
+            c->poison_msg = std::string(what) + ": ranks disagree on buffer shape or operation";
+        }
+        fail(DOPINF_B200_ERR_COLLECTIVE, msg);
+    }
+}
+
+}  // namespace
+
+void coll_allreduce(dopinf_b200_ctx* c, const void* send, void* recv, size_t count, ncclDataType_t type,
+                    ncclRedOp_t op, const char* what) {
+    before(c, count, reduce_tag(op, type), what);
+    const ncclResult_t r = ncclAllReduce(send, recv, count, type, op, c->comm, c->stream);
+    if (r != ncclSuccess) poison_and_fail(c, std::string(what) + ": " + ncclGetErrorString(r));
+    issued(c);
+}
+
+void coll_allgather(dopinf_b200_ctx* c, const void* send, void* recv, size_t count, ncclDataType_t type,
+                    const char* what) {
+    before(c, count, kTagAllgather, what);
+    const ncclResult_t r = ncclAllGather(send, recv, count, type, c->comm, c->stream);
+    if (r != ncclSuccess) poison_and_fail(c, std::string(what) + ": " + ncclGetErrorString(r));
+    issued(c);
+}
+
+void coll_broadcast(dopinf_b200_ctx* c, void* buf, size_t count, ncclDataType_t type, int root, const char* what) {
+    before(c, count, kTagBroadcast + root, what);
+    const ncclResult_t r = ncclBroadcast(buf, buf, count, type, root, c->comm, c->stream);
+    if (r != ncclSuccess) poison_and_fail(c, std::string(what) + ": " + ncclGetErrorString(r));
+    issued(c);
+}
+
+void join_stream(dopinf_b200_ctx* c, cudaStream_t s) {
+    if (!c->poisoned) {
+        cudaStreamSynchronize(s);
+        return;
+    }
+    const auto t0 = Clock::now();
+    while (cudaStreamQuery(s) == cudaErrorNotReady && Clock::now() - t0 < std::chrono::seconds(20)) {
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+    cudaGetLastError();
+}
+
+}  // namespace capi
+}  // namespace dopinf_b200
+
+void dopinf_b200_ctx::sync(const char* what) {
+    if (!coll_pending) {
+        ck(cudaStreamSynchronize(stream), what);
+        return;
+    }
+    // A collective is queued: poll the stream and the communicator until the
+    // deadline (spin briefly first: most collectives finish within microseconds).
+    const auto t0 = Clock::now();
+    const auto deadline = t0 + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(coll_timeout_s));
+    for (long long it = 0;; ++it) {
+        const cudaError_t e = cudaStreamQuery(stream);
+        if (e == cudaSuccess) {
+            coll_pending = false;
+            return;
+        }
+        if (e != cudaErrorNotReady) ck(e, what);
+        if (comm) {
+            ncclResult_t st = ncclSuccess;
+            if (ncclCommGetAsyncError(comm, &st) == ncclSuccess && st != ncclSuccess && st != ncclInProgress) {
+                const std::string msg = std::string(what) + ": NCCL asynchronous error: " + ncclGetErrorString(st);
+                abort_comm(this);
+                poison_and_fail(this, msg);
+            }
+        }
+        const auto now = Clock::now();
+        if (now >= deadline) {
+            abort_comm(this);
+            poison_and_fail(this, "collective timed out waiting for peer ranks");
+        }
+        if (now - t0 < std::chrono::milliseconds(2)) {
+            std::this_thread::yield();
+        } else {
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+}
+
+extern "C" {
+
+int dopinf_b200_check_uniform(const long long* table, int p, int rank, const char* what, char* msg,
+                              size_t msg_cap) {
+    if (!table || p < 1 || rank < 0 || rank >= p) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    const std::string w = what ? what : "collective";
+    const long long* mine = table + 3 * static_cast<size_t>(rank);
+    std::string m;
+    for (int r = 0; r < p && m.empty(); ++r) {
+        const long long* t = table + 3 * static_cast<size_t>(r);
+        if (t[0] != mine[0]) {
+            m = w + ": ranks are out of step (rank " + std::to_string(rank) + " is at collective " +
+                std::to_string(mine[0]) + ", rank " + std::to_string(r) + " at " + std::to_string(t[0]) + ")";
+        } else if (t[1] != mine[1] || t[2] != mine[2]) {
+            // comm_inprocess.cpp:145-148
+            m = w + ": rank " + std::to_string(rank) + " passed count " + std::to_string(mine[1]) + ", rank " +
+                std::to_string(r) + " passed count " + std::to_string(t[1]);
+            if (t[1] == mine[1]) m += " (operations differ)";
+        }
+    }
+    if (m.empty()) return DOPINF_B200_OK;
+    if (msg && msg_cap > 0) {
+        const size_t n = std::min(m.size(), msg_cap - 1);
+        std::memcpy(msg, m.data(), n);
+        msg[n] = '\0';
+    }
+    return DOPINF_B200_ERR_COLLECTIVE;
+}
+
+int dopinf_b200_set_collective_timeout(dopinf_b200_ctx* c, double seconds) {
+    return guarded(c, [&] {
+        require(seconds > 0.0, "set_collective_timeout: seconds must be positive");
+        c->coll_timeout_s = seconds;
+    });
+}
+
+int dopinf_b200_set_collective_checks(dopinf_b200_ctx* c, int enabled) {
+    return guarded(c, [&] { c->coll_checks = enabled != 0; });
+}
+
+int dopinf_b200_ctx_poisoned(const dopinf_b200_ctx* c) { return c && c->poisoned ? 1 : 0; }
+
+int dopinf_b200_debug_inject(dopinf_b200_ctx* c, int what) {
+    return guarded(c, [&] {
+        require(what == 0 || what == DOPINF_B200_INJECT_STALL, "debug_inject: unknown fault");
+        require(what == 0 || c->comm, "debug_inject: the context has no NCCL communicator");
+        c->inject = what;
+    });
+}
+
+int dopinf_b200_ordered_sum(dopinf_b200_ctx* c, const double* parts, int p, size_t count, double* out) {
+    return guarded(c, [&] {
+        require(p >= 1 && (count == 0 || (parts && out)), "ordered_sum: bad arguments");
+        if (count == 0) return;
+        const size_t n = static_cast<size_t>(p) * count;
+        double* dev = c->span.get<double>(n + count, "span");
+        ck(cudaMemcpyAsync(dev, parts, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "parts H2D");
+        ck(gram::launch_ordered_sum(dev, p, count, count, dev + n, c->stream), "ordered sum");
+        ck(cudaMemcpyAsync(out, dev + n, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        c->sync("ordered_sum");
+    });
+}
+
+}  // extern "C"

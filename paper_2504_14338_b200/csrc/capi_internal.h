@@ -22,6 +22,7 @@
 #include <limits>
 #include <mutex>
 #include <new>
+#include <optional>
 #include <set>
 #include <string>
 #include <thread>
@@ -189,21 +190,46 @@ struct dopinf_b200_ctx {
     }
     ncclComm_t comm = nullptr;
     bool owns_comm = true, owns_stream = true;  // false: handed in by dopinf_b200_ctx_create_external
-    int gram_reduce = DOPINF_B200_GRAM_REDUCE_ORDERED;
+    int gram_reduce = DOPINF_B200_GRAM_REDUCE_NCCL;
     std::string err;
+
+    // Collectives (capi_coll.cu). Every NCCL call goes through coll_*: a
+    // poisoned context refuses them, an optional (count, op) agreement check
+    // runs first, and sync() waits for a queued collective with a deadline
+    // (ncclCommGetAsyncError polled; on expiry ncclCommAbort + poison), the
+    // reference's group semantics (comm_inprocess.cpp:41-87).
+    double coll_timeout_s = 60.0;    // comm_inprocess.cpp kTimeout
+    bool coll_checks = false;        // verify_uniform (comm_inprocess.cpp:139-151) before each collective
+    bool coll_pending = false;       // an NCCL op is queued on `stream` since the last completed sync
+    bool poisoned = false;
+    std::string poison_msg;
+    long long coll_seq = 0;          // collectives issued (agreement checks compare it across ranks)
+    int inject = 0;                  // dopinf_b200_debug_inject (one-shot)
+    int* stall_flag = nullptr;       // host-mapped release flag of an injected stall
+    DBuf coll_scratch;
 
     // Gram state
     int K = 0;                 // nt of the Gram held on the device
-    bool have_gram = false;
+    bool have_gram = false;    // dmat holds a Gram (local, reduced or set_gram)
+    bool local_valid = false;  // packed holds this rank's local partial (K(K+1)/2 + status slot)
+    bool dmat_local = false;   // dmat is the unpacked local partial
     int plan_K = -1;
     long long plan_rows = -1;
     gram::Plan plan;
     int tiles_K = -1;
-    DBuf tiles, work, counters, packed, gather, dmat, dhost_in, reduce_scratch;
+    DBuf tiles, work, counters, packed, gpacked, gather, dmat, dhost_in, reduce_scratch;
     bool counters_zeroed = false;
     // scratch
     DBuf scales, tr, trt, qhat, sel, rows_out, span;
     PinnedBuf staging;
+    // Pinned landing zone for the small results of collectives: a D2H into
+    // pageable memory would block the host until the stream drains, i.e.
+    // outside sync()'s deadline.
+    PinnedBuf coll_host;
+    template <class T>
+    T* small_pinned(size_t count) {
+        return static_cast<T*>(coll_host.get(std::max<size_t>(count * sizeof(T), 64)));
+    }
     // device eigensolve (dopinf_b200_eig_sym_desc / dopinf_b200_reduced_map)
     eig::Solver solver;
     DBuf eig_a, eig_w, eig_work, eig_info, eig_v, eig_lambda, tr_dev;
@@ -234,7 +260,8 @@ struct dopinf_b200_ctx {
         cudaEventRecord(ev[stage][which], stream);
         if (which == 1) ev_done[stage] = true;
     }
-    void sync(const char* what) { ck(cudaStreamSynchronize(stream), what); }
+    // Wait for the stream; with a collective queued, poll with the deadline.
+    void sync(const char* what);
 };
 
 struct dopinf_b200_block {
@@ -319,18 +346,68 @@ struct Fd {
     }
 };
 
+// ---- collectives (capi_coll.cu) ------------------------------------------------
+// True when the context's collectives run over NCCL (a communicator, or a
+// poisoned context whose calls must keep failing).
+inline bool coll(const dopinf_b200_ctx* c) { return c->comm != nullptr || c->poisoned; }
+void coll_allreduce(dopinf_b200_ctx* c, const void* send, void* recv, size_t count, ncclDataType_t type,
+                    ncclRedOp_t op, const char* what);
+void coll_allgather(dopinf_b200_ctx* c, const void* send, void* recv, size_t count, ncclDataType_t type,
+                    const char* what);
+void coll_broadcast(dopinf_b200_ctx* c, void* buf, size_t count, ncclDataType_t type, int root, const char* what);
+// Bounded wait on a side stream (a poisoned context must not hang in teardown).
+void join_stream(dopinf_b200_ctx* c, cudaStream_t s);
+// The status slot a rank contributes to a SUM-reduced buffer: 2^rank when it
+// failed (exact for up to 52 ranks; beyond that every failure reads as rank 52+).
+inline double failure_bit(const dopinf_b200_ctx* c, bool failed) {
+    return failed ? std::ldexp(1.0, std::min(c->rank, 52)) : 0.0;
+}
+// Lowest failing rank from a summed status slot, -1 when none failed.
+inline int lowest_failed(double bits) {
+    if (!(bits > 0.0)) return -1;
+    for (int r = 0; r <= 52; ++r) {
+        if (std::fmod(std::floor(bits / std::ldexp(1.0, r)), 2.0) == 1.0) return r;
+    }
+    return 52;
+}
+// Run a rank-local step whose failure must still let this rank enter the
+// collective that follows (so peers learn of it instead of timing out).
+template <class F>
+std::optional<Fail> attempt(dopinf_b200_ctx* c, F&& fn) {
+    if (!coll(c)) {
+        fn();
+        return std::nullopt;
+    }
+    try {
+        fn();
+    } catch (const Fail& f) {
+        if (c->poisoned) throw;
+        return f;
+    } catch (const std::bad_alloc&) {
+        return Fail{DOPINF_B200_ERR_OUT_OF_MEMORY, "host allocation failed"};
+    }
+    return std::nullopt;
+}
+// After the collective: rethrow this rank's own failure, else report a peer's
+// (the reference's peers see CollectiveError "rank r aborted", comm_inprocess.cpp:171).
+inline void settle(const std::optional<Fail>& own, int failed_rank) {
+    if (own) throw *own;
+    if (failed_rank >= 0) fail(DOPINF_B200_ERR_COLLECTIVE, "rank " + std::to_string(failed_rank) + " aborted");
+}
+
 // ---- helpers defined in capi.cu / capi_io.cu --------------------------------
 void materialize(dopinf_b200_block* b);
 void run_stats(dopinf_b200_block* b, bool center);
 void do_center(dopinf_b200_block* b, double* means_host, bool side_copy = false);
-void do_global_scales(dopinf_b200_block* b, double* scales_host, size_t* degenerate);
+void do_global_scales(dopinf_b200_block* b, double* scales_host, size_t* degenerate,
+                      const std::optional<Fail>& earlier = std::nullopt);
 void do_scale(dopinf_b200_block* b, const double* scales_host);
 void copy_d_out(dopinf_b200_ctx* c, double* d_host);
-void unpack(dopinf_b200_ctx* c);
+void unpack(dopinf_b200_ctx* c, const double* packed);
 void ensure_tiles(dopinf_b200_ctx* c, int K);
 int* ensure_counters(dopinf_b200_ctx* c);
 void do_local_gram(dopinf_b200_block* b, double* d_host);
-void do_global_gram(dopinf_b200_ctx* c, double* d_host);
+void do_global_gram(dopinf_b200_ctx* c, double* d_host, const std::optional<Fail>& local_failure = std::nullopt);
 bool pread_all(int fd, void* dst, size_t bytes, uint64_t off);
 void open_snp1(Fd& f, const std::string& path);
 void validate_snp1(const Snp1& h);

@@ -33,8 +33,8 @@ struct StreamChunk {
 // Joins the copy stream when an entry point leaves (also on failure): work a
 // streamed pass left there (the last variable's scaling) is done by then.
 struct SideJoin {
-    cudaStream_t s;
-    ~SideJoin() { cudaStreamSynchronize(s); }
+    dopinf_b200_ctx* c;
+    ~SideJoin() { join_stream(c, c->copy_stream); }
 };
 
 struct StreamSource {
@@ -109,6 +109,8 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
     b->pending_center = false;
     b->stats_valid = false;
     c->have_gram = false;
+    c->local_valid = false;
+    c->dmat_local = false;
     c->K = K;
     const std::vector<StreamChunk> chunks = stream_chunks(b, chunk_rows, !src.synth);
     while (c->chunk_events.size() < chunks.size() + 1) {
@@ -124,10 +126,10 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
         gram::make_stream_plan(std::max<long long>(first_rows, 1), K, c->num_sms, split_rows);
     double* work = c->work.get<double>(full.workspace_doubles, "workspace");
     double* gv = c->gv.get<double>(count * b->n_vars, "per-variable Grams");
-    double* vm = b->varmax.get<double>(b->n_vars, "varmax");
-    double* ds = c->scales.get<double>(b->n_vars, "scales");
+    double* vm = b->varmax.get<double>(b->n_vars + 1, "varmax");
+    double* ds = c->scales.get<double>(b->n_vars + 1, "scales");
     double* mn = b->means.get<double>(std::max<size_t>(b->rows, 1), "means");
-    double* packed = c->packed.get<double>(count, "packed");
+    double* packed = c->packed.get<double>(count + 1, "packed");  // + status slot (0)
     double* ring = src.synth ? c->ring.get<double>(2 * static_cast<size_t>(first_rows) * b->ld, "chunk ring")
                              : nullptr;
     const bool from_file = src.fd >= 0;
@@ -194,9 +196,8 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
                                    groups, scratch),
                "gram reduce");
             if (scaling) {
-                if (c->size > 1) {
-                    ckn(ncclAllReduce(vm + ch.var, ds + ch.var, 1, ncclFloat64, ncclMax, c->comm, c->stream),
-                        "allreduce(MAX)");
+                if (coll(c)) {
+                    coll_allreduce(c, vm + ch.var, ds + ch.var, 1, ncclFloat64, ncclMax, "allreduce(MAX)");
                 } else {
                     ck(cudaMemcpyAsync(ds + ch.var, vm + ch.var, sizeof(double), cudaMemcpyDeviceToDevice,
                                        c->stream),
@@ -215,7 +216,7 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
                     }
                     ck(transform::launch_apply(b->q + v0 * b->ld, b->ld, static_cast<long long>(b->nx_i), K,
                                                static_cast<long long>(b->nx_i), nullptr, ds + ch.var, c->num_sms,
-                                               s),
+                                               s, /*skip_zero_scale=*/true),
                        "scale");
                 }
             }
@@ -227,8 +228,8 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
     if (from_file && !chunks.empty()) ck(cudaEventSynchronize(c->chunk_events[chunks.size() - 1]), "ring");
     if (b->rows == 0 && scaling) {  // an empty rank still joins the MAX collectives
         for (size_t v = 0; v < b->n_vars; ++v) {
-            if (c->size > 1) {
-                ckn(ncclAllReduce(vm + v, ds + v, 1, ncclFloat64, ncclMax, c->comm, c->stream), "allreduce(MAX)");
+            if (coll(c)) {
+                coll_allreduce(c, vm + v, ds + v, 1, ncclFloat64, ncclMax, "allreduce(MAX)");
             } else {
                 ck(cudaMemcpyAsync(ds + v, vm + v, sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
             }
@@ -237,8 +238,9 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
     ck(gram::launch_combine_vars(gv, static_cast<int>(b->n_vars), count, scaling ? ds : nullptr, packed,
                                  c->stream),
        "combine");
+    ck(cudaMemsetAsync(packed + count, 0, sizeof(double), c->stream), "memset");
     c->record(DOPINF_B200_STAGE_STREAM, 1);
-    c->have_gram = true;
+    c->local_valid = true;
     if (means_host && b->rows > 0) c->d2h(means_host, mn, b->rows * sizeof(double), "means D2H");
     if (scaling) {
         std::vector<double> s(b->n_vars);
@@ -421,12 +423,11 @@ int dopinf_b200_snapshot_pass_host(dopinf_b200_block* b, const double* host, siz
     auto* c = b->ctx;
     return guarded(c, [&] {
         require(host_ld >= b->nt && (b->rows == 0 || host), "snapshot_pass_host: bad host buffer");
-        SideJoin join{c->copy_stream};
+        SideJoin join{c};
         StreamSource src;
         src.host = host;
         src.host_ld = host_ld;
         do_stream_pass(b, src, scaling != 0, means, scales);
-        unpack(c);
         do_global_gram(c, d);
         c->sync("snapshot_pass_host");
     });
@@ -463,7 +464,7 @@ int dopinf_b200_block_read(dopinf_b200_ctx* c, const char* path, size_t row_begi
     *out = nullptr;
     dopinf_b200_block* b = nullptr;
     const int rc = guarded(c, [&] {
-        SideJoin join{c->copy_stream};
+        SideJoin join{c};
         Fd f;
         Snp1 h;
         b = open_file_block(c, path, row_begin, row_end, f, h);
@@ -490,7 +491,7 @@ int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* c, const char* path, size_t 
     *out = nullptr;
     dopinf_b200_block* b = nullptr;
     const int rc = guarded(c, [&] {
-        SideJoin join{c->copy_stream};
+        SideJoin join{c};
         Fd f;
         Snp1 h;
         b = open_file_block(c, path, row_begin, row_end, f, h);
@@ -500,7 +501,6 @@ int dopinf_b200_snapshot_pass_file(dopinf_b200_ctx* c, const char* path, size_t 
         const std::string p(path);
         src.path = &p;
         do_stream_pass(b, src, scaling != 0, means, scales);
-        unpack(c);
         do_global_gram(c, d);
         c->sync("snapshot_pass_file");
     });
@@ -530,7 +530,7 @@ int dopinf_b200_stream_pass_synth(dopinf_b200_ctx* c, size_t n_vars, size_t nx_i
         struct Release {
             dopinf_b200_block& b;
             ~Release() {
-                cudaStreamSynchronize(b.ctx->stream);
+                join_stream(b.ctx, b.ctx->stream);
                 b.means.release();
                 b.varmax.release();
             }
@@ -543,7 +543,6 @@ int dopinf_b200_stream_pass_synth(dopinf_b200_ctx* c, size_t n_vars, size_t nx_i
         src.noise = noise;
         src.amps = amps;
         do_stream_pass(&view, src, scaling != 0, means, scales);
-        unpack(c);
         do_global_gram(c, d);
         c->sync("stream_pass_synth");
     });

@@ -13,9 +13,11 @@ namespace {
 void host_allreduce(dopinf_b200_ctx* c, double* data, size_t count, ncclRedOp_t op) {
     double* buf = c->span.get<double>(count, "span");
     ck(cudaMemcpyAsync(buf, data, count * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
-    ckn(ncclAllReduce(buf, buf, count, ncclFloat64, op, c->comm, c->stream), "allreduce");
-    ck(cudaMemcpyAsync(data, buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    coll_allreduce(c, buf, buf, count, ncclFloat64, op, "allreduce");
+    double* pin = c->small_pinned<double>(count);
+    ck(cudaMemcpyAsync(pin, buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
     c->sync("allreduce");
+    std::memcpy(data, pin, count * sizeof(double));
 }
 
 // G = DhatᵀDhat (d × d, full, bitwise symmetric) with the Gram kernel on the
@@ -63,154 +65,162 @@ GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r
     const int S = R * (R + 1) / 2, D = R + S + 1, KK = NT - 1;
     const size_t ldd = (static_cast<size_t>(D) + 1) / 2 * 2;
 
-    // Q̂ (r × nt) on the device
-    const double* dq;
-    if (qhat_host) {
-        double* q = c->rom_qhat.get<double>(r * nt, "rom qhat");
-        ck(cudaMemcpyAsync(q, qhat_host, r * nt * sizeof(double), cudaMemcpyHostToDevice, c->stream), "qhat H2D");
-        dq = q;
-    } else {
-        require(c->qhat_r == r && c->qhat_nt == nt, "grid_search: no device Q-hat of this shape on the context");
-        dq = c->qhat.get<double>(r * nt, "qhat");
-    }
-    // pair-independent data: Dhat, Qhat2ᵀ, qhat_rows, G = DhatᵀDhat, Dhatᵀ Qhat2ᵀ
-    double* dhat = c->rom_dhat.get<double>(static_cast<size_t>(KK) * ldd, "dhat");
-    double* q2t = c->rom_q2t.get<double>(static_cast<size_t>(KK) * r, "qhat2t");
-    double* qrows = c->rom_qrows.get<double>(nt * r, "qhat rows");
-    double* g = c->rom_g.get<double>(static_cast<size_t>(D) * D, "dhat gram");
-    double* rhs = c->rom_rhs.get<double>(static_cast<size_t>(D) * r, "rhs");
-    ck(rom::launch_assemble(dq, R, NT, dhat, ldd, q2t, c->stream), "assemble");
-    ck(rom::launch_transpose(dq, R, NT, qrows, c->stream), "transpose");
-    // DhatᵀDhat: bit-identical to linalg::gram (FMA chains) up to d = 2048;
-    // larger systems on the tensor-pipe Gram kernel
-    if (D <= 2048) {
-        ck(rom::launch_gram_exact(dhat, ldd, KK, D, g, c->stream), "dhat gram");
-    } else {
-        rom_gram(c, dhat, ldd, KK, D, g);
-    }
-    ck(rom::launch_rhs(dhat, ldd, q2t, KK, D, R, rhs, c->stream), "rhs");
-
-    // this rank's candidates, solved / integrated / scored in batches that fit
     const size_t n_reg = n1 * n2;
-    size_t pb = 0, pe = 0;
-    if (dopinf_b200_distribute_pairs(n_reg, c->rank, c->size, &pb, &pe) != DOPINF_B200_OK) {
-        fail(DOPINF_B200_ERR_INVALID_ARGUMENT, g_thread_err);
-    }
-    const std::pair<size_t, size_t> mine(pb, pe);
-    const size_t np = mine.second - mine.first;
-    const size_t per_pair = static_cast<size_t>(D) * D + static_cast<size_t>(D) * r + nt_p * r;
-    size_t batch = std::max<size_t>(1, std::min<size_t>(std::max<size_t>(np, 1),
-                                                         (size_t(8) << 30) / (per_pair * sizeof(double))));
-    if (const char* env = std::getenv("DOPINF_B200_GRID_BATCH")) {  // test knob: pairs per batch
-        const long long v = std::atoll(env);
-        if (v > 0) batch = std::min<size_t>(batch, static_cast<size_t>(v));
-    }
-    std::string err;
-    int* info = c->rom_info.get<int>(2 * batch, "potrf info");
-    double* betas = c->rom_betas.get<double>(2 * batch, "betas");
-    double* lhs = c->rom_lhs.get<double>(batch * D * D, "lhs");
-    double* rhsb = c->rom_rhsb.get<double>(batch * D * r, "rhs batch");
-    double* traj = c->rom_traj.get<double>(batch * nt_p * r, "trajectories");
-    double* scores = c->rom_scores.get<double>(batch * rom::kScoreFields, "scores");
-    cudaEvent_t ev[2];
-    ck(cudaEventCreate(&ev[0]), "event");
-    ck(cudaEventCreate(&ev[1]), "event");
-    struct EvGuard {
-        cudaEvent_t* e;
-        ~EvGuard() {
-            cudaEventDestroy(e[0]);
-            cudaEventDestroy(e[1]);
-        }
-    } evg{ev};
-
     double best_err = std::numeric_limits<double>::infinity();
     size_t best = n_reg;
     double n_diverged = 0.0, n_growth = 0.0, rom_ms = 0.0;
     std::vector<double> best_traj;
-    for (size_t p0 = mine.first; p0 < mine.second; p0 += batch) {
-        const size_t nb = std::min(batch, mine.second - p0);
-        std::vector<double> hb(2 * nb);
-        for (size_t k = 0; k < nb; ++k) {
-            hb[k] = b1[(p0 + k) / n2];
-            hb[nb + k] = b2[(p0 + k) % n2];
+    // This rank's share; a failure here still reaches the first collective
+    // below, so the peers raise "rank r aborted" rather than wait out the deadline.
+    const std::optional<Fail> own = attempt(c, [&] {
+        // Q̂ (r × nt) on the device
+        const double* dq;
+        if (qhat_host) {
+            double* q = c->rom_qhat.get<double>(r * nt, "rom qhat");
+            ck(cudaMemcpyAsync(q, qhat_host, r * nt * sizeof(double), cudaMemcpyHostToDevice, c->stream), "qhat H2D");
+            dq = q;
+        } else {
+            require(c->qhat_r == r && c->qhat_nt == nt, "grid_search: no device Q-hat of this shape on the context");
+            dq = c->qhat.get<double>(r * nt, "qhat");
         }
-        ck(cudaMemcpyAsync(betas, hb.data(), 2 * nb * sizeof(double), cudaMemcpyHostToDevice, c->stream), "betas");
-        ck(rom::launch_systems(g, D, R, betas, betas + nb, static_cast<int>(nb), rhs, lhs, rhsb, c->stream),
-           "systems");
-        ck(cudaMemsetAsync(info, 0, 2 * nb * sizeof(int), c->stream), "memset");
-        // Cholesky factors over concurrent cuSOLVER lanes, then every pair's
-        // triangular solves in one launch (shared-memory substitution); systems
-        // beyond the shared-memory solve use cuSOLVER's potrs per pair
-        if (D <= 1760) {
-            if (c->solver.cholesky(lhs, D, static_cast<int>(nb), info, c->stream, &err) != cudaSuccess) {
+        // pair-independent data: Dhat, Qhat2ᵀ, qhat_rows, G = DhatᵀDhat, Dhatᵀ Qhat2ᵀ
+        double* dhat = c->rom_dhat.get<double>(static_cast<size_t>(KK) * ldd, "dhat");
+        double* q2t = c->rom_q2t.get<double>(static_cast<size_t>(KK) * r, "qhat2t");
+        double* qrows = c->rom_qrows.get<double>(nt * r, "qhat rows");
+        double* g = c->rom_g.get<double>(static_cast<size_t>(D) * D, "dhat gram");
+        double* rhs = c->rom_rhs.get<double>(static_cast<size_t>(D) * r, "rhs");
+        ck(rom::launch_assemble(dq, R, NT, dhat, ldd, q2t, c->stream), "assemble");
+        ck(rom::launch_transpose(dq, R, NT, qrows, c->stream), "transpose");
+        // DhatᵀDhat: bit-identical to linalg::gram (FMA chains) up to d = 2048;
+        // larger systems on the tensor-pipe Gram kernel
+        if (D <= 2048) {
+            ck(rom::launch_gram_exact(dhat, ldd, KK, D, g, c->stream), "dhat gram");
+        } else {
+            rom_gram(c, dhat, ldd, KK, D, g);
+        }
+        ck(rom::launch_rhs(dhat, ldd, q2t, KK, D, R, rhs, c->stream), "rhs");
+
+        // this rank's candidates, solved / integrated / scored in batches that fit
+        size_t pb = 0, pe = 0;
+        if (dopinf_b200_distribute_pairs(n_reg, c->rank, c->size, &pb, &pe) != DOPINF_B200_OK) {
+            fail(DOPINF_B200_ERR_INVALID_ARGUMENT, g_thread_err);
+        }
+        const std::pair<size_t, size_t> mine(pb, pe);
+        const size_t np = mine.second - mine.first;
+        const size_t per_pair = static_cast<size_t>(D) * D + static_cast<size_t>(D) * r + nt_p * r;
+        size_t batch = std::max<size_t>(1, std::min<size_t>(std::max<size_t>(np, 1),
+                                                             (size_t(8) << 30) / (per_pair * sizeof(double))));
+        if (const char* env = std::getenv("DOPINF_B200_GRID_BATCH")) {  // test knob: pairs per batch
+            const long long v = std::atoll(env);
+            if (v > 0) batch = std::min<size_t>(batch, static_cast<size_t>(v));
+        }
+        std::string err;
+        int* info = c->rom_info.get<int>(2 * batch, "potrf info");
+        double* betas = c->rom_betas.get<double>(2 * batch, "betas");
+        double* lhs = c->rom_lhs.get<double>(batch * D * D, "lhs");
+        double* rhsb = c->rom_rhsb.get<double>(batch * D * r, "rhs batch");
+        double* traj = c->rom_traj.get<double>(batch * nt_p * r, "trajectories");
+        double* scores = c->rom_scores.get<double>(batch * rom::kScoreFields, "scores");
+        cudaEvent_t ev[2];
+        ck(cudaEventCreate(&ev[0]), "event");
+        ck(cudaEventCreate(&ev[1]), "event");
+        struct EvGuard {
+            cudaEvent_t* e;
+            ~EvGuard() {
+                cudaEventDestroy(e[0]);
+                cudaEventDestroy(e[1]);
+            }
+        } evg{ev};
+
+        for (size_t p0 = mine.first; p0 < mine.second; p0 += batch) {
+            const size_t nb = std::min(batch, mine.second - p0);
+            std::vector<double> hb(2 * nb);
+            for (size_t k = 0; k < nb; ++k) {
+                hb[k] = b1[(p0 + k) / n2];
+                hb[nb + k] = b2[(p0 + k) % n2];
+            }
+            ck(cudaMemcpyAsync(betas, hb.data(), 2 * nb * sizeof(double), cudaMemcpyHostToDevice, c->stream), "betas");
+            ck(rom::launch_systems(g, D, R, betas, betas + nb, static_cast<int>(nb), rhs, lhs, rhsb, c->stream),
+               "systems");
+            ck(cudaMemsetAsync(info, 0, 2 * nb * sizeof(int), c->stream), "memset");
+            // Cholesky factors over concurrent cuSOLVER lanes, then every pair's
+            // triangular solves in one launch (shared-memory substitution); systems
+            // beyond the shared-memory solve use cuSOLVER's potrs per pair
+            if (D <= 1760) {
+                if (c->solver.cholesky(lhs, D, static_cast<int>(nb), info, c->stream, &err) != cudaSuccess) {
+                    fail(DOPINF_B200_ERR_DEVICE, err);
+                }
+                ck(rom::launch_chol_solve(lhs, D, static_cast<int>(nb), rhsb, R, c->stream), "cholesky solve");
+            } else if (c->solver.spd_solve(lhs, D, static_cast<int>(nb), rhsb, R, info, c->stream, &err) != cudaSuccess) {
                 fail(DOPINF_B200_ERR_DEVICE, err);
             }
-            ck(rom::launch_chol_solve(lhs, D, static_cast<int>(nb), rhsb, R, c->stream), "cholesky solve");
-        } else if (c->solver.spd_solve(lhs, D, static_cast<int>(nb), rhsb, R, info, c->stream, &err) != cudaSuccess) {
-            fail(DOPINF_B200_ERR_DEVICE, err);
-        }
-        ck(cudaEventRecord(ev[0], c->stream), "event");
-        ck(rom::launch_integrate(rhsb, R, qrows, NTP, static_cast<int>(nb), traj, c->stream), "integrate");
-        ck(cudaEventRecord(ev[1], c->stream), "event");
-        ck(rom::launch_score(traj, NTP, R, qrows, NT, static_cast<int>(nb), scores, c->stream), "score");
-        std::vector<int> hinfo(2 * nb);
-        std::vector<double> sc(nb * rom::kScoreFields);
-        ck(cudaMemcpyAsync(hinfo.data(), info, hinfo.size() * sizeof(int), cudaMemcpyDeviceToHost, c->stream),
-           "info D2H");
-        ck(cudaMemcpyAsync(sc.data(), scores, sc.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
-           "scores D2H");
-        c->sync("grid search");
-        float f = 0.0f;
-        cudaEventElapsedTime(&f, ev[0], ev[1]);
-        rom_ms += f;
-        // pairs in index order, as the reference's loop (rom_search.cpp:214-225)
-        for (size_t k = 0; k < nb; ++k) {
-            if (hinfo[k] != 0 || hinfo[nb + k] != 0) {
-                fail(DOPINF_B200_ERR_SOLVE, "positive definite solve failed (dposv info=" +
-                                                std::to_string(hinfo[k] != 0 ? hinfo[k] : hinfo[nb + k]) + ")");
-            }
-            const double* o = &sc[k * rom::kScoreFields];
-            double score = std::numeric_limits<double>::infinity();
-            if (o[0] == 0.0) {
-                n_diverged += 1.0;
-            } else {
-                if (o[3] >= 0.0) {
-                    fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "training_error: reference row " +
-                                                               std::to_string(static_cast<long long>(o[3])) +
-                                                               " has zero norm");
+            ck(cudaEventRecord(ev[0], c->stream), "event");
+            ck(rom::launch_integrate(rhsb, R, qrows, NTP, static_cast<int>(nb), traj, c->stream), "integrate");
+            ck(cudaEventRecord(ev[1], c->stream), "event");
+            ck(rom::launch_score(traj, NTP, R, qrows, NT, static_cast<int>(nb), scores, c->stream), "score");
+            std::vector<int> hinfo(2 * nb);
+            std::vector<double> sc(nb * rom::kScoreFields);
+            ck(cudaMemcpyAsync(hinfo.data(), info, hinfo.size() * sizeof(int), cudaMemcpyDeviceToHost, c->stream),
+               "info D2H");
+            ck(cudaMemcpyAsync(sc.data(), scores, sc.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+               "scores D2H");
+            c->sync("grid search");
+            float f = 0.0f;
+            cudaEventElapsedTime(&f, ev[0], ev[1]);
+            rom_ms += f;
+            // pairs in index order, as the reference's loop (rom_search.cpp:214-225)
+            for (size_t k = 0; k < nb; ++k) {
+                if (hinfo[k] != 0 || hinfo[nb + k] != 0) {
+                    fail(DOPINF_B200_ERR_SOLVE, "positive definite solve failed (dposv info=" +
+                                                    std::to_string(hinfo[k] != 0 ? hinfo[k] : hinfo[nb + k]) + ")");
                 }
-                if (o[4] != 0.0) {
-                    fail(DOPINF_B200_ERR_INVALID_ARGUMENT,
-                         "growth_ratio: training data is constant; deviation ratio undefined");
-                }
-                if (o[2] < max_growth) {
-                    score = o[1];
+                const double* o = &sc[k * rom::kScoreFields];
+                double score = std::numeric_limits<double>::infinity();
+                if (o[0] == 0.0) {
+                    n_diverged += 1.0;
                 } else {
-                    n_growth += 1.0;
+                    if (o[3] >= 0.0) {
+                        fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "training_error: reference row " +
+                                                                   std::to_string(static_cast<long long>(o[3])) +
+                                                                   " has zero norm");
+                    }
+                    if (o[4] != 0.0) {
+                        fail(DOPINF_B200_ERR_INVALID_ARGUMENT,
+                             "growth_ratio: training data is constant; deviation ratio undefined");
+                    }
+                    if (o[2] < max_growth) {
+                        score = o[1];
+                    } else {
+                        n_growth += 1.0;
+                    }
+                }
+                if (score < best_err) {
+                    best_err = score;
+                    best = p0 + k;
+                    best_traj.resize(nt_p * r);
+                    ck(cudaMemcpy(best_traj.data(), traj + k * nt_p * r, nt_p * r * sizeof(double),
+                                  cudaMemcpyDeviceToHost),
+                       "trajectory D2H");
                 }
             }
-            if (score < best_err) {
-                best_err = score;
-                best = p0 + k;
-                best_traj.resize(nt_p * r);
-                ck(cudaMemcpy(best_traj.data(), traj + k * nt_p * r, nt_p * r * sizeof(double),
-                              cudaMemcpyDeviceToHost),
-                   "trajectory D2H");
-            }
         }
-    }
+
+    });
 
     // agree on the winner across ranks (rom_search.cpp:227-261)
     GridOutcome out;
     double global_min = best_err;
-    if (c->size > 1) {
-        std::vector<double> v = {best_err};
-        host_allreduce(c, v.data(), 1, ncclMin);
+    if (coll(c)) {
+        // MIN of the errors, and of (failed ? rank : size): the lowest failed rank
+        std::vector<double> v = {own ? std::numeric_limits<double>::infinity() : best_err,
+                                 static_cast<double>(own ? c->rank : c->size)};
+        host_allreduce(c, v.data(), 2, ncclMin);
         global_min = v[0];
+        settle(own, v[1] < c->size ? static_cast<int>(v[1]) : -1);
     }
     if (global_min == std::numeric_limits<double>::infinity()) {
         std::vector<double> counts = {n_diverged, n_growth};
-        if (c->size > 1) host_allreduce(c, counts.data(), 2, ncclSum);
+        if (coll(c)) host_allreduce(c, counts.data(), 2, ncclSum);
         fail(DOPINF_B200_ERR_NO_ADMISSIBLE_PAIR,
              "no admissible regularization pair among " + std::to_string(n_reg) + " candidates (" +
                  std::to_string(static_cast<long>(counts[0])) + " diverged, " +
@@ -218,7 +228,7 @@ GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r
                  std::to_string(max_growth) + ")");
     }
     int owner = 0;
-    if (c->size > 1) {
+    if (coll(c)) {
         std::vector<double> claim = {best_err == global_min ? static_cast<double>(c->rank)
                                                             : static_cast<double>(c->size)};
         host_allreduce(c, claim.data(), 1, ncclMin);
@@ -231,14 +241,16 @@ GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r
         packet[2] = rom_ms * 1e-3;
         std::copy(best_traj.begin(), best_traj.end(), packet.begin() + 3);
     }
-    if (c->size > 1) {
+    if (coll(c)) {
         double* dp = c->rom_packet.get<double>(packet.size(), "packet");
         ck(cudaMemcpyAsync(dp, packet.data(), packet.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream),
            "packet H2D");
-        ckn(ncclBroadcast(dp, dp, packet.size(), ncclFloat64, owner, c->comm, c->stream), "broadcast");
-        ck(cudaMemcpyAsync(packet.data(), dp, packet.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+        coll_broadcast(c, dp, packet.size(), ncclFloat64, owner, "broadcast");
+        double* pin = c->small_pinned<double>(packet.size());
+        ck(cudaMemcpyAsync(pin, dp, packet.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
            "packet D2H");
         c->sync("broadcast");
+        std::memcpy(packet.data(), pin, packet.size() * sizeof(double));
     }
     out.beta1 = packet[0];
     out.beta2 = packet[1];

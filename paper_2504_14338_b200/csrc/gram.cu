@@ -347,8 +347,10 @@ __global__ void unpack_kernel(const double* __restrict__ packed, int K, double* 
     }
 }
 
-// Streamed pass: D = Σ_v G_v / (s_v·s_v) over the per-variable Grams of the
-// centered rows, variables in order (scales == nullptr: plain Σ_v G_v).
+// Streamed pass: D = Σ_v (G_v / s_v) / s_v over the per-variable Grams of the
+// centered rows, variables in order (scales == nullptr: plain Σ_v G_v). Two
+// divisions rather than one by s_v²: s_v² leaves the double range for
+// |s_v| outside ~[1e-154, 1e154] where the reference's scaled values are fine.
 __global__ void combine_vars_kernel(const double* __restrict__ gv, int n_vars, size_t count,
                                     const double* __restrict__ scales, double* __restrict__ out) {
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < count;
@@ -356,19 +358,19 @@ __global__ void combine_vars_kernel(const double* __restrict__ gv, int n_vars, s
         double acc = 0.0;
         for (int v = 0; v < n_vars; ++v) {
             const double g = gv[static_cast<size_t>(v) * count + e];
-            acc += scales ? g / (scales[v] * scales[v]) : g;
+            acc += scales ? g / scales[v] / scales[v] : g;
         }
         out[e] = acc;
     }
 }
 
 // Ascending-rank sum of p packed triangles (comm_inprocess.cpp:101-112 order).
-__global__ void ordered_sum_kernel(const double* __restrict__ parts, int p, size_t count,
+__global__ void ordered_sum_kernel(const double* __restrict__ parts, int p, size_t count, size_t stride,
                                    double* __restrict__ out) {
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < count;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         double acc = parts[e];
-        for (int r = 1; r < p; ++r) acc += parts[static_cast<size_t>(r) * count + e];
+        for (int r = 1; r < p; ++r) acc += parts[static_cast<size_t>(r) * stride + e];
         out[e] = acc;
     }
 }
@@ -551,6 +553,7 @@ Plan make_plan(long long n_rows, int K, int num_sms, size_t workspace_cap_bytes)
 cudaError_t make_tensor_map(CUtensorMap* map, const double* q, long long n_rows, int K, size_t ld) {
     auto fn = tensor_map_encoder();
     if (!fn) return cudaErrorNotSupported;
+    if (n_rows >= (1LL << 31)) return cudaErrorInvalidValue;  // TMA row coordinates are int32
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(n_rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * sizeof(double))};
     const cuuint32_t box[2] = {16u, static_cast<cuuint32_t>(BK)};  // 128 B rows → 128B swizzle
@@ -641,10 +644,10 @@ cudaError_t launch_unpack(const double* packed, int K, double* d, cudaStream_t s
     return cudaGetLastError();
 }
 
-cudaError_t launch_ordered_sum(const double* parts, int p, size_t count, double* out,
+cudaError_t launch_ordered_sum(const double* parts, int p, size_t count, size_t stride, double* out,
                                cudaStream_t stream) {
     const int grid = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 16));
-    ordered_sum_kernel<<<std::max(grid, 1), 256, 0, stream>>>(parts, p, count, out);
+    ordered_sum_kernel<<<std::max(grid, 1), 256, 0, stream>>>(parts, p, count, stride, out);
     note_launch();
     return cudaGetLastError();
 }

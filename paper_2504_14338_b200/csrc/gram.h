@@ -48,7 +48,7 @@ cudaError_t launch_gram(const Plan& plan, const CUtensorMap& map, const TileInfo
 // Plan for one streamed chunk of `chunk_rows` rows cut into splits of
 // `split_rows`; its items accumulate into the same split slots chunk after chunk.
 Plan make_stream_plan(long long chunk_rows, int K, int num_sms, long long split_rows);
-// D = Σ_v gv[v] / scales[v]² (scales == nullptr: Σ_v gv[v]), variables in order.
+// D = Σ_v (gv[v] / scales[v]) / scales[v] (scales == nullptr: Σ_v gv[v]), variables in order.
 cudaError_t launch_combine_vars(const double* gv, int n_vars, size_t count, const double* scales,
                                 double* out, cudaStream_t stream);
 // Split groups for the fixed-order reduction (1 = one pass over all splits;
@@ -58,7 +58,8 @@ size_t reduce_scratch_doubles(const Plan& plan, int groups);
 cudaError_t launch_reduce(const Plan& plan, const TileInfo* d_tiles, const double* work,
                           double* packed, cudaStream_t stream, int groups = 1, double* scratch = nullptr);
 cudaError_t launch_unpack(const double* packed, int K, double* d, cudaStream_t stream);
-cudaError_t launch_ordered_sum(const double* parts, int p, size_t count, double* out,
+// out[e] = parts[0][e] + parts[1][e] + ... (rank r's part at parts + r*stride).
+cudaError_t launch_ordered_sum(const double* parts, int p, size_t count, size_t stride, double* out,
                                cudaStream_t stream);
 
 inline size_t packed_count(int K) { return static_cast<size_t>(K) * (K + 1) / 2; }

@@ -144,7 +144,7 @@ __device__ __forceinline__ double group_dot(const double* __restrict__ a, const 
 }
 
 // All pairs' ROMs in parallel, one CTA per pair: integrate (rom_search.cpp:
-// 60-85) from q0 for n_steps rows. ops_p: column-major d × r (column i =
+// 62-87) from q0 for n_steps rows. ops_p: column-major d × r (column i =
 // [A_i (r), F_i (s), c_i]: the solve's output layout). traj_p: n_steps × r.
 __global__ void __launch_bounds__(1024)
     integrate_kernel(const double* __restrict__ ops, int r, const double* __restrict__ q0, int n_steps,

@@ -133,7 +133,10 @@ __global__ void __launch_bounds__(kStatsWarps * 32)
     }
 }
 
-// x ← (x − mean[row]) / scale[var]  (or x − mean when scales == nullptr).
+// x ← (x − mean[row]) / scale[var]  (or x − mean when scales == nullptr);
+// a zero scale divides like the reference's div_scalar (±inf / NaN), unless
+// skip_zero (the streamed pass: a degenerate variable stays centered, as the
+// reference leaves it when compute_global_scales throws before scaling).
 // Warp per row; each lane issues kApplyBatch (8) independent 16-byte loads before
 // any store (streaming hints: the block is touched once per pass).
 constexpr int kApplyBatch = 8;
@@ -141,7 +144,7 @@ constexpr int kApplyBatch = 8;
 template <bool kScale>
 __global__ void __launch_bounds__(256)
     apply_kernel(double* __restrict__ q, size_t ld, long long rows, int K, long long nx_i,
-                 const double* __restrict__ means, const double* __restrict__ scales) {
+                 const double* __restrict__ means, const double* __restrict__ scales, int skip_zero) {
     const int lane = threadIdx.x % 32;
     const long long warp0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
     const long long nwarps = static_cast<long long>(gridDim.x) * blockDim.x / 32;
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(256)
     for (long long row = warp0; row < rows; row += nwarps) {
         const double neg = means ? -means[row] : -0.0;
         const double s = kScale ? scales[row / nx_i] : 1.0;
-        if (kScale && s == 0.0) continue;  // degenerate variable: left centered, host raises
+        if (kScale && skip_zero && s == 0.0) continue;
         double2* p = reinterpret_cast<double2*>(q + static_cast<size_t>(row) * ld);
         for (int c = lane; c < pairs; c += 32 * kApplyBatch) {
             double2 v[kApplyBatch];
@@ -190,13 +193,13 @@ cudaError_t launch_stats(const double* q, size_t ld, long long rows, int K, long
 
 cudaError_t launch_apply(double* q, size_t ld, long long rows, int K, long long nx_i,
                          const double* means, const double* scales, int num_sms,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, bool skip_zero_scale) {
     const long long want = (rows + 7) / 8;
     const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(want, num_sms * 16LL)));
     if (scales) {
-        apply_kernel<true><<<grid, 256, 0, stream>>>(q, ld, rows, K, nx_i, means, scales);
+        apply_kernel<true><<<grid, 256, 0, stream>>>(q, ld, rows, K, nx_i, means, scales, skip_zero_scale ? 1 : 0);
     } else {
-        apply_kernel<false><<<grid, 256, 0, stream>>>(q, ld, rows, K, nx_i, means, scales);
+        apply_kernel<false><<<grid, 256, 0, stream>>>(q, ld, rows, K, nx_i, means, scales, 0);
     }
     note_launch();
     return cudaGetLastError();

@@ -52,7 +52,7 @@ def test_library_is_sm100a_only():
 
 def test_abi_version_and_status_strings():
     l = lib()
-    assert l.dopinf_b200_abi_version() == 1
+    assert l.dopinf_b200_abi_version() == 2
     assert l.dopinf_b200_status_string(4) == b"DegenerateVariableError"
     assert l.dopinf_b200_status_string(2) == b"PartitionError"
 
@@ -120,8 +120,26 @@ def _rank_main(rank, world, port, q, nv, nx, nt, out):
     from paper_2504_14338_b200.distributed import max_over_ranks, share_unique_id
 
     o = Oracle()
-    # Unique-id exchange (rank 0's bytes reach every rank unchanged).
-    uid = share_unique_id(rank, fake=bytes(range(128)))
+    # bench.py's control plane: rank 0 makes a real NCCL unique id through the
+    # C ABI and every rank receives the same 128 bytes
+    uid = share_unique_id(rank)
+    ids = [None] * world
+    dist.all_gather_object(ids, uid)
+    assert len(uid) == 128 and all(i == uid for i in ids)
+    # the library's verify_uniform rule (dopinf_b200_check_uniform) on the
+    # descriptors the ranks all-gather: same verdict on every rank
+    verdicts = []
+    for count_of in (lambda r: 6, lambda r: 3 if r == 1 else 2):
+        desc = torch.tensor([7, count_of(rank), 0], dtype=torch.int64)
+        rows = [torch.zeros(3, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(rows, desc)
+        try:
+            api.check_uniform(torch.stack(rows).numpy(), rank, "allreduce")
+            verdicts.append("ok")
+        except api.CollectiveError as e:
+            verdicts.append(str(e))
+    # the reference data flow over the ranks (restated with the oracle): MAX of
+    # the scales, ascending-rank SUM of the Grams (comm_inprocess.cpp order)
     plan = api.partition_rows(nx, world)
     b, e = plan[rank].begin, plan[rank].end
     block = np.concatenate([q[j * nx + b: j * nx + e] for j in range(nv)])
@@ -129,18 +147,20 @@ def _rank_main(rank, world, port, q, nv, nx, nt, out):
     local_max = torch.from_numpy(o.local_maxabs(c, nv, e - b))
     dist.all_reduce(local_max, op=dist.ReduceOp.MAX)
     c = o.scale(c, nv, e - b, local_max.numpy())
-    # The C ABI's ORDERED Gram reduction: all-gather the partials, sum in
-    # ascending rank order (the reference's in-process order).
     parts = [torch.zeros(nt * nt, dtype=torch.float64) for _ in range(world)]
     dist.all_gather(parts, torch.from_numpy(o.gram(c).ravel()))
     d = torch.from_numpy(o.allreduce_sum(np.stack([p.numpy() for p in parts])))
     assert max_over_ranks(float(rank)) == world - 1
+    np.save(f"{out}.{rank}.npy", np.array(verdicts, dtype=object), allow_pickle=True)
     if rank == 0:
-        np.save(out, np.concatenate([d.numpy().ravel(), np.frombuffer(uid, dtype=np.uint8).astype(float)]))
+        np.save(out, d.numpy())
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_matches_reference_order(tmp_path):
+def test_two_rank_gloo_control_plane(tmp_path):
+    """world_size 2 over gloo: the real unique-id exchange, the library's
+    collective agreement rule on both ranks, and the reference's data flow
+    (oracle restatement) against the one-process oracle pass."""
     import torch.multiprocessing as mp
 
     from oracle.cpu import Oracle
@@ -152,12 +172,28 @@ def test_two_rank_gloo_matches_reference_order(tmp_path):
     out = tmp_path / "d.npy"
     mp.start_processes(_rank_main, args=(2, _free_port(), q, nv, nx, nt, str(out)), nprocs=2, join=True,
                        start_method="spawn")
-    got = np.load(out)
-    d = got[: nt * nt].reshape(nt, nt)
-    uid = got[nt * nt:].astype(np.uint8).tobytes()
-    assert uid == bytes(range(128))
+    d = np.load(out).reshape(nt, nt)
     _, _, _, d_ref = oracle_pass(o, q, nv, nx, 2)
     assert np.array_equal(d, d_ref)  # ascending-rank sum = the reference's in-process order
+    v0 = list(np.load(f"{out}.0.npy", allow_pickle=True))
+    v1 = list(np.load(f"{out}.1.npy", allow_pickle=True))
+    assert v0[0] == v1[0] == "ok"
+    # test_comm.cpp:95-112: a count mismatch raises on every rank, naming the counts
+    assert v0[1] == "allreduce: rank 0 passed count 2, rank 1 passed count 3"
+    assert v1[1] == "allreduce: rank 1 passed count 3, rank 0 passed count 2"
+
+
+def test_check_uniform_rules():
+    from paper_2504_14338_b200 import api
+
+    ok = np.array([[4, 10, 1], [4, 10, 1], [4, 10, 1]])
+    for r in range(3):
+        api.check_uniform(ok, r)
+    with pytest.raises(api.CollectiveError, match=r"^allreduce: rank 2 passed count 10, rank 0 passed count 10 "
+                                                  r"\(operations differ\)$"):
+        api.check_uniform(np.array([[4, 10, 0], [4, 10, 0], [4, 10, 1]]), 2)  # test_comm.cpp:114-123
+    with pytest.raises(api.CollectiveError, match="out of step"):
+        api.check_uniform(np.array([[4, 10, 1], [5, 10, 1]]), 0, "broadcast")
 
 
 def test_distribute_pairs_known_answers():
