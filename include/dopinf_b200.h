@@ -198,6 +198,10 @@ void dopinf_b200_block_destroy(dopinf_b200_block* block);
 int dopinf_b200_block_upload(dopinf_b200_block* block, const double* host, size_t host_ld);
 /* Materialises any pending transform, then copies the values to the host. */
 int dopinf_b200_block_download(dopinf_b200_block* block, double* host, size_t host_ld);
+/* Rows [row0, row0 + nrows) of the (materialised) block to the host, pitch
+ * host_ld: a block larger than host memory is read out in slices. */
+int dopinf_b200_block_download_rows(dopinf_b200_block* block, size_t row0, size_t nrows, double* host,
+                                    size_t host_ld);
 /* Device pointer and pitch (elements) of the block values. */
 int dopinf_b200_block_device(dopinf_b200_block* block, double** values, size_t* ld);
 /* Seeded synthetic snapshots on the device (BASELINE.json configs 1, 2, 4):
@@ -207,6 +211,11 @@ int dopinf_b200_block_device(dopinf_b200_block* block, double** values, size_t* 
  * The generator is plumbing for the bench/tests, not part of the pass. */
 int dopinf_b200_block_synth_oscillator(dopinf_b200_block* block, uint64_t seed, int n_modes,
                                        double dt, double noise, const double* amps);
+/* The same generator for variables var0 .. var0 + n_vars - 1 of a larger
+ * dataset (amps: n_vars entries for those variables, or NULL): the bytes one
+ * variable's rows have inside a streamed pass over the whole dataset. */
+int dopinf_b200_block_synth_oscillator_vars(dopinf_b200_block* block, int var0, uint64_t seed, int n_modes,
+                                            double dt, double noise, const double* amps);
 /* Seeded i.i.d. N(0,1) plus amplitude * (rank-`rank` low-rank component)
  * (BASELINE.json config 3). */
 int dopinf_b200_block_synth_lowrank(dopinf_b200_block* block, uint64_t seed, int rank,

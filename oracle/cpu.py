@@ -70,6 +70,8 @@ class Oracle:
                                                            C.c_int]
             lib.oracle_gram.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp]
             lib.oracle_allreduce_sum.argtypes = [_dp, C.c_int, C.c_size_t, _dp]
+            lib.oracle_gram_entries.argtypes = [_dp, C.c_size_t, C.c_size_t, _sp, _sp, C.c_size_t, _dp]
+            lib.oracle_row_stats.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp]
             lib.oracle_matmul_tn.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
             lib.oracle_matmul.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
             lib.oracle_matmul_nt.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
@@ -141,6 +143,68 @@ class Oracle:
         d = np.empty((cols, cols))
         self.lib.oracle_gram(_d(q), rows, cols, _d(d))
         return d
+
+    def gram_entries(self, q, ii, jj, acc, threads: int = 8):
+        """linalg.cpp:50-58 entries (ii[p], jj[p]) continued over the rows of q
+        (reference row order per entry; pairs split over threads, each pair's
+        chain sequential). acc (float64, len = pairs) is updated in place."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        ii = np.ascontiguousarray(ii, dtype=np.uintp)
+        jj = np.ascontiguousarray(jj, dtype=np.uintp)
+        assert acc.dtype == np.float64 and acc.flags.c_contiguous and acc.size == ii.size == jj.size
+        rows, ld = q.shape
+        bounds = np.linspace(0, ii.size, threads + 1).astype(int)
+
+        def run(t):
+            a, b = bounds[t], bounds[t + 1]
+            if b > a:
+                sub = acc[a:b]
+                self.lib.oracle_gram_entries(_d(q), ld, rows, ii[a:b].ctypes.data_as(_sp),
+                                             jj[a:b].ctypes.data_as(_sp), b - a, sub.ctypes.data_as(_dp))
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(run, range(threads)))
+        return acc
+
+    def row_stats(self, q, threads: int = 16):
+        """Per row: center_in_place's mean and the max |centered value|
+        (transform.cpp:14-15, 29-31) without writing q; rows split over threads."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        assert q.dtype == np.float64 and q.flags.c_contiguous
+        rows, cols = q.shape
+        means, maxabs = np.empty(rows), np.empty(rows)
+        bounds = np.linspace(0, rows, threads + 1).astype(int)
+
+        def run(t):
+            a, b = bounds[t], bounds[t + 1]
+            if b > a:
+                self.lib.oracle_row_stats(_d(q[a:b]), cols, b - a, cols, _d(means[a:b]), _d(maxabs[a:b]))
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(run, range(threads)))
+        return means, maxabs
+
+    def center_rows(self, q, threads: int = 16):
+        """center() over row slices in parallel (each row is independent):
+        returns (centered copy, means) bit-identical to center(q)."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        q = np.array(q, dtype=np.float64, order="C", copy=True)
+        rows, cols = q.shape
+        means = np.empty(rows)
+        bounds = np.linspace(0, rows, threads + 1).astype(int)
+
+        def run(t):
+            a, b = bounds[t], bounds[t + 1]
+            if b > a:
+                self.lib.oracle_center_in_place(_d(q[a:b]), b - a, cols, _d(means[a:b]))
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(run, range(threads)))
+        return q, means
 
     def allreduce_sum(self, parts):
         parts = _f(parts)

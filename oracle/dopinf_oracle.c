@@ -172,6 +172,26 @@ void oracle_center_in_place(double* q, size_t rows, size_t cols, double* means) 
     }
 }
 
+/* center_in_place's mean (transform.cpp:14-15) and the max-abs that
+ * compute_global_scales then takes of the centered row (transform.cpp:29-31),
+ * without writing the centered values: max over t of |fl(x_t + (-mean))|,
+ * the same numbers center_in_place stores. Rows at pitch ld. */
+void oracle_row_stats(const double* q, size_t ld, size_t rows, size_t cols, double* means,
+                      double* maxabs) {
+    for (size_t i = 0; i < rows; ++i) {
+        const double* row = q + i * ld;
+        const double mean = oracle_k_sum(row, cols) / (double)cols;
+        const double neg = -mean;
+        double m = 0.0;
+        for (size_t t = 0; t < cols; ++t) {
+            const double a = fabs(row[t] + neg);
+            if (a > m) m = a;
+        }
+        means[i] = mean;
+        maxabs[i] = m;
+    }
+}
+
 /* transform.cpp:29-31: per-variable max-abs over the contiguous
  * nx_i * nt segment of variable j (before the MAX all-reduce). */
 void oracle_local_maxabs(const double* q, size_t n_vars, size_t nx_i, size_t cols,
@@ -229,6 +249,19 @@ void oracle_gram(const double* q, size_t rows, size_t cols, double* d) {
     for (size_t l = 0; l < rows; ++l) {
         const double* ql = q + l * cols;
         for (size_t i = 0; i < cols; ++i) oracle_k_axpy(ql[i], ql, d + i * cols, cols);
+    }
+}
+
+/* linalg.cpp:50-58 gram restricted to the entries (ii[p], jj[p]) and
+ * continued over a further slice of rows (pitch ld): entry (i, j) of the
+ * reference's Gram only ever receives axpy's fma(q(l, i), q(l, j), c(i, j)),
+ * rows ascending, so acc[p] carried across consecutive row slices ends as the
+ * reference's value bit for bit (for a slice sequence in block-row order). */
+void oracle_gram_entries(const double* q, size_t ld, size_t rows, const size_t* ii, const size_t* jj,
+                         size_t npairs, double* acc) {
+    for (size_t l = 0; l < rows; ++l) {
+        const double* ql = q + l * ld;
+        for (size_t p = 0; p < npairs; ++p) acc[p] = fma(ql[ii[p]], ql[jj[p]], acc[p]);
     }
 }
 

@@ -69,6 +69,9 @@ SIGNATURES = {
     "dopinf_b200_block_destroy": (None, [_vp]),
     "dopinf_b200_block_upload": (C.c_int, [_vp, _dp, C.c_size_t]),
     "dopinf_b200_block_download": (C.c_int, [_vp, _dp, C.c_size_t]),
+    "dopinf_b200_block_download_rows": (C.c_int, [_vp, C.c_size_t, C.c_size_t, _dp, C.c_size_t]),
+    "dopinf_b200_block_synth_oscillator_vars": (C.c_int, [_vp, C.c_int, C.c_uint64, C.c_int, C.c_double,
+                                                           C.c_double, _dp]),
     "dopinf_b200_block_device": (C.c_int, [_vp, C.POINTER(_dp), _sp]),
     "dopinf_b200_block_synth_oscillator": (C.c_int, [_vp, C.c_uint64, C.c_int, C.c_double, C.c_double,
                                                       _dp]),

@@ -445,16 +445,26 @@ class LocalBlock:
         _check(_lib.load().dopinf_b200_block_download(self._h, _lib.dptr(out), self.nt), self.ctx, "download")
         return out
 
+    def rows_to(self, row0: int, out: np.ndarray) -> np.ndarray:
+        """Rows [row0, row0 + len(out)) into `out` ((n, nt) float64, e.g. pinned)."""
+        out = _out(out, (out.shape[0], self.nt))
+        _check(_lib.load().dopinf_b200_block_download_rows(self._h, row0, out.shape[0], _lib.dptr(out), self.nt),
+               self.ctx, "download_rows")
+        return out
+
     def device_ptr(self):
         p = _lib._dp()
         ld = C.c_size_t()
         _check(_lib.load().dopinf_b200_block_device(self._h, C.byref(p), C.byref(ld)), self.ctx)
         return C.cast(p, C.c_void_p).value, ld.value
 
-    def synth_oscillator(self, seed: int, n_modes: int, dt: float = 1e-3, noise: float = 1e-3, amps=None):
+    def synth_oscillator(self, seed: int, n_modes: int, dt: float = 1e-3, noise: float = 1e-3, amps=None,
+                         var0: int = 0):
+        """Seeded generator (BASELINE configs 1, 2, 4); var0 > 0 makes the rows of
+        variables var0.. of a larger dataset (amps: one entry per block variable)."""
         a = None if amps is None else _f64(amps, (self.n_vars,))
-        _check(_lib.load().dopinf_b200_block_synth_oscillator(self._h, seed, n_modes, dt, noise,
-                                                              _lib.dptr(a)), self.ctx, "synth")
+        _check(_lib.load().dopinf_b200_block_synth_oscillator_vars(self._h, var0, seed, n_modes, dt, noise,
+                                                                   _lib.dptr(a)), self.ctx, "synth")
 
     def synth_lowrank(self, seed: int, rank: int = 50, amplitude: float = 10.0):
         _check(_lib.load().dopinf_b200_block_synth_lowrank(self._h, seed, rank, amplitude), self.ctx, "synth")

@@ -673,6 +673,23 @@ int dopinf_b200_block_download(dopinf_b200_block* b, double* host, size_t host_l
     });
 }
 
+int dopinf_b200_block_download_rows(dopinf_b200_block* b, size_t row0, size_t nrows, double* host,
+                                    size_t host_ld) {
+    if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    auto* c = b->ctx;
+    return guarded(c, [&] {
+        require(host_ld >= b->nt && (nrows == 0 || host), "block_download_rows: bad host buffer");
+        require(row0 <= b->rows && nrows <= b->rows - row0, "block_download_rows: rows outside the block");
+        materialize(b);
+        if (nrows > 0) {
+            ck(cudaMemcpy2DAsync(host, host_ld * sizeof(double), b->q + row0 * b->ld, b->ld * sizeof(double),
+                                 b->nt * sizeof(double), nrows, cudaMemcpyDeviceToHost, c->stream),
+               "download");
+        }
+        c->sync("block_download_rows");
+    });
+}
+
 int dopinf_b200_block_device(dopinf_b200_block* b, double** values, size_t* ld) {
     if (!b || !values || !ld) return DOPINF_B200_ERR_INVALID_ARGUMENT;
     return guarded(b->ctx, [&] {
@@ -686,14 +703,20 @@ int dopinf_b200_block_device(dopinf_b200_block* b, double** values, size_t* ld) 
 
 int dopinf_b200_block_synth_oscillator(dopinf_b200_block* b, uint64_t seed, int n_modes, double dt,
                                        double noise, const double* amps) {
+    return dopinf_b200_block_synth_oscillator_vars(b, 0, seed, n_modes, dt, noise, amps);
+}
+
+int dopinf_b200_block_synth_oscillator_vars(dopinf_b200_block* b, int var0, uint64_t seed, int n_modes, double dt,
+                                            double noise, const double* amps) {
     if (!b) return DOPINF_B200_ERR_INVALID_ARGUMENT;
     auto* c = b->ctx;
     return guarded(c, [&] {
+        require(var0 >= 0, "synth: var0 must be >= 0");
         if (b->rows == 0) return;
         ck(synth::oscillator(b->q, b->ld, static_cast<long long>(b->rows), static_cast<int>(b->nt),
                              static_cast<long long>(b->nx_i), static_cast<long long>(b->row_begin),
                              static_cast<int>(b->n_vars), seed, n_modes, dt, noise, amps, c->num_sms,
-                             c->stream),
+                             c->stream, var0),
            "synth");
         b->pending_center = false;
         b->stats_valid = false;

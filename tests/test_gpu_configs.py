@@ -1,0 +1,253 @@
+"""Parity at the BASELINE.json configurations, at full size (north star:
+"results must match the reference oracle on identical seeded inputs").
+
+The oracle (oracle/dopinf_oracle.c, pinned to the compiled reference) runs on
+the host's 16 cores over the same bytes the device pass consumed, downloaded
+in slices:
+
+  C2  4 vars x 262,144 pts, K=1200 (the bench config, 10.1 GB): means, scales
+      and the whole transformed block bit-identical; 2,100 Gram entries in
+      the reference's own summation order (linalg.cpp:50-58: rows ascending,
+      one FMA per row) plus every diagonal entry; D·v = Qᵀ(Q v) for a seeded
+      v; Q̂ = T_rᵀD bit-identical.
+  C5  the C2 data, r in {20, 40, 80}: Φ_r rows against linalg::matmul's order
+      (4,096 sampled rows + 1,000 probe rows), basis_rows and
+      reconstruct_probes over a 2K horizon bit-identical to the reference.
+  C3  1 var x 4,194,304 pts, K=4096 (137 GB resident): Gram entries in
+      reference order and D·v over the whole block.
+  C4  8 vars x 4,194,304 pts, K=1500, amplitudes 1e-2..1e5 (403 GB, never
+      resident): the streamed pass's means (all 33.5 M rows) and scales
+      bit-identical, and its Gram entries against the reference order over
+      rows regenerated chunk by chunk.
+
+Tolerances: Gram relative error <= 1e-12 (north star), Φ_r <= 1e-9.
+DOPINF_SKIP_SLOW=1 skips this module (quick iterations only).
+"""
+import os
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("DOPINF_SKIP_SLOW") == "1", reason="DOPINF_SKIP_SLOW=1")]
+
+GRAM_TOL = 1e-12
+BASIS_TOL = 1e-9
+POOL = ThreadPoolExecutor(16)
+
+
+def api():
+    from paper_2504_14338_b200 import api as a
+
+    return a
+
+
+def pinned(rows, cols):
+    import torch
+
+    return torch.empty((rows, cols), dtype=torch.float64, pin_memory=True).numpy()
+
+
+def par_rows(fn, rows, parts=16):
+    """fn(a, b) over 16 row slices in parallel (numpy / ctypes release the GIL)."""
+    bounds = np.linspace(0, rows, parts + 1).astype(int)
+    return list(POOL.map(lambda t: fn(bounds[t], bounds[t + 1]), range(parts)))
+
+
+def divide_vars(q, row0, nx_i, scales):
+    """scale_in_place (transform.cpp:43-49) on rows of a block starting at block
+    row row0: IEEE division by the row's variable scale (numpy's / is IEEE)."""
+    def run(a, b):
+        for v in range(len(scales)):
+            lo, hi = max(a, v * nx_i - row0), min(b, (v + 1) * nx_i - row0)
+            if hi > lo:
+                np.divide(q[lo:hi], scales[v], out=q[lo:hi])
+    par_rows(run, q.shape[0])
+
+
+def sample_pairs(K, seed, n_cols=64):
+    """Gram entries checked: all (i <= j) among n_cols seeded columns (first and
+    last included), plus optionally every diagonal entry."""
+    rng = np.random.default_rng(seed)
+    cols = np.unique(np.concatenate([[0, K - 1], rng.choice(K, n_cols - 2, replace=False)]))
+    ii, jj = np.triu_indices(cols.size)
+    return cols, cols[ii], cols[jj]
+
+
+def gram_report(d, ii, jj, acc, what):
+    got = d[ii, jj]
+    rel_sampled = float(np.linalg.norm(got - acc) / np.linalg.norm(acc))
+    worst_entry = float(np.max(np.abs(got - acc)) / np.linalg.norm(d))
+    print(f"{what}: {ii.size} entries, sampled relative Frobenius {rel_sampled:.3e}, "
+          f"max entry error / ||D||_F {worst_entry:.3e}")
+    assert rel_sampled <= GRAM_TOL and worst_entry <= GRAM_TOL
+    return rel_sampled
+
+
+def dv_report(d, w, v, what):
+    err = float(np.linalg.norm(d @ v - w) / (np.linalg.norm(d) * np.linalg.norm(v)))
+    print(f"{what}: ||D v - Q^T(Q v)|| / (||D||_F ||v||) = {err:.3e}")
+    assert err <= GRAM_TOL
+    return err
+
+
+def tr_from(d, r):
+    lam, vec = np.linalg.eigh(d)
+    lam, vec = lam[::-1][:r], vec[:, ::-1][:, :r]
+    return np.ascontiguousarray(vec / np.sqrt(lam))
+
+
+# ---- C2 (+ C5 on the same block) -------------------------------------------------------
+@pytest.fixture(scope="module")
+def c2(ctx, oracle):
+    a = api()
+    nv, nx, K = 4, 262144, 1200
+    rows = nv * nx
+    blk = a.LocalBlock(ctx, nv, a.RowRange(0, nx), K)
+    blk.synth_oscillator(seed=2, n_modes=40, dt=1e-3, noise=1e-4)
+    raw = blk.rows_to(0, pinned(rows, K))
+    params, d = a.snapshot_pass(blk, scaling=True)
+    q = blk.rows_to(0, pinned(rows, K))
+    yield dict(blk=blk, raw=raw, q=q, params=params, d=d, nv=nv, nx=nx, K=K)
+    blk.close()
+
+
+def test_c2_transform_bitwise_whole_block(c2, oracle):
+    t0 = time.time()
+    raw, q, p, nv, nx = c2["raw"], c2["q"], c2["params"], c2["nv"], c2["nx"]
+    means, maxabs = oracle.row_stats(raw)
+    assert np.array_equal(p.local_means, means)  # all 1,048,576 rows
+    scales = maxabs.reshape(nv, nx).max(axis=1)  # MAX over the rows (order free)
+    assert np.array_equal(p.scales, scales)
+    ref = np.empty_like(raw)
+    par_rows(lambda a, b: np.add(raw[a:b], -means[a:b, None], out=ref[a:b]), raw.shape[0])
+    divide_vars(ref, 0, nx, scales)
+    assert np.array_equal(q, ref)  # the whole 10.1 GB block, bit for bit
+    print(f"C2 transform: {raw.shape[0]} rows bitwise ({time.time() - t0:.1f} s)")
+
+
+def test_c2_gram_reference_order_and_dv(c2, oracle):
+    q, d, K = c2["q"], c2["d"], c2["K"]
+    _, ii, jj = sample_pairs(K, seed=22)
+    ii = np.concatenate([ii, np.arange(K)])
+    jj = np.concatenate([jj, np.arange(K)])
+    acc = np.zeros(ii.size)
+    oracle.gram_entries(q, ii, jj, acc, threads=16)
+    gram_report(d, ii, jj, acc, "C2 Gram")
+    assert np.array_equal(d, d.T)  # bitwise symmetric (linalg.hpp:17)
+    v = np.random.default_rng(7).standard_normal(K)
+    dv_report(d, q.T @ (q @ v), v, "C2 Gram")
+
+
+def test_c2_projection_bitwise(c2, ctx, oracle):
+    a = api()
+    d = c2["d"]
+    tr = tr_from(d, 40)
+    assert np.array_equal(a.project_resident(ctx, tr), oracle.project(tr, d))
+
+
+@pytest.mark.parametrize("r", [20, 40, 80])
+def test_c5_basis_and_probes(c2, ctx, oracle, reference, r):
+    a = api()
+    blk, q, d, p, nv, nx, K = c2["blk"], c2["q"], c2["d"], c2["params"], c2["nv"], c2["nx"], c2["K"]
+    tr = tr_from(d, r)
+    phi = a.basis(blk, tr)  # DMMA tall GEMM, rows x r
+    rng = np.random.default_rng(500 + r)
+    probe_rows = np.sort(rng.choice(nv * nx, 1000, replace=False))
+    rows = np.unique(np.concatenate([rng.choice(nv * nx, 4096, replace=False), probe_rows, [0, nv * nx - 1]]))
+    want = oracle.matmul(q[rows], tr)  # linalg::matmul (postprocess.cpp:66) order
+    err = float(np.linalg.norm(phi[rows] - want) / np.linalg.norm(want))
+    print(f"C5 r={r}: Phi_r on {rows.size} rows rel {err:.3e}")
+    assert err <= BASIS_TOL
+    # all 1,048,576 rows against an independent fp64 product (threaded BLAS)
+    full = float(np.linalg.norm(phi - q @ tr) / np.linalg.norm(phi))
+    print(f"C5 r={r}: Phi_r all rows vs numpy Q T_r rel {full:.3e}")
+    assert full <= BASIS_TOL
+    # basis_rows (postprocess.cpp:12-34) bit-identical on the 1,000 probe rows
+    assert np.array_equal(a.basis_rows(blk, tr, probe_rows), oracle.basis_rows(q, tr, probe_rows))
+    # reconstruct_probes (postprocess.cpp:36-61) over nt_p = 2K from a ROM-like
+    # trajectory, against the compiled reference on each probe's rows
+    nt_p = 2 * K
+    t = np.arange(nt_p)[:, None] * 1e-3
+    qt = np.cos(t * (1.0 + np.arange(r))[None, :]) * np.exp(-0.1 * t) * 0.05
+    var, idx = probe_rows // nx, probe_rows % nx
+    probes = [a.Probe(int(v), int(i)) for v, i in zip(var, idx)]
+    got = a.reconstruct_probes(blk, tr, qt, probes, p)
+    assert len(got) == 1000
+    for k in range(0, 1000, 37):  # the reference on a 4-row block holding the probe's point
+        rows4 = np.array([v * nx + idx[k] for v in range(nv)])
+        series, owned = reference.reconstruct_probes(q[rows4], nv, int(idx[k]), tr, qt, p.local_means[rows4],
+                                                     p.scales, True, [var[k]], [idx[k]])
+        assert owned[0] and np.array_equal(got[k].values, series[0])
+
+
+# ---- C3: K = 4096 on 4,194,304 rows (137 GB resident) -----------------------------------
+def test_c3_gram_k4096(ctx, oracle):
+    a = api()
+    n, K = 4194304, 4096
+    blk = a.LocalBlock(ctx, 1, a.RowRange(0, n), K)
+    blk.synth_lowrank(seed=3, rank=50, amplitude=10.0)
+    d = a.local_gram(blk)  # the SYRK of config 3 (raw values)
+    t0 = time.time()
+    cols, ii, jj = sample_pairs(K, seed=33)
+    acc = np.zeros(ii.size)
+    v = np.random.default_rng(8).standard_normal(K)
+    w = np.zeros(K)
+    step = 131072
+    buf = pinned(step, K)
+    for r0 in range(0, n, step):
+        chunk = blk.rows_to(r0, buf)
+        sub = np.ascontiguousarray(chunk[:, cols])
+        oracle.gram_entries(sub, np.searchsorted(cols, ii), np.searchsorted(cols, jj), acc, threads=16)
+        w += chunk.T @ (chunk @ v)
+    gram_report(d, ii, jj, acc, "C3 K=4096 Gram")
+    dv_report(d, w, v, "C3 K=4096 Gram")
+    print(f"C3 oracle pass {time.time() - t0:.1f} s")
+    blk.close()
+
+
+# ---- C4: 8 vars x 4,194,304 pts, K = 1500, streamed (403 GB) -------------------------------
+def test_c4_streamed_pass(ctx, oracle):
+    a = api()
+    nv, nx, K, modes, noise = 8, 4194304, 1500, 60, 1e-4
+    amps = np.logspace(-2, 5, nv)
+    params, d = a.stream_pass_synth(ctx, nv, a.RowRange(0, nx), K, seed=4, n_modes=modes, dt=1e-3, noise=noise,
+                                    amps=amps, scaling=True)
+    t0 = time.time()
+    step = 262144
+    buf = pinned(step, K)
+
+    def rows_of(v, p0):
+        """Variable v's rows at points [p0, p0 + step): the bytes the stream made."""
+        cb = a.LocalBlock(ctx, 1, a.RowRange(p0, p0 + step), K)
+        cb.synth_oscillator(seed=4, n_modes=modes, dt=1e-3, noise=noise, amps=amps[v:v + 1], var0=v)
+        cb.rows_to(0, buf)
+        cb.close()
+        return buf
+
+    # pass 1: every variable's rows regenerated chunk by chunk; means of all
+    # 33.5 M rows and the per-variable max |centered| -> scales, bitwise
+    means = np.empty(nv * nx)
+    scales = np.zeros(nv)
+    for v in range(nv):
+        for p0 in range(0, nx, step):
+            m, mx = oracle.row_stats(rows_of(v, p0))
+            means[v * nx + p0: v * nx + p0 + step] = m
+            scales[v] = max(scales[v], float(mx.max()))
+    assert np.array_equal(params.local_means, means)
+    assert np.array_equal(params.scales, scales)
+    # pass 2: Gram entries of the transformed rows in block-row order (variable
+    # major), the reference's summation order
+    cols, ii, jj = sample_pairs(K, seed=44)
+    ci, cj = np.searchsorted(cols, ii), np.searchsorted(cols, jj)
+    acc = np.zeros(ii.size)
+    for v in range(nv):
+        for p0 in range(0, nx, step):
+            q = rows_of(v, p0)
+            m = means[v * nx + p0: v * nx + p0 + step]
+            sub = (q[:, cols] + (-m)[:, None]) / scales[v]  # center_in_place, then scale_in_place
+            oracle.gram_entries(np.ascontiguousarray(sub), ci, cj, acc, threads=16)
+    gram_report(d, ii, jj, acc, "C4 streamed Gram (amplitudes 1e-2..1e5)")
+    print(f"C4 oracle passes {time.time() - t0:.1f} s")

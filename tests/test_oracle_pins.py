@@ -211,3 +211,33 @@ def test_oracle_probes_vs_reference(oracle, reference, r, nt_p):
         series = np.array([[oracle.k_dot(basis[k], qt[t]) for t in range(nt_p)]])
         got[k] = oracle.inverse_transform(series, 1, means[row:row + 1], scales[row // nx:row // nx + 1], True)[0]
     assert np.array_equal(got, want)
+
+
+# ---- the sliced checkers used at config scale (tests/test_gpu_configs.py) ------------------------
+@pytest.mark.parametrize("m,k", [(1, 1), (37, 9), (1000, 64), (333, 130)])
+def test_sliced_checkers_match_whole_block(oracle, m, k):
+    # gram_entries carried over row slices = entries of the whole-block gram
+    # (the golden-pinned restatement of linalg.cpp:50-58); row_stats = center's
+    # means and the max |centered| that compute_global_scales takes
+    q = oracle.rng(m * 7 + k).matrix(m, k) * 3.0 + 1.5
+    c, means = oracle.center(q)
+    m2, mx = oracle.row_stats(q, threads=3)
+    assert np.array_equal(m2, means) and np.array_equal(mx, np.abs(c).max(axis=1))
+    c2, means2 = oracle.center_rows(q, threads=5)
+    assert np.array_equal(c2, c) and np.array_equal(means2, means)
+    d = oracle.gram(c)
+    ii, jj = np.triu_indices(k)
+    acc = np.zeros(ii.size)
+    for a, b in ((0, m // 3), (m // 3, m // 2), (m // 2, m)):
+        oracle.gram_entries(c[a:b], ii, jj, acc, threads=4)
+    assert np.array_equal(acc, d[ii, jj])
+
+
+def test_sliced_gram_entries_vs_reference(oracle, reference):
+    q = oracle.rng(5).matrix(4000, 48)
+    d = reference.gram(q)
+    ii, jj = np.triu_indices(48)
+    acc = np.zeros(ii.size)
+    for a in range(0, 4000, 1024):
+        oracle.gram_entries(q[a:a + 1024], ii, jj, acc)
+    assert np.array_equal(acc, d[ii, jj])
