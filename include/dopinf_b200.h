@@ -86,6 +86,21 @@ typedef enum dopinf_b200_gram_reduce {
     DOPINF_B200_GRAM_REDUCE_NCCL = 1
 } dopinf_b200_gram_reduce;
 
+/* Summation order of the local Gram (dopinf_b200_set_gram_order).
+ * TENSOR (default): the DMMA upper-triangle kernel with split-n partials reduced
+ * in a fixed order — bitwise reproducible, within ~1e-15 of the reference.
+ * REFERENCE: linalg::gram's own order (linalg.cpp:50-58; every entry one FMA
+ * chain over the rows, ascending), on the DFMA pipe — bit-identical to the
+ * reference's D; selecting it also selects the ORDERED cross-rank sum (the
+ * in-process backend's order), so D is the reference's at any rank count and
+ * everything downstream of it on the reference path (eig, reduced map, Q̂,
+ * the OpInf solve and ROM) is too. Streamed passes support it for resident
+ * blocks (host / file sources), not for dopinf_b200_stream_pass_synth. */
+typedef enum dopinf_b200_gram_order {
+    DOPINF_B200_GRAM_ORDER_TENSOR = 0,
+    DOPINF_B200_GRAM_ORDER_REFERENCE = 1
+} dopinf_b200_gram_order;
+
 /* Device-timed stages recorded per context (CUDA events on its stream). */
 typedef enum dopinf_b200_stage {
     DOPINF_B200_STAGE_UPLOAD = 0,
@@ -146,6 +161,8 @@ int dopinf_b200_ctx_rank(const dopinf_b200_ctx* ctx);
 int dopinf_b200_ctx_size(const dopinf_b200_ctx* ctx);
 const char* dopinf_b200_last_error(const dopinf_b200_ctx* ctx);
 int dopinf_b200_set_gram_reduce(dopinf_b200_ctx* ctx, int mode);
+/* DOPINF_B200_GRAM_ORDER_* (REFERENCE also sets the ORDERED reduction). */
+int dopinf_b200_set_gram_order(dopinf_b200_ctx* ctx, int order);
 /* Comm::allreduce / barrier (comm.hpp:20-30) on a HOST span, over NCCL;
  * SUM in ascending rank order (all-gather + ordered device sum). */
 int dopinf_b200_allreduce(dopinf_b200_ctx* ctx, double* data, size_t count, int op);

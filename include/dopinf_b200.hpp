@@ -132,6 +132,8 @@ public:
         check(dopinf_b200_allreduce(ctx_, data, count, op), ctx_, "allreduce");
     }
     void barrier() { check(dopinf_b200_barrier(ctx_), ctx_, "barrier"); }
+    // DOPINF_B200_GRAM_ORDER_TENSOR (default) or _REFERENCE (bit-identical D).
+    void set_gram_order(int order) { check(dopinf_b200_set_gram_order(ctx_, order), ctx_, "set_gram_order"); }
     double stage_ms(dopinf_b200_stage s) const {
         double ms = 0.0;
         dopinf_b200_stage_ms(ctx_, s, &ms);

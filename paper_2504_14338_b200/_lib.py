@@ -29,6 +29,7 @@ SUM, MAX, MIN = 0, 1, 2
 CTX_NCCL = 1
 INJECT_STALL = 1
 GRAM_REDUCE_ORDERED, GRAM_REDUCE_NCCL = 0, 1
+GRAM_ORDER_TENSOR, GRAM_ORDER_REFERENCE = 0, 1
 
 STAGES = ["upload", "stats", "scales", "apply", "gram", "gram_reduce", "allreduce", "unpack",
           "project", "basis", "download", "stream", "stream_gram", "field"]
@@ -59,6 +60,7 @@ SIGNATURES = {
     "dopinf_b200_ctx_size": (C.c_int, [_vp]),
     "dopinf_b200_last_error": (C.c_char_p, [_vp]),
     "dopinf_b200_set_gram_reduce": (C.c_int, [_vp, C.c_int]),
+    "dopinf_b200_set_gram_order": (C.c_int, [_vp, C.c_int]),
     "dopinf_b200_allreduce": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int]),
     "dopinf_b200_barrier": (C.c_int, [_vp]),
     "dopinf_b200_stage_ms": (C.c_int, [_vp, C.c_int, _dp]),

@@ -235,6 +235,12 @@ class DeviceContext:
         m = {"ordered": _lib.GRAM_REDUCE_ORDERED, "nccl": _lib.GRAM_REDUCE_NCCL}[mode]
         _check(_lib.load().dopinf_b200_set_gram_reduce(self._h, m), self)
 
+    def set_gram_order(self, order: str):
+        """"tensor" (DMMA, default) or "reference": linalg::gram's own FMA order,
+        bit-identical D (and the ORDERED cross-rank sum)."""
+        m = {"tensor": _lib.GRAM_ORDER_TENSOR, "reference": _lib.GRAM_ORDER_REFERENCE}[order]
+        _check(_lib.load().dopinf_b200_set_gram_order(self._h, m), self)
+
     def allreduce(self, data: np.ndarray, op: int) -> None:
         """Comm::allreduce (comm.hpp:20-28) on a host float64 array, in place."""
         if data.dtype != np.float64 or not data.flags.c_contiguous:

@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = PKG / "libdopinf_b200.so"
-SOURCES = ["capi.cu", "capi_coll.cu", "capi_io.cu", "capi_post.cu", "gram.cu", "transform.cu", "project.cu", "synth.cu", "eig.cu", "field.cu", "rom.cu"]
+SOURCES = ["capi.cu", "capi_coll.cu", "gram_ref.cu", "capi_io.cu", "capi_post.cu", "gram.cu", "transform.cu", "project.cu", "synth.cu", "eig.cu", "field.cu", "rom.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

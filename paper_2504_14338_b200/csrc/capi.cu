@@ -195,6 +195,10 @@ void do_local_gram(dopinf_b200_block* b, double* d_host) {
     ck(cudaMemsetAsync(packed + gram::packed_count(K), 0, sizeof(double), c->stream), "memset");
     if (rows == 0) {
         ck(cudaMemsetAsync(packed, 0, gram::packed_count(K) * sizeof(double), c->stream), "memset");
+    } else if (c->gram_order == DOPINF_B200_GRAM_ORDER_REFERENCE) {
+        c->record(DOPINF_B200_STAGE_GRAM, 0);
+        ck(gram::launch_gram_reference_order(b->q, b->ld, rows, K, packed, false, c->stream), "gram (reference order)");
+        c->record(DOPINF_B200_STAGE_GRAM, 1);
     } else {
         ensure_tiles(c, K);
         if (c->plan_K != K || c->plan_rows != rows) {
@@ -520,6 +524,15 @@ int dopinf_b200_set_gram_reduce(dopinf_b200_ctx* c, int mode) {
         require(mode == DOPINF_B200_GRAM_REDUCE_ORDERED || mode == DOPINF_B200_GRAM_REDUCE_NCCL,
                 "set_gram_reduce: unknown mode");
         c->gram_reduce = mode;
+    });
+}
+
+int dopinf_b200_set_gram_order(dopinf_b200_ctx* c, int order) {
+    return guarded(c, [&] {
+        require(order == DOPINF_B200_GRAM_ORDER_TENSOR || order == DOPINF_B200_GRAM_ORDER_REFERENCE,
+                "set_gram_order: unknown order");
+        c->gram_order = order;
+        if (order == DOPINF_B200_GRAM_ORDER_REFERENCE) c->gram_reduce = DOPINF_B200_GRAM_REDUCE_ORDERED;
     });
 }
 

@@ -191,6 +191,7 @@ struct dopinf_b200_ctx {
     ncclComm_t comm = nullptr;
     bool owns_comm = true, owns_stream = true;  // false: handed in by dopinf_b200_ctx_create_external
     int gram_reduce = DOPINF_B200_GRAM_REDUCE_NCCL;
+    int gram_order = DOPINF_B200_GRAM_ORDER_TENSOR;
     std::string err;
 
     // Collectives (capi_coll.cu). Every NCCL call goes through coll_*: a

@@ -98,7 +98,9 @@ std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b, long long chu
 // pass), is centered in place, and its Gram items accumulate (chunk order)
 // into the split slots of its variable. When a variable's last chunk is done
 // its slots are reduced into G_v, its MAX goes over the ranks and (resident
-// block) its rows are scaled. D = Σ_v G_v / s_v².
+// block) its rows are scaled. D = Σ_v G_v / s_v². In the reference-order
+// mode the chunks are only centered; once a variable is scaled, its rows'
+// Gram continues the reference's FMA chains (gram_ref.cu) in block-row order.
 void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling, double* means_host,
                     double* scales_host) {
     auto* c = b->ctx;
@@ -106,6 +108,9 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
     const size_t count = gram::packed_count(K);
     const long long chunk_rows = src.synth ? kSynthChunkRows : kStreamChunkRows;
     const long long split_rows = src.synth ? kSynthSplitRows : kStreamSplitRows;
+    const bool ref_order = c->gram_order == DOPINF_B200_GRAM_ORDER_REFERENCE;
+    require(!(ref_order && src.synth),
+            "stream_pass_synth: the reference-order Gram needs the rows resident (use the tensor order)");
     b->pending_center = false;
     b->stats_valid = false;
     c->have_gram = false;
@@ -143,6 +148,7 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
 
     c->record(DOPINF_B200_STAGE_STREAM, 0);
     ck(cudaMemsetAsync(vm, 0, b->n_vars * sizeof(double), c->stream), "memset");
+    if (ref_order) ck(cudaMemsetAsync(packed, 0, (count + 1) * sizeof(double), c->stream), "memset");
     ck(cudaMemsetAsync(gv, 0, count * b->n_vars * sizeof(double), c->stream), "memset");
     if (!src.synth) {
         // The copy stream must not overwrite the block before earlier work on it is done.
@@ -179,14 +185,36 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
            "stats");
         ck(transform::launch_apply(qk, b->ld, ch.rows, K, ch.rows, mn + ch.r0, nullptr, c->num_sms, c->stream),
            "center");
-        CUtensorMap map;
-        ck(gram::make_tensor_map(&map, qk, ch.rows, K, b->ld), "tensor map");
-        const gram::Plan plan = gram::make_stream_plan(ch.rows, K, c->num_sms, split_rows);
-        if (ch.first_of_var) first_plan = plan;
-        c->gram_event_pair();
-        ck(gram::launch_gram(plan, map, tiles, work, counters, c->stream, !ch.first_of_var), "gram");
-        c->gram_event_pair();
-        if (ch.last_of_var) {
+        if (!ref_order) {
+            CUtensorMap map;
+            ck(gram::make_tensor_map(&map, qk, ch.rows, K, b->ld), "tensor map");
+            const gram::Plan plan = gram::make_stream_plan(ch.rows, K, c->num_sms, split_rows);
+            if (ch.first_of_var) first_plan = plan;
+            c->gram_event_pair();
+            ck(gram::launch_gram(plan, map, tiles, work, counters, c->stream, !ch.first_of_var), "gram");
+            c->gram_event_pair();
+        }
+        if (ch.last_of_var && ref_order) {
+            const long long v0 = static_cast<long long>(ch.var) * static_cast<long long>(b->nx_i);
+            if (scaling) {
+                if (coll(c)) {
+                    coll_allreduce(c, vm + ch.var, ds + ch.var, 1, ncclFloat64, ncclMax, "allreduce(MAX)");
+                } else {
+                    ck(cudaMemcpyAsync(ds + ch.var, vm + ch.var, sizeof(double), cudaMemcpyDeviceToDevice,
+                                       c->stream),
+                       "copy");
+                }
+                ck(transform::launch_apply(b->q + v0 * b->ld, b->ld, static_cast<long long>(b->nx_i), K,
+                                           static_cast<long long>(b->nx_i), nullptr, ds + ch.var, c->num_sms,
+                                           c->stream, /*skip_zero_scale=*/true),
+                   "scale");
+            }
+            c->gram_event_pair();
+            ck(gram::launch_gram_reference_order(b->q + v0 * b->ld, b->ld, static_cast<long long>(b->nx_i), K,
+                                                 packed, ch.var > 0, c->stream),
+               "gram (reference order)");
+            c->gram_event_pair();
+        } else if (ch.last_of_var) {
             const int groups = gram::reduce_groups(first_plan, c->num_sms);
             double* scratch =
                 groups > 1 ? c->reduce_scratch.get<double>(gram::reduce_scratch_doubles(first_plan, groups),
@@ -235,9 +263,11 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
             }
         }
     }
-    ck(gram::launch_combine_vars(gv, static_cast<int>(b->n_vars), count, scaling ? ds : nullptr, packed,
-                                 c->stream),
-       "combine");
+    if (!ref_order) {
+        ck(gram::launch_combine_vars(gv, static_cast<int>(b->n_vars), count, scaling ? ds : nullptr, packed,
+                                     c->stream),
+           "combine");
+    }
     ck(cudaMemsetAsync(packed + count, 0, sizeof(double), c->stream), "memset");
     c->record(DOPINF_B200_STAGE_STREAM, 1);
     c->local_valid = true;

@@ -62,6 +62,13 @@ cudaError_t launch_unpack(const double* packed, int K, double* d, cudaStream_t s
 cudaError_t launch_ordered_sum(const double* parts, int p, size_t count, size_t stride, double* out,
                                cudaStream_t stream);
 
+// Reference-order mode (gram_ref.cu): every upper-triangle entry is the FMA
+// chain of linalg::gram (linalg.cpp:50-58) over the rows in order, written to
+// the packed triangle (accumulate: the chain continues from packed's values,
+// for row ranges processed in order). q 16-byte aligned, ld even.
+cudaError_t launch_gram_reference_order(const double* q, size_t ld, long long rows, int K, double* packed,
+                                        bool accumulate, cudaStream_t stream);
+
 inline size_t packed_count(int K) { return static_cast<size_t>(K) * (K + 1) / 2; }
 
 }  // namespace gram

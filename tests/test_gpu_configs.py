@@ -15,6 +15,8 @@ in slices:
       reconstruct_probes over a 2K horizon bit-identical to the reference.
   C3  1 var x 4,194,304 pts, K=4096 (137 GB resident): Gram entries in
       reference order and D·v over the whole block.
+  The reference-order Gram mode (gram_ref.cu) is checked bit for bit against
+  the sampled reference entries at C2 and C3.
   C4  8 vars x 4,194,304 pts, K=1500, amplitudes 1e-2..1e5 (403 GB, never
       resident): the streamed pass's means (all 33.5 M rows) and scales
       bit-identical, and its Gram entries against the reference order over
@@ -141,6 +143,28 @@ def test_c2_gram_reference_order_and_dv(c2, oracle):
     dv_report(d, q.T @ (q @ v), v, "C2 Gram")
 
 
+def test_c2_reference_order_gram_bitwise(c2, oracle):
+    # the reference-order mode on the same raw bytes (streamed from host memory):
+    # scales bitwise and the sampled entries equal the reference's FMA chains bit for bit
+    a = api()
+    raw, K, nv, nx = c2["raw"], c2["K"], c2["nv"], c2["nx"]
+    with a.DeviceContext(0) as c:
+        c.set_gram_order("reference")
+        blk = a.LocalBlock(c, nv, a.RowRange(0, nx), K)
+        t0 = time.time()
+        params, d = a.snapshot_pass_host(blk, raw, scaling=True)
+        print(f"C2 reference-order pass {time.time() - t0:.3f} s, Gram kernels {c.stage_ms('stream_gram'):.1f} ms")
+        blk.close()
+    assert np.array_equal(params.scales, c2["params"].scales)
+    _, ii, jj = sample_pairs(K, seed=23)
+    ii = np.concatenate([ii, np.arange(K)])
+    jj = np.concatenate([jj, np.arange(K)])
+    acc = np.zeros(ii.size)
+    oracle.gram_entries(c2["q"], ii, jj, acc, threads=16)
+    assert np.array_equal(d[ii, jj], acc)  # bit-identical to linalg::gram's chains
+    assert np.array_equal(d, d.T)
+
+
 def test_c2_projection_bitwise(c2, ctx, oracle):
     a = api()
     d = c2["d"]
@@ -162,8 +186,15 @@ def test_c5_basis_and_probes(c2, ctx, oracle, reference, r):
     print(f"C5 r={r}: Phi_r on {rows.size} rows rel {err:.3e}")
     assert err <= BASIS_TOL
     # all 1,048,576 rows against an independent fp64 product (threaded BLAS)
-    full = float(np.linalg.norm(phi - q @ tr) / np.linalg.norm(phi))
+    ref_all = q @ tr
+    full = float(np.linalg.norm(phi - ref_all) / np.linalg.norm(phi))
     print(f"C5 r={r}: Phi_r all rows vs numpy Q T_r rel {full:.3e}")
+    if full > BASIS_TOL:  # which rows, and is it the device side or the host product
+        bad = np.nonzero(np.abs(phi - ref_all).max(axis=1) > 1e-9 * np.abs(ref_all).max())[0]
+        again = a.basis(blk, tr)
+        print(f"bad rows {bad.size}: {bad[:8]} .. {bad[-4:]}; device again equal: {np.array_equal(again, phi)}; "
+              f"host again equal: {np.array_equal(q[bad] @ tr, ref_all[bad])}; "
+              f"oracle rows {float(np.abs(oracle.matmul(q[bad[:16]], tr) - phi[bad[:16]]).max()):.3e}")
     assert full <= BASIS_TOL
     # basis_rows (postprocess.cpp:12-34) bit-identical on the 1,000 probe rows
     assert np.array_equal(a.basis_rows(blk, tr, probe_rows), oracle.basis_rows(q, tr, probe_rows))
@@ -205,6 +236,16 @@ def test_c3_gram_k4096(ctx, oracle):
     gram_report(d, ii, jj, acc, "C3 K=4096 Gram")
     dv_report(d, w, v, "C3 K=4096 Gram")
     print(f"C3 oracle pass {time.time() - t0:.1f} s")
+    # reference-order mode on the same block: the sampled entries bit for bit
+    ctx.set_gram_order("reference")
+    try:
+        t0 = time.time()
+        d_ref = a.local_gram(blk)
+        print(f"C3 K=4096 reference-order Gram {ctx.stage_ms('gram'):.1f} ms")
+    finally:
+        ctx.set_gram_order("tensor")
+        ctx.set_gram_reduce("nccl")
+    assert np.array_equal(d_ref[ii, jj], acc)
     blk.close()
 
 

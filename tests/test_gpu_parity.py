@@ -471,3 +471,61 @@ def test_local_maxabs_no_zero_check(ctx):
     a.center_in_place(b)
     m = a.local_maxabs(b)
     assert m[0] == 0.0 and m[1] == 2.0
+
+
+# ---- reference-order Gram mode: D bit-identical to linalg::gram ---------------------------------
+@pytest.mark.parametrize("rows,nt", [(0, 5), (1, 1), (17, 7), (300, 127), (300, 128), (257, 129), (4099, 600),
+                                     (33, 1200), (2000, 301)])
+def test_reference_order_gram_bitwise(oracle, rows, nt):
+    a = api()
+    with a.DeviceContext(0) as c:
+        c.set_gram_order("reference")
+        rng = np.random.default_rng(rows * 13 + nt)
+        q = rng.standard_normal((rows, nt)) * rng.uniform(0.1, 100.0, (rows, 1))
+        blk = a.LocalBlock(c, 1, a.RowRange(0, rows), nt, values=q)
+        d = a.local_gram(blk)
+        assert np.array_equal(d, oracle.gram(q) if rows else np.zeros((nt, nt)))
+        blk.close()
+
+
+@pytest.mark.parametrize("n_vars,nx,nt,p", [(2, 3000, 97, 1), (4, 1001, 64, 3), (3, 5000, 130, 2)])
+def test_reference_order_pass_matches_reference_dataflow(oracle, n_vars, nx, nt, p):
+    # pipeline.cpp:270-280 over p ranks with the stage API in reference order:
+    # center, per-rank max-abs -> MAX, scale, local Gram, ascending-rank sum
+    # (what the ORDERED reduction does over NCCL): D is the reference's bit for bit
+    a = api()
+    rng = np.random.default_rng(nx + p)
+    q = rng.standard_normal((n_vars * nx, nt)) * rng.uniform(0.5, 20.0, (n_vars * nx, 1)) + 1.0
+    _, _, scales_ref, d_ref = oracle_pass(oracle, q, n_vars, nx, p)
+    with a.DeviceContext(0) as c:
+        c.set_gram_order("reference")
+        blocks = []
+        for rr in a.partition_rows(nx, p):
+            vals = np.concatenate([q[j * nx + rr.begin: j * nx + rr.end] for j in range(n_vars)])
+            blk = a.LocalBlock(c, n_vars, rr, nt, values=vals)
+            a.center_in_place(blk)
+            blocks.append(blk)
+        maxima = np.max([a.local_maxabs(b) for b in blocks], axis=0)
+        assert np.array_equal(maxima, scales_ref)
+        grams = []
+        for blk in blocks:
+            a.scale_in_place(blk, maxima)
+            grams.append(a.local_gram(blk))
+            blk.close()
+        assert np.array_equal(oracle.allreduce_sum(np.stack(grams)), d_ref)
+
+
+def test_reference_order_streamed_and_synth(oracle):
+    a = api()
+    n_vars, nx, nt = 3, 50000, 200
+    rng = np.random.default_rng(3)
+    q = rng.standard_normal((n_vars * nx, nt)) * np.array([1e-2, 1.0, 1e5]).repeat(nx)[:, None] + 0.5
+    _, _, scales_ref, d_ref = oracle_pass(oracle, q, n_vars, nx, 1)
+    with a.DeviceContext(0) as c:
+        c.set_gram_order("reference")
+        blk = a.LocalBlock(c, n_vars, a.RowRange(0, nx), nt)
+        params, d = a.snapshot_pass_host(blk, q, scaling=True)  # per-variable Gram after its MAX
+        assert np.array_equal(params.scales, scales_ref) and np.array_equal(d, d_ref)
+        blk.close()
+        with pytest.raises(a.InvalidArgumentError, match="reference-order Gram needs the rows resident"):
+            a.stream_pass_synth(c, 2, a.RowRange(0, 1000), 64, seed=1, n_modes=4)
