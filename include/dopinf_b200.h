@@ -219,6 +219,8 @@ int dopinf_b200_block_download(dopinf_b200_block* block, double* host, size_t ho
  * host_ld: a block larger than host memory is read out in slices. */
 int dopinf_b200_block_download_rows(dopinf_b200_block* block, size_t row0, size_t nrows, double* host,
                                     size_t host_ld);
+/* {n_vars, nx_i, row_begin, nt} of a block (e.g. one dopinf_b200_block_read made). */
+int dopinf_b200_block_shape(const dopinf_b200_block* block, size_t* dims);
 /* Device pointer and pitch (elements) of the block values. */
 int dopinf_b200_block_device(dopinf_b200_block* block, double** values, size_t* ld);
 /* Seeded synthetic snapshots on the device (BASELINE.json configs 1, 2, 4):

@@ -25,6 +25,17 @@
 // caller's host block. Each rank thread binds its Context first
 // (dopinf_b200::Bind), mirroring one Comm per rank under run_on_workers.
 //
+// Residency: each host-block function uploads (and, for the transforms,
+// downloads) the block. Every stage also has an overload on DeviceBlock
+// (data::to_device / data::read_block_device): the same chain written against
+// a DeviceBlock keeps the block on the GPU from the first stage to the last —
+//   auto dev = dopinf_b200::data::read_block_device(path, plan, rank, header);
+//   params.local_means = dopinf_b200::transform::center_in_place(dev);
+//   params.scales = dopinf_b200::transform::compute_global_scales(dev, header, comm);
+//   dopinf_b200::transform::scale_in_place(dev, params.scales);
+//   Matrix gram = dopinf_b200::pod::global_gram(dopinf_b200::pod::local_gram<Matrix>(dev), comm);
+// include/dopinf_b200_pipeline.hpp chains them into pipeline::run_rank.
+//
 // Errors: with DOPINF_B200_REFERENCE_ERRORS defined (after including the
 // reference's "dopinf/errors.hpp"), failures throw the reference classes
 // (dopinf::InvalidArgumentError, PartitionError, CollectiveError,
@@ -204,7 +215,11 @@ bool host_collectives(CommT& comm, const char* what) {
 #endif
 }  // namespace detail
 
-// Device mirror of one host LocalBlock (data.hpp:38-42).
+// Device-resident LocalBlock (data.hpp:38-42): (n_vars·nx_i) × nt on the GPU.
+// Every stage below has an overload on DeviceBlock, so the reference's stage
+// chain (pipeline.cpp:270-298) written against a DeviceBlock runs with the
+// block resident: one upload (data::to_device or data::read_block_device),
+// then only means, scales and D cross PCIe.
 class DeviceBlock {
 public:
     DeviceBlock(Context& c, std::size_t n_vars, std::size_t nx_i, std::size_t row_begin, std::size_t nt)
@@ -222,13 +237,23 @@ public:
     void upload(const double* host, std::size_t ld) {
         Context::check(dopinf_b200_block_upload(b_, host, ld), ctx_.handle(), "upload");
     }
-    void download(double* host, std::size_t ld) {
+    void download(double* host, std::size_t ld) const {
         Context::check(dopinf_b200_block_download(b_, host, ld), ctx_.handle(), "download");
     }
     dopinf_b200_block* handle() const { return b_; }
     Context& context() const { return ctx_; }
+    std::size_t n_vars() const { return shape(0); }
+    std::size_t nx_i() const { return shape(1); }
+    std::size_t row_begin() const { return shape(2); }
+    std::size_t nt() const { return shape(3); }
+    std::size_t rows() const { return n_vars() * nx_i(); }
 
 private:
+    std::size_t shape(int k) const {
+        std::size_t dims[4] = {};
+        Context::check(dopinf_b200_block_shape(b_, dims), nullptr, "block_shape");
+        return dims[k];
+    }
     Context& ctx_;
     dopinf_b200_block* b_ = nullptr;
 };
@@ -325,25 +350,34 @@ LocalBlockT read_block(const std::string& path, const PlanT& plan, int rank, con
     d.download(block.values.data(), header.nt);
     return block;
 }
+
+// A host LocalBlock's values on the device (one upload), for the resident
+// overloads below; to_host copies them back into a host block.
+template <class LocalBlockT>
+DeviceBlock to_device(const LocalBlockT& block, std::size_t n_vars) {
+    return ::dopinf_b200::detail::uploaded(block, n_vars);
+}
+template <class LocalBlockT>
+void to_host(const DeviceBlock& d, LocalBlockT& block) {
+    d.download(block.values.data(), block.values.cols());
+}
 }  // namespace data
 
 namespace transform {
-// transform.cpp:10-20
-template <class LocalBlockT>
-std::vector<double> center_in_place(LocalBlockT& block) {
-    DeviceBlock d = detail::uploaded(block, detail::n_vars_of(block));
-    std::vector<double> means(block.values.rows());
+// transform.cpp:10-20 on the resident block: returns the per-row means; the
+// subtraction is fused into the next pass over the block.
+inline std::vector<double> center_in_place(DeviceBlock& d) {
+    std::vector<double> means(d.rows());
     Context::check(dopinf_b200_center(d.handle(), means.data()), d.context().handle(), "center_in_place");
-    d.download(block.values.data(), block.values.cols());
     return means;
 }
 
-// transform.cpp:22-41 (MAX all-reduce over NCCL; `comm` must be this rank's).
-template <class LocalBlockT, class HeaderT, class CommT>
-std::vector<double> compute_global_scales(const LocalBlockT& block, const HeaderT& header, CommT& comm) {
-    const bool host = detail::host_collectives(comm, "compute_global_scales");
+// transform.cpp:22-41 (MAX over the bound Context's NCCL ranks, or over the
+// caller's Comm when every rank binds a size-1 Context).
+template <class HeaderT, class CommT>
+std::vector<double> compute_global_scales(const DeviceBlock& d, const HeaderT& header, CommT& comm) {
+    const bool host = ::dopinf_b200::detail::host_collectives(comm, "compute_global_scales");
     const std::size_t n_vars = static_cast<std::size_t>(header.n_vars);
-    DeviceBlock d = detail::uploaded(block, n_vars);
     std::vector<double> scales(n_vars);
     std::size_t bad = 0;
     int rc = DOPINF_B200_OK;
@@ -352,7 +386,8 @@ std::vector<double> compute_global_scales(const LocalBlockT& block, const Header
         // transform.cpp:28-39: local max-abs, MAX over the caller's Comm, zero check
         Context::check(dopinf_b200_local_maxabs(d.handle(), scales.data()), d.context().handle(),
                        "compute_global_scales");
-        comm.allreduce(std::span<double>(scales), static_cast<detail::ReduceOpT<CommT>>(detail::kMax));
+        comm.allreduce(std::span<double>(scales),
+                       static_cast<::dopinf_b200::detail::ReduceOpT<CommT>>(::dopinf_b200::detail::kMax));
         for (std::size_t j = 0; j < n_vars && rc == DOPINF_B200_OK; ++j) {
             if (scales[j] == 0.0) {
                 rc = DOPINF_B200_ERR_DEGENERATE_VARIABLE;
@@ -372,40 +407,66 @@ std::vector<double> compute_global_scales(const LocalBlockT& block, const Header
 }
 
 // transform.cpp:43-49
+inline void scale_in_place(DeviceBlock& d, const std::vector<double>& scales) {
+    Context::check(dopinf_b200_scale(d.handle(), scales.data()), d.context().handle(), "scale_in_place");
+}
+
+// Host-block versions: the reference's value semantics (the caller's host
+// block is mutated), through one upload and one download each.
+template <class LocalBlockT>
+std::vector<double> center_in_place(LocalBlockT& block) {
+    DeviceBlock d = ::dopinf_b200::detail::uploaded(block, ::dopinf_b200::detail::n_vars_of(block));
+    std::vector<double> means = center_in_place(d);
+    d.download(block.values.data(), block.values.cols());
+    return means;
+}
+
+template <class LocalBlockT, class HeaderT, class CommT>
+std::vector<double> compute_global_scales(const LocalBlockT& block, const HeaderT& header, CommT& comm) {
+    const DeviceBlock d = ::dopinf_b200::detail::uploaded(block, static_cast<std::size_t>(header.n_vars));
+    return compute_global_scales(d, header, comm);
+}
+
 template <class LocalBlockT>
 void scale_in_place(LocalBlockT& block, const std::vector<double>& scales) {
-    DeviceBlock d = detail::uploaded(block, scales.size());
-    Context::check(dopinf_b200_scale(d.handle(), scales.data()), d.context().handle(), "scale_in_place");
+    DeviceBlock d = ::dopinf_b200::detail::uploaded(block, scales.size());
+    scale_in_place(d, scales);
     d.download(block.values.data(), block.values.cols());
 }
 }  // namespace transform
 
 namespace pod {
-// pod.cpp:11-13: returns MatrixT (the block's values type) nt x nt.
-template <class LocalBlockT>
-auto local_gram(const LocalBlockT& block) -> std::decay_t<decltype(block.values)> {
-    using MatrixT = std::decay_t<decltype(block.values)>;
-    const std::size_t nt = block.values.cols();
-    DeviceBlock d = detail::uploaded(block, detail::n_vars_of(block));
+// pod.cpp:11-13 on the resident block: nt x nt as MatrixT (e.g. dopinf::Matrix).
+template <class MatrixT>
+MatrixT local_gram(const DeviceBlock& d) {
+    const std::size_t nt = d.nt();
     MatrixT out(nt, nt);
     Context::check(dopinf_b200_local_gram(d.handle(), out.data()), d.context().handle(), "local_gram");
     return out;
 }
 
+// pod.cpp:11-13: returns MatrixT (the block's values type) nt x nt.
+template <class LocalBlockT>
+auto local_gram(const LocalBlockT& block) -> std::decay_t<decltype(block.values)> {
+    using MatrixT = std::decay_t<decltype(block.values)>;
+    const DeviceBlock d = ::dopinf_b200::detail::uploaded(block, ::dopinf_b200::detail::n_vars_of(block));
+    return local_gram<MatrixT>(d);
+}
+
 // pod.cpp:15-18: reduces the device copy of the last local Gram of this rank.
 template <class MatrixT, class CommT>
 MatrixT global_gram(MatrixT local, CommT& comm) {
-    if (detail::host_collectives(comm, "global_gram")) {
+    if (::dopinf_b200::detail::host_collectives(comm, "global_gram")) {
 #if __cplusplus >= 202002L
         // pod.cpp:15-18 verbatim: the caller's Comm sums the local Grams
         comm.allreduce(std::span<double>(local.data(), local.rows() * local.cols()),
-                       static_cast<detail::ReduceOpT<CommT>>(detail::kSum));
+                       static_cast<::dopinf_b200::detail::ReduceOpT<CommT>>(::dopinf_b200::detail::kSum));
 #endif
         return local;
     }
     if (local.rows() != local.cols()) throw InvalidArgumentError("global_gram: local Gram is not square");
-    Context::check(dopinf_b200_global_gram(detail::ctx().handle(), local.data(), local.rows()),
-                   detail::ctx().handle(), "global_gram");
+    Context::check(dopinf_b200_global_gram(::dopinf_b200::detail::ctx().handle(), local.data(), local.rows()),
+                   ::dopinf_b200::detail::ctx().handle(), "global_gram");
     return local;
 }
 
@@ -442,9 +503,9 @@ template <class MatrixT>
 MatrixT project(const MatrixT& tr, const MatrixT& d) {
     if (tr.rows() != d.rows() || d.rows() != d.cols()) throw InvalidArgumentError("matmul_tn: row counts differ");
     MatrixT out(tr.cols(), d.cols());
-    Context::check(dopinf_b200_project_host(detail::ctx().handle(), tr.data(), d.data(), d.rows(), tr.cols(),
-                                            out.data()),
-                   detail::ctx().handle(), "project");
+    Context::check(dopinf_b200_project_host(::dopinf_b200::detail::ctx().handle(), tr.data(), d.data(), d.rows(),
+                                            tr.cols(), out.data()),
+                   ::dopinf_b200::detail::ctx().handle(), "project");
     return out;
 }
 }  // namespace pod
@@ -458,8 +519,8 @@ OutcomeT grid_search(const MatrixT& qhat, const ConfigT& config, CommT& comm) {
     // With size-1 Contexts under a wider Comm every rank evaluates all pairs
     // (same winner: the first minimum, as the reference's lowest-rank claim over
     // contiguous pair ranges) and reports the owner distribute_pairs gives it.
-    const bool host = detail::host_collectives(comm, "grid_search");
-    Context& c = detail::ctx();
+    const bool host = ::dopinf_b200::detail::host_collectives(comm, "grid_search");
+    Context& c = ::dopinf_b200::detail::ctx();
     std::vector<double> traj(config.nt_p * qhat.rows());
     double pair[2] = {0.0, 0.0}, err = 0.0, secs = 0.0;
     int owner = -1;
@@ -492,11 +553,10 @@ OutcomeT grid_search(const MatrixT& qhat, const ConfigT& config, CommT& comm) {
 }  // namespace rom_search
 
 namespace postprocess {
-// postprocess.cpp:12-34 (bit-identical order).
-template <class LocalBlockT, class MatrixT>
-MatrixT basis_rows(const LocalBlockT& block, const MatrixT& tr, const std::vector<std::size_t>& local_rows) {
-    if (block.values.cols() != tr.rows()) throw InvalidArgumentError("basis_rows: block and map disagree on nt");
-    DeviceBlock d = detail::uploaded(block, detail::n_vars_of(block));
+// postprocess.cpp:12-34 on the resident block (bit-identical order).
+template <class MatrixT>
+MatrixT basis_rows(const DeviceBlock& d, const MatrixT& tr, const std::vector<std::size_t>& local_rows) {
+    if (d.nt() != tr.rows()) throw InvalidArgumentError("basis_rows: block and map disagree on nt");
     MatrixT out(local_rows.size(), tr.cols());
     Context::check(dopinf_b200_basis_rows(d.handle(), tr.data(), tr.cols(), local_rows.data(), local_rows.size(),
                                           out.data()),
@@ -504,23 +564,34 @@ MatrixT basis_rows(const LocalBlockT& block, const MatrixT& tr, const std::vecto
     return out;
 }
 
-// Φ_r = Q · T_r (postprocess.cpp:66), DMMA tall GEMM.
 template <class LocalBlockT, class MatrixT>
-MatrixT basis(const LocalBlockT& block, const MatrixT& tr) {
-    if (block.values.cols() != tr.rows()) throw InvalidArgumentError("matmul: inner dimensions differ");
-    DeviceBlock d = detail::uploaded(block, detail::n_vars_of(block));
-    MatrixT out(block.values.rows(), tr.cols());
+MatrixT basis_rows(const LocalBlockT& block, const MatrixT& tr, const std::vector<std::size_t>& local_rows) {
+    if (block.values.cols() != tr.rows()) throw InvalidArgumentError("basis_rows: block and map disagree on nt");
+    const DeviceBlock d = ::dopinf_b200::detail::uploaded(block, ::dopinf_b200::detail::n_vars_of(block));
+    return basis_rows(d, tr, local_rows);
+}
+
+// Φ_r = Q · T_r (postprocess.cpp:66), DMMA tall GEMM.
+template <class MatrixT>
+MatrixT basis(const DeviceBlock& d, const MatrixT& tr) {
+    if (d.nt() != tr.rows()) throw InvalidArgumentError("matmul: inner dimensions differ");
+    MatrixT out(d.rows(), tr.cols());
     Context::check(dopinf_b200_basis(d.handle(), tr.data(), tr.cols(), out.data()), d.context().handle(), "basis");
     return out;
 }
 
+template <class LocalBlockT, class MatrixT>
+MatrixT basis(const LocalBlockT& block, const MatrixT& tr) {
+    if (block.values.cols() != tr.rows()) throw InvalidArgumentError("matmul: inner dimensions differ");
+    const DeviceBlock d = ::dopinf_b200::detail::uploaded(block, ::dopinf_b200::detail::n_vars_of(block));
+    return basis(d, tr);
+}
+
 // postprocess::reconstruct_probes (postprocess.cpp:36-61), bit-identical: one
 // SeriesT {probe, values} per probe whose index lies in the block's row range.
-template <class SeriesT, class LocalBlockT, class MatrixT, class ProbeSetT, class ParamsT>
-std::vector<SeriesT> reconstruct_probes(const LocalBlockT& block, const MatrixT& tr, const MatrixT& qtilde,
+template <class SeriesT, class MatrixT, class ProbeSetT, class ParamsT>
+std::vector<SeriesT> reconstruct_probes(const DeviceBlock& d, const MatrixT& tr, const MatrixT& qtilde,
                                         const ProbeSetT& probes, const ParamsT& params) {
-    const std::size_t n_vars = detail::n_vars_of(block);
-    DeviceBlock d = detail::uploaded(block, n_vars);
     std::vector<std::size_t> var, index;
     for (const auto& p : probes) {
         var.push_back(p.var);
@@ -545,28 +616,40 @@ std::vector<SeriesT> reconstruct_probes(const LocalBlockT& block, const MatrixT&
     return series;
 }
 
+template <class SeriesT, class LocalBlockT, class MatrixT, class ProbeSetT, class ParamsT>
+std::vector<SeriesT> reconstruct_probes(const LocalBlockT& block, const MatrixT& tr, const MatrixT& qtilde,
+                                        const ProbeSetT& probes, const ParamsT& params) {
+    const DeviceBlock d = ::dopinf_b200::detail::uploaded(block, ::dopinf_b200::detail::n_vars_of(block));
+    return reconstruct_probes<SeriesT>(d, tr, qtilde, probes, params);
+}
+
 // postprocess::reconstruct_field (postprocess.cpp:63-70): (Q·T_r)·Q̃ᵀ mapped back
 // with the TransformParams, (n_vars·nx_i) × nt_p; DMMA with the inverse
 // transform fused.
-template <class LocalBlockT, class MatrixT, class ParamsT>
-MatrixT reconstruct_field(const LocalBlockT& block, const MatrixT& tr, const MatrixT& qtilde, const ParamsT& params) {
-    if (block.values.cols() != tr.rows()) throw InvalidArgumentError("matmul: inner dimensions differ");
+template <class MatrixT, class ParamsT>
+MatrixT reconstruct_field(const DeviceBlock& d, const MatrixT& tr, const MatrixT& qtilde, const ParamsT& params) {
+    if (d.nt() != tr.rows()) throw InvalidArgumentError("matmul: inner dimensions differ");
     if (qtilde.cols() != tr.cols()) throw InvalidArgumentError("matmul_nt: column counts differ");
-    if (block.values.rows() != params.local_means.size()) {
+    if (d.rows() != params.local_means.size()) {
         throw InvalidArgumentError("inverse_transform_block: row count does not match the transform");
     }
-    const std::size_t n_vars = detail::n_vars_of(block);
-    if (params.scaling_enabled && params.scales.size() != n_vars) {
+    if (params.scaling_enabled && params.scales.size() != d.n_vars()) {
         throw InvalidArgumentError("reconstruct_field: scales do not match the block's variables");
     }
-    DeviceBlock d = detail::uploaded(block, n_vars);
-    MatrixT out(block.values.rows(), qtilde.rows());
+    MatrixT out(d.rows(), qtilde.rows());
     Context::check(dopinf_b200_reconstruct_field(d.handle(), tr.data(), tr.cols(), qtilde.data(), qtilde.rows(),
                                                  params.local_means.data(),
                                                  params.scaling_enabled ? params.scales.data() : nullptr,
                                                  params.scaling_enabled ? 1 : 0, out.data()),
                    d.context().handle(), "reconstruct_field");
     return out;
+}
+
+template <class LocalBlockT, class MatrixT, class ParamsT>
+MatrixT reconstruct_field(const LocalBlockT& block, const MatrixT& tr, const MatrixT& qtilde, const ParamsT& params) {
+    if (block.values.cols() != tr.rows()) throw InvalidArgumentError("matmul: inner dimensions differ");
+    const DeviceBlock d = ::dopinf_b200::detail::uploaded(block, ::dopinf_b200::detail::n_vars_of(block));
+    return reconstruct_field(d, tr, qtilde, params);
 }
 }  // namespace postprocess
 

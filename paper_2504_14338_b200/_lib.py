@@ -75,6 +75,7 @@ SIGNATURES = {
     "dopinf_b200_block_synth_oscillator_vars": (C.c_int, [_vp, C.c_int, C.c_uint64, C.c_int, C.c_double,
                                                            C.c_double, _dp]),
     "dopinf_b200_block_device": (C.c_int, [_vp, C.POINTER(_dp), _sp]),
+    "dopinf_b200_block_shape": (C.c_int, [_vp, _sp]),
     "dopinf_b200_block_synth_oscillator": (C.c_int, [_vp, C.c_uint64, C.c_int, C.c_double, C.c_double,
                                                       _dp]),
     "dopinf_b200_block_synth_lowrank": (C.c_int, [_vp, C.c_uint64, C.c_int, C.c_double]),

@@ -117,7 +117,7 @@ def build_parity_harness() -> Path | None:
     out = ROOT / "tests" / "cpp" / "_build" / "parity"
     out.parent.mkdir(parents=True, exist_ok=True)
     src = ROOT / "tests" / "cpp" / "parity_main.cpp"
-    if not _stale(out, [src, LIB, ROOT / "include" / "dopinf_b200.hpp", lib_ref]):
+    if not _stale(out, [src, LIB, ROOT / "include" / "dopinf_b200.hpp", ROOT / "include" / "dopinf_b200_pipeline.hpp", lib_ref]):
         return out
     cmd = ["g++", "-std=gnu++20", "-O2", f"-I{ROOT / 'oracle' / 'shim'}", f"-I{ref_src / 'include'}",
            f"-I{ROOT / 'include'}", str(src), str(lib_ref), f"-L{PKG}", "-ldopinf_b200",

@@ -650,6 +650,12 @@ int dopinf_b200_block_upload(dopinf_b200_block* b, const double* host, size_t ho
     auto* c = b->ctx;
     return guarded(c, [&] {
         require(host_ld >= b->nt && (b->rows == 0 || host), "block_upload: bad host buffer");
+        if (b->rows > 0 && b->rows * b->nt * sizeof(double) >= (size_t(64) << 20) && !is_pinned(host)) {
+            staged_upload(b, host, host_ld);  // records the UPLOAD stage itself
+            b->pending_center = false;
+            b->stats_valid = false;
+            return;
+        }
         c->record(DOPINF_B200_STAGE_UPLOAD, 0);
         if (b->rows > 0) {
             if (host_ld == b->ld) {
@@ -701,6 +707,15 @@ int dopinf_b200_block_download_rows(dopinf_b200_block* b, size_t row0, size_t nr
         }
         c->sync("block_download_rows");
     });
+}
+
+int dopinf_b200_block_shape(const dopinf_b200_block* b, size_t* dims) {
+    if (!b || !dims) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    dims[0] = b->n_vars;
+    dims[1] = b->nx_i;
+    dims[2] = b->row_begin;
+    dims[3] = b->nt;
+    return DOPINF_B200_OK;
 }
 
 int dopinf_b200_block_device(dopinf_b200_block* b, double** values, size_t* ld) {

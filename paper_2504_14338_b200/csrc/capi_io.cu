@@ -45,26 +45,56 @@ struct StreamSource {
     int n_modes = 0;
     double dt = 0.0, noise = 0.0;
     const double* amps = nullptr;  // host [n_vars] or null
+    bool pageable = false;         // host rows not pinned: staged through the pinned ring
     int fd = -1;                   // SNP1 file rows → pinned ring → resident block
     const Snp1* file = nullptr;
     const std::string* path = nullptr;
 };
 
-// File source: read chunk k of the block's rows into pinned ring slot k % 2
-// and enqueue its H2D on the copy stream; chunk_events[k] marks the copy done
-// (the compute stream waits on it; the read of chunk k + 2 into the same slot
-// waits on it from the host).
-void file_chunk_h2d(dopinf_b200_block* b, const StreamSource& src, const std::vector<StreamChunk>& chunks,
-                    size_t k, double* ring, size_t slot_doubles) {
+// Pageable host rows [r0, r0 + rows) (pitch sld) → dense pinned slot (pitch
+// nt) on up to file_reader_threads() threads: a pageable H2D runs through the
+// driver's staging at ~10 GB/s; parallel host copies into pinned memory plus a
+// pinned H2D run at the link rate.
+void copy_rows_parallel(double* dst, const double* src, size_t sld, size_t nt, long long rows) {
+    const size_t total = static_cast<size_t>(rows) * nt;
+    const int n = static_cast<int>(std::min<size_t>(file_reader_threads(), std::max<size_t>(1, total >> 20)));
+    auto part = [&](int i) {
+        const long long a = rows * i / n, e = rows * (i + 1) / n;
+        if (sld == nt) {
+            std::memcpy(dst + a * nt, src + a * nt, static_cast<size_t>(e - a) * nt * sizeof(double));
+        } else {
+            for (long long r = a; r < e; ++r) std::memcpy(dst + r * nt, src + r * sld, nt * sizeof(double));
+        }
+    };
+    if (n <= 1) {
+        part(0);
+        return;
+    }
+    std::vector<std::thread> threads;
+    for (int i = 1; i < n; ++i) threads.emplace_back(part, i);
+    part(0);
+    for (auto& t : threads) t.join();
+}
+
+// Staged source (SNP1 file or pageable host rows): fill pinned ring slot k % 2
+// with chunk k of the block's rows and enqueue its H2D on the copy stream;
+// chunk_events[k] marks the copy done (the compute stream waits on it; filling
+// chunk k + 2 into the same slot waits on it from the host).
+void staged_chunk_h2d(dopinf_b200_block* b, const StreamSource& src, const std::vector<StreamChunk>& chunks,
+                      size_t k, double* ring, size_t slot_doubles) {
     auto* c = b->ctx;
     const StreamChunk& ch = chunks[k];
     if (k >= 2) ck(cudaEventSynchronize(c->chunk_events[k - 2]), "ring slot");
     double* slot = ring + (k % 2) * slot_doubles;
-    const uint64_t local0 = static_cast<uint64_t>(ch.r0) - static_cast<uint64_t>(ch.var) * b->nx_i;
-    const uint64_t first = static_cast<uint64_t>(ch.var) * src.file->nx + b->row_begin + local0;
-    const size_t bytes = static_cast<size_t>(ch.rows) * b->nt * sizeof(double);
-    if (!pread_parallel(src.fd, slot, bytes, src.file->data_offset + first * b->nt * sizeof(double))) {
-        format_fail("snapshot file truncated in variable '" + src.file->names[ch.var] + "': " + *src.path);
+    if (src.fd >= 0) {
+        const uint64_t local0 = static_cast<uint64_t>(ch.r0) - static_cast<uint64_t>(ch.var) * b->nx_i;
+        const uint64_t first = static_cast<uint64_t>(ch.var) * src.file->nx + b->row_begin + local0;
+        const size_t bytes = static_cast<size_t>(ch.rows) * b->nt * sizeof(double);
+        if (!pread_parallel(src.fd, slot, bytes, src.file->data_offset + first * b->nt * sizeof(double))) {
+            format_fail("snapshot file truncated in variable '" + src.file->names[ch.var] + "': " + *src.path);
+        }
+    } else {
+        copy_rows_parallel(slot, src.host + static_cast<size_t>(ch.r0) * src.host_ld, src.host_ld, b->nt, ch.rows);
     }
     ck(copy_rows(b->q + ch.r0 * b->ld, b->ld, slot, b->nt, b->nt, ch.rows, cudaMemcpyHostToDevice, c->copy_stream),
        "chunk H2D");
@@ -137,9 +167,9 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
     double* packed = c->packed.get<double>(count + 1, "packed");  // + status slot (0)
     double* ring = src.synth ? c->ring.get<double>(2 * static_cast<size_t>(first_rows) * b->ld, "chunk ring")
                              : nullptr;
-    const bool from_file = src.fd >= 0;
+    const bool staged = src.fd >= 0 || src.pageable;  // through the pinned ring
     const size_t slot_doubles = static_cast<size_t>(first_rows) * b->nt;
-    double* fring = from_file && !chunks.empty()
+    double* fring = staged && !chunks.empty()
                         ? static_cast<double*>(c->file_ring.get(2 * slot_doubles * sizeof(double)))
                         : nullptr;
     std::vector<double> amps_v;  // per-variable amplitude slice for the generator
@@ -155,8 +185,8 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
         cudaEvent_t ready = c->chunk_events[chunks.size()];
         ck(cudaEventRecord(ready, c->stream), "event");
         ck(cudaStreamWaitEvent(c->copy_stream, ready, 0), "event wait");
-        if (from_file && !chunks.empty()) file_chunk_h2d(b, src, chunks, 0, fring, slot_doubles);
-        for (size_t k = 0; !from_file && k < chunks.size(); ++k) {
+        if (staged && !chunks.empty()) staged_chunk_h2d(b, src, chunks, 0, fring, slot_doubles);
+        for (size_t k = 0; !staged && k < chunks.size(); ++k) {
             const StreamChunk& ch = chunks[k];
             ck(copy_rows(b->q + ch.r0 * b->ld, b->ld, src.host + ch.r0 * src.host_ld, src.host_ld, b->nt, ch.rows,
                          cudaMemcpyHostToDevice, c->copy_stream),
@@ -250,10 +280,10 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
             }
         }
         // the host reads chunk k + 1 while the device copies and reduces chunk k
-        if (from_file && k + 1 < chunks.size()) file_chunk_h2d(b, src, chunks, k + 1, fring, slot_doubles);
+        if (staged && k + 1 < chunks.size()) staged_chunk_h2d(b, src, chunks, k + 1, fring, slot_doubles);
     }
     // the pinned ring is free for the next call once the last copy has landed
-    if (from_file && !chunks.empty()) ck(cudaEventSynchronize(c->chunk_events[chunks.size() - 1]), "ring");
+    if (staged && !chunks.empty()) ck(cudaEventSynchronize(c->chunk_events[chunks.size() - 1]), "ring");
     if (b->rows == 0 && scaling) {  // an empty rank still joins the MAX collectives
         for (size_t v = 0; v < b->n_vars; ++v) {
             if (coll(c)) {
@@ -304,7 +334,7 @@ void do_block_read(dopinf_b200_block* b, const StreamSource& src) {
     cudaEvent_t ready = c->chunk_events[chunks.size()];
     ck(cudaEventRecord(ready, c->stream), "event");
     ck(cudaStreamWaitEvent(c->copy_stream, ready, 0), "event wait");
-    for (size_t k = 0; k < chunks.size(); ++k) file_chunk_h2d(b, src, chunks, k, fring, slot_doubles);
+    for (size_t k = 0; k < chunks.size(); ++k) staged_chunk_h2d(b, src, chunks, k, fring, slot_doubles);
     ck(cudaStreamWaitEvent(c->stream, c->chunk_events[chunks.size() - 1], 0), "event wait");
     c->record(DOPINF_B200_STAGE_UPLOAD, 1);
     ck(cudaEventSynchronize(c->chunk_events[chunks.size() - 1]), "ring");
@@ -330,6 +360,17 @@ dopinf_b200_block* open_file_block(dopinf_b200_ctx* c, const char* path, size_t 
 }
 
 }  // namespace
+
+// Block upload from pageable host rows through the pinned ring (parallel host
+// copies ‖ pinned H2D): several times the driver's pageable copy rate.
+void staged_upload(dopinf_b200_block* b, const double* host, size_t host_ld) {
+    StreamSource src;
+    src.host = host;
+    src.host_ld = host_ld;
+    src.pageable = true;
+    do_block_read(b, src);
+}
+
 
 // Exactly `bytes` at `off`, or false (EOF / error).
 bool pread_all(int fd, void* dst, size_t bytes, uint64_t off) {
@@ -457,6 +498,7 @@ int dopinf_b200_snapshot_pass_host(dopinf_b200_block* b, const double* host, siz
         StreamSource src;
         src.host = host;
         src.host_ld = host_ld;
+        src.pageable = b->rows > 0 && !is_pinned(host);
         do_stream_pass(b, src, scaling != 0, means, scales);
         do_global_gram(c, d);
         c->sync("snapshot_pass_host");

@@ -15,7 +15,9 @@
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
+#include <fstream>
 #include <functional>
+#include <iterator>
 #include <string>
 #include <vector>
 
@@ -33,6 +35,7 @@
 
 #define DOPINF_B200_REFERENCE_ERRORS 1
 #include "dopinf_b200.hpp"
+#include "dopinf_b200_pipeline.hpp"
 
 using namespace dopinf;
 
@@ -855,7 +858,126 @@ int main() {
                         t_pass + t_eig + t_search + t_post, t_pass, t_eig, t_search, t_post);
         }
         g_gpu->set_gram_order(DOPINF_B200_GRAM_ORDER_TENSOR);
+
+        // 7. The drop-in pipeline (include/dopinf_b200_pipeline.hpp) in place of
+        //    pipeline::run on the same config: with the reference-order Gram every
+        //    artifact but timings.csv and the field file is the reference's byte for
+        //    byte, at one rank (the streamed file pass) and at three in-process ranks
+        //    (size-1 contexts, the reference Comm's MAX and ascending-rank SUM).
+        for (int workers : {1, 3}) {
+            pipeline::PipelineConfig c2 = cfg;
+            c2.workers = workers;
+            c2.out_dir = (dir / ("ref_w" + std::to_string(workers))).string();
+            auto ta = clk::now();
+            const pipeline::RunResult rr = workers == 1 ? refrun : pipeline::run(c2);
+            const double t_ref = workers == 1 ? ref_total : secs(ta);
+            const std::string ref_dir = workers == 1 ? cfg.out_dir : c2.out_dir;
+            c2.out_dir = (dir / ("dropin_w" + std::to_string(workers))).string();
+            dopinf_b200::pipeline::Options opt;
+            opt.gram_order = DOPINF_B200_GRAM_ORDER_REFERENCE;
+            ta = clk::now();
+            const pipeline::RunResult dr = dopinf_b200::pipeline::run(c2, opt);
+            const double t_drop = secs(ta);
+            auto bytes = [](const fs::path& f) {
+                std::ifstream in(f, std::ios::binary);
+                return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+            };
+            std::string differ;
+            std::size_t n_same = 0;
+            for (const auto& e : fs::directory_iterator(ref_dir)) {
+                const std::string name = e.path().filename().string();
+                if (name == "timings.csv" || name.rfind("field_rank", 0) == 0) continue;
+                std::string want = bytes(e.path()), got = bytes(fs::path(c2.out_dir) / name);
+                if (name == "resolved.cfg") {  // the out = line names each run's directory
+                    want = want.substr(0, want.rfind("out = "));
+                    got = got.substr(0, got.rfind("out = "));
+                }
+                if (want == got) {
+                    ++n_same;
+                } else {
+                    differ += name + " ";
+                }
+            }
+            double fgap = 0.0;
+            for (int r = 0; r < workers; ++r) {
+                const std::string f = "field_rank" + std::to_string(r) + ".snp1";
+                const data::SnapshotHeader fh = data::read_header((fs::path(ref_dir) / f).string());
+                const data::PartitionPlan one = data::partition_rows(fh.nx, 1);
+                fgap = std::max(fgap, rel_frob(data::read_block((fs::path(c2.out_dir) / f).string(), one, 0, fh).values,
+                                               data::read_block((fs::path(ref_dir) / f).string(), one, 0, fh).values));
+            }
+            const bool same = differ.empty() && dr.r == rr.r && dr.pair_opt == rr.pair_opt && dr.train_err == rr.train_err;
+            report(same && fgap <= 1e-10,
+                   "config 1: dopinf_b200::pipeline::run in place of pipeline::run, workers = " + std::to_string(workers),
+                   std::to_string(n_same) + " artifacts byte-identical" + (differ.empty() ? "" : ", DIFFER: " + differ) +
+                       "; field files rel " + fmt(fgap) + " <= 1e-10; reference " + fmt(t_ref) + " s, drop-in " +
+                       fmt(t_drop) + " s");
+            const double* st = dr.stage_seconds.data();
+            std::printf("TIMING config1 drop-in pipeline workers=%d: %.3f s (rank 0: load %.3f transform %.3f "
+                        "gram_reduce %.3f eig_project %.3f search %.3f postprocess %.3f); reference %.3f s\n",
+                        workers, t_drop, st[0], st[1], st[2], st[3], st[4], st[5], t_ref);
+        }
         fs::remove_all(dir);
+    }
+
+    // 8. BASELINE config 2 (4 vars × 262,144 points, K = 1200) through the C++
+    //    mirror's stage chain (pipeline.cpp:270-280) three ways, timed on the host
+    //    clock around the synchronous calls: the reference-signature host-block
+    //    functions (value semantics: the block crosses PCIe per stage), the same
+    //    chain on a DeviceBlock (one upload, then resident), and the fused
+    //    streamed pass (dopinf_b200_snapshot_pass_host, H2D overlapped with the
+    //    transform and the Gram). All three give the same means, scales and D.
+    if (!std::getenv("DOPINF_PARITY_SKIP_C2")) {
+        using clk = std::chrono::steady_clock;
+        auto secs = [](clk::time_point a) { return std::chrono::duration<double>(clk::now() - a).count(); };
+        const std::size_t nv = 4, nx = 262144, nt = 1200;
+        data::LocalBlock host;
+        host.row_range = {0, nx};
+        host.values = Matrix(nv * nx, nt);
+        {
+            dopinf_b200::DeviceBlock gen(*g_gpu, nv, nx, 0, nt);
+            dopinf_b200::Context::check(dopinf_b200_block_synth_oscillator(gen.handle(), 2, 40, 1e-3, 1e-4, nullptr),
+                                        g_gpu->handle(), "synth");
+            gen.download(host.values.data(), nt);
+        }
+        const data::SnapshotHeader h = header_for(nv, nx, nt);
+        std::vector<double> m0, s0, m1, s1, m2(nv * nx), s2(nv);
+        Matrix d0, d1, d2(nt, nt);
+        double t_host = 0, t_dev = 0, t_fused = 0, t_upload = 0;
+        comm::run_on_workers(1, [&](comm::Comm& c) {
+            dopinf_b200::Bind bind(*g_gpu);
+            for (int rep = 0; rep < 2; ++rep) {  // second repetition timed (first: allocations, page-in)
+                data::LocalBlock b = host;
+                auto t0 = clk::now();
+                m0 = dopinf_b200::transform::center_in_place(b);
+                s0 = dopinf_b200::transform::compute_global_scales(b, h, c);
+                dopinf_b200::transform::scale_in_place(b, s0);
+                d0 = dopinf_b200::pod::global_gram(dopinf_b200::pod::local_gram(b), c);
+                t_host = secs(t0);
+                t0 = clk::now();
+                dopinf_b200::DeviceBlock dev = dopinf_b200::data::to_device(host, nv);
+                t_upload = secs(t0);
+                m1 = dopinf_b200::transform::center_in_place(dev);
+                s1 = dopinf_b200::transform::compute_global_scales(dev, h, c);
+                dopinf_b200::transform::scale_in_place(dev, s1);
+                d1 = dopinf_b200::pod::global_gram(dopinf_b200::pod::local_gram<Matrix>(dev), c);
+                t_dev = secs(t0);
+                dopinf_b200::DeviceBlock dev2(*g_gpu, nv, nx, 0, nt);
+                t0 = clk::now();
+                dopinf_b200::Context::check(dopinf_b200_snapshot_pass_host(dev2.handle(), host.values.data(), nt, 1,
+                                                                           m2.data(), s2.data(), d2.data()),
+                                            g_gpu->handle(), "snapshot_pass_host");
+                t_fused = secs(t0);
+            }
+        });
+        const bool same = m0 == m1 && m1 == m2 && s0 == s1 && s1 == s2 && d0 == d1 && rel_frob(d2, d1) <= 1e-12;
+        report(same, "config 2 stage chain: host-block mirror, DeviceBlock mirror and fused pass agree",
+               "means and scales bitwise, D bitwise (host/DeviceBlock) and rel " + fmt(rel_frob(d2, d1)) +
+                   " (fused: per-variable Grams)");
+        std::printf("TIMING config2 Steps II-III from a pageable host block (10.1 GB): host-block mirror chain %.3f s; "
+                    "DeviceBlock chain %.3f s (upload %.3f s + resident stages %.3f s); fused snapshot_pass_host "
+                    "%.3f s\n",
+                    t_host, t_dev, t_upload, t_dev - t_upload, t_fused);
     }
 
     std::printf("parity: %s\n", g_fail == 0 ? "all checks passed" : "FAILURES");
