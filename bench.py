@@ -357,16 +357,121 @@ def run_ours(args, wl):
     return 0
 
 
+# ---- config 1: the whole pipeline (Steps I-V) --------------------------------------------------------
+def run_pipeline_workload(args):
+    """BASELINE config 1 ("full dOpInf pipeline, single rank"): wall time of
+    Steps I-V from an SNP1 file through the B200 chain (streamed file pass,
+    device eigensolve, projection, device grid search, probes, streamed field
+    file) beside the reference's pipeline::run on the same file, plus the
+    device dsyevd against the reference's LAPACK dsyev at K = 600 and 1200.
+    Prints one JSON line (a secondary workload: the bench metric line is
+    config 2's)."""
+    import torch
+
+    from paper_2504_14338_b200 import api
+
+    nv, nx, nt, r, nt_p = 2, 16384, 600, 10, 1200
+    b1 = b2 = api.logspace(1e-6, 1e2, 8)
+    probes = [(0, 0), (0, 5000), (1, 9999), (1, 16383)]
+    work = Path(tempfile.mkdtemp(prefix="dopinf_c1_"))
+    ctx = api.DeviceContext(0)
+    gen = api.LocalBlock(ctx, nv, api.RowRange(0, nx), nt)
+    gen.synth_oscillator(seed=1, n_modes=20, dt=1e-3, noise=1e-3)
+    raw = gen.values
+    gen.close()
+    header = api.SnapshotHeader(nv, nx, nt, ["var0", "var1"])
+    data = str(work / "c1.snp1")
+    api.write_snapshots(data, header, [raw[:nx], raw[nx:]])
+    plan = api.partition_rows(nx, 1)
+    cfg = api.SearchConfig(b1, b2, 1.2, nt_p)
+    pr = [api.Probe(v, i) for v, i in probes]
+
+    def ours():
+        t = [time.perf_counter()]
+        blk, params, d = api.snapshot_pass_file(data, plan, 0, header, ctx, scaling=True)
+        t.append(time.perf_counter())
+        api.eig_sym_desc(ctx, vectors=False)
+        api.reduced_map(ctx, r, download=False)
+        api.project_resident(ctx, None, r=r)
+        t.append(time.perf_counter())
+        out = api.grid_search(None, cfg, ctx, r=r, nt=nt)
+        t.append(time.perf_counter())
+        api.reconstruct_probes(blk, None, out.trajectory, pr, params, r=r)
+        api.write_field(blk, None, out.trajectory, params, header.var_names, str(work / "field_rank0.snp1"), r=r)
+        t.append(time.perf_counter())
+        blk.close()
+        return np.diff(t), out
+
+    for _ in range(max(args.warmup, 1)):
+        ours()
+    runs = [ours() for _ in range(args.steps)]
+    st = np.median(np.array([x[0] for x in runs]), axis=0)
+    pair = runs[-1][1].pair_opt
+    line = {"workload": "config1-pipeline: 2 vars x 16384 pts, K=600, r=10, 8x8 (b1, b2) in [1e-6, 1e2], "
+                        "nt_p=1200, 4 probes, field file",
+            "metric": "dOpInf pipeline wall time, Steps I-V from an SNP1 file", "unit": "s",
+            "higher_is_better": False, "steps": args.steps, "warmup": args.warmup,
+            "value": round(float(st.sum()), 4),
+            "stages_s": {"file+transform+gram (I-III)": round(float(st[0]), 4),
+                         "eig+reduced_map+project (III)": round(float(st[1]), 4),
+                         "grid_search (IV)": round(float(st[2]), 4),
+                         "probes+field file (V)": round(float(st[3]), 4)},
+            "chain": "snapshot_pass_file -> eig_sym_desc (cuSOLVER dsyevd) -> reduced_map -> project -> "
+                     "grid_search (device) -> reconstruct_probes -> write_field", "pair": list(pair)}
+    # the device eigensolve against the reference's dsyev at K = 600 (this D) and 1200 (config 2's)
+    eig = {}
+    from oracle.cpu import Reference
+
+    have_ref = Reference.available()
+    ref = Reference() if have_ref else None
+    for K, (nvk, nxk, modes, noise, seed) in ((600, (2, 16384, 20, 1e-3, 1)), (1200, (4, 262144, 40, 1e-4, 2))):
+        blk = api.LocalBlock(ctx, nvk, api.RowRange(0, nxk), K)
+        blk.synth_oscillator(seed=seed, n_modes=modes, dt=1e-3, noise=noise)
+        _, d = api.snapshot_pass(blk, scaling=True)
+        blk.close()
+        times = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            api.eig_sym_desc(ctx, vectors=True)
+            times.append(time.perf_counter() - t0)
+        eig[f"K={K}"] = {"device_dsyevd_s": round(min(times), 4)}
+        if ref is not None:
+            t0 = time.perf_counter()
+            ref.eig_reduced_map(d, 10)
+            eig[f"K={K}"]["reference_dsyev_s"] = round(time.perf_counter() - t0, 4)
+    line["eig"] = eig
+    if ref is not None:
+        for workers in (1, os.cpu_count() or 1):
+            t0 = time.perf_counter()
+            stages, res = ref.pipeline_run(data, work / f"ref_w{workers}", workers, r, True, b1, b2, 1.2, nt_p, probes)
+            line[f"reference_pipeline_run_workers{workers}"] = {
+                "wall_s": round(time.perf_counter() - t0, 4),
+                "stages_s": dict(zip(["load", "transform", "gram_reduce", "eig_project", "search", "postprocess"],
+                                     [round(float(x), 4) for x in stages])),
+                "pair": [res[1], res[2]]}
+        line["reference_kind"] = "compiled reference (oracle/_ref), OPENBLAS_NUM_THREADS=1 as its CLI"
+    ctx.close()
+    import shutil
+
+    shutil.rmtree(work, ignore_errors=True)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["c1-pipeline"], default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.workload == "c1-pipeline":
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+        return run_pipeline_workload(args)
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference_arm(args, wl)

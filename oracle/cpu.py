@@ -318,6 +318,8 @@ class Reference:
             lib.ref_eig_reduced_map.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, _dp]
             lib.ref_grid_search.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp, C.c_size_t,
                                             C.c_double, C.c_size_t, _dp, _dp]
+            lib.ref_pipeline_run.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_long, C.c_int, _dp, C.c_size_t, _dp,
+                                             C.c_size_t, C.c_double, C.c_size_t, _sp, _sp, C.c_size_t, _dp, _dp]
             lib.ref_write_snapshots.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_char_p, _dp]
             lib.ref_read_header.argtypes = [C.c_char_p, _sp, C.c_char_p, C.c_size_t]
             lib.ref_read_block.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
@@ -452,6 +454,17 @@ class Reference:
         return a, f, c
 
     # ---- data.cpp: SNP1 container ---------------------------------------------------
+    def pipeline_run(self, path, out_dir, workers, fixed_rank, scaling, b1, b2, max_growth, nt_p, probes):
+        """pipeline::run (pipeline.cpp:400-414) -> (stage_seconds[6] of rank 0, (r, beta1, beta2, train_err))."""
+        b1, b2 = _f(b1), _f(b2)
+        pv = np.ascontiguousarray([p[0] for p in probes], dtype=np.uintp)
+        pi = np.ascontiguousarray([p[1] for p in probes], dtype=np.uintp)
+        st, res = np.zeros(6), np.zeros(4)
+        self._ok(self.lib.ref_pipeline_run(os.fsencode(str(path)), os.fsencode(str(out_dir)), workers, fixed_rank,
+                                           1 if scaling else 0, _d(b1), b1.size, _d(b2), b2.size, max_growth, nt_p,
+                                           pv.ctypes.data_as(_sp), pi.ctypes.data_as(_sp), pv.size, _d(st), _d(res)))
+        return st, (int(res[0]), float(res[1]), float(res[2]), float(res[3]))
+
     def write_snapshots(self, path, names, variables):
         """data::write_snapshots (data.cpp:105-131)."""
         full = _f(np.concatenate([np.asarray(v, dtype=np.float64) for v in variables], axis=0))

@@ -435,3 +435,42 @@ int ref_reconstruct_probes(const double* q, std::size_t n_vars, std::size_t nx_i
 }
 
 }  // extern "C"
+
+#include "dopinf/pipeline.hpp"
+
+extern "C" {
+
+// pipeline::run (pipeline.cpp:400-414), Steps I–V from the SNP1 file `path`
+// into out_dir: scaling on, r = fixed_rank (0: energy 0.9995), an n1 × n2
+// (β1, β2) grid, max_growth, nt_p, the probes (var, index). stage_seconds
+// receives rank 0's six stage times (load, transform, gram_reduce,
+// eig_project, search, postprocess); result = {r, beta1, beta2, train_err}.
+int ref_pipeline_run(const char* path, const char* out_dir, int workers, long fixed_rank, int scaling,
+                     const double* b1, std::size_t n1, const double* b2, std::size_t n2, double max_growth,
+                     std::size_t nt_p, const std::size_t* probe_var, const std::size_t* probe_index,
+                     std::size_t n_probes, double* stage_seconds, double* result) {
+    try {
+        pipeline::PipelineConfig cfg;
+        cfg.data_path = path;
+        cfg.out_dir = out_dir;
+        cfg.workers = workers;
+        cfg.fixed_rank = fixed_rank;
+        cfg.scaling = scaling != 0;
+        cfg.b1.assign(b1, b1 + n1);
+        cfg.b2.assign(b2, b2 + n2);
+        cfg.max_growth = max_growth;
+        cfg.nt_p = nt_p;
+        for (std::size_t i = 0; i < n_probes; ++i) cfg.probes.push_back({probe_var[i], probe_index[i]});
+        const pipeline::RunResult res = pipeline::run(cfg);
+        for (std::size_t s = 0; s < pipeline::kStageCount; ++s) stage_seconds[s] = res.stage_seconds[s];
+        result[0] = static_cast<double>(res.r);
+        result[1] = res.pair_opt.beta1;
+        result[2] = res.pair_opt.beta2;
+        result[3] = res.train_err;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+}  // extern "C"

@@ -682,7 +682,9 @@ int dopinf_b200_block_download(dopinf_b200_block* b, double* host, size_t host_l
         require(host_ld >= b->nt && (b->rows == 0 || host), "block_download: bad host buffer");
         materialize(b);
         c->record(DOPINF_B200_STAGE_DOWNLOAD, 0);
-        if (b->rows > 0) {
+        if (b->rows > 0 && b->rows * b->nt * sizeof(double) >= (size_t(64) << 20) && !is_pinned(host)) {
+            staged_download(b, 0, b->rows, host, host_ld);
+        } else if (b->rows > 0) {
             ck(cudaMemcpy2DAsync(host, host_ld * sizeof(double), b->q, b->ld * sizeof(double),
                                  b->nt * sizeof(double), b->rows, cudaMemcpyDeviceToHost, c->stream),
                "download");
@@ -700,7 +702,9 @@ int dopinf_b200_block_download_rows(dopinf_b200_block* b, size_t row0, size_t nr
         require(host_ld >= b->nt && (nrows == 0 || host), "block_download_rows: bad host buffer");
         require(row0 <= b->rows && nrows <= b->rows - row0, "block_download_rows: rows outside the block");
         materialize(b);
-        if (nrows > 0) {
+        if (nrows * b->nt * sizeof(double) >= (size_t(64) << 20) && !is_pinned(host)) {
+            staged_download(b, row0, nrows, host, host_ld);
+        } else if (nrows > 0) {
             ck(cudaMemcpy2DAsync(host, host_ld * sizeof(double), b->q + row0 * b->ld, b->ld * sizeof(double),
                                  b->nt * sizeof(double), nrows, cudaMemcpyDeviceToHost, c->stream),
                "download");

@@ -411,6 +411,7 @@ void do_local_gram(dopinf_b200_block* b, double* d_host);
 void do_global_gram(dopinf_b200_ctx* c, double* d_host, const std::optional<Fail>& local_failure = std::nullopt);
 bool pread_all(int fd, void* dst, size_t bytes, uint64_t off);
 void staged_upload(dopinf_b200_block* b, const double* host, size_t host_ld);
+void staged_download(dopinf_b200_block* b, size_t row0, size_t nrows, double* host, size_t host_ld);
 void open_snp1(Fd& f, const std::string& path);
 void validate_snp1(const Snp1& h);
 void check_snp1_payload(const Snp1& h, const std::string& path);

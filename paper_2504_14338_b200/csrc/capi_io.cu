@@ -361,6 +361,47 @@ dopinf_b200_block* open_file_block(dopinf_b200_ctx* c, const char* path, size_t 
 
 }  // namespace
 
+// Rows [row0, row0 + nrows) of the materialised block to pageable host memory
+// through the pinned ring: the D2H of one slot overlaps the parallel copy out
+// of the other.
+void staged_download(dopinf_b200_block* b, size_t row0, size_t nrows, double* host, size_t host_ld) {
+    auto* c = b->ctx;
+    const size_t chunk = static_cast<size_t>(kStreamChunkRows);
+    const size_t slot_doubles = std::min(chunk, nrows) * b->nt;
+    auto* ring = static_cast<double*>(c->file_ring.get(2 * slot_doubles * sizeof(double)));
+    const size_t n = (nrows + chunk - 1) / chunk;
+    ensure_events(c->chunk_events, 2);
+    auto d2h = [&](size_t k) {
+        const size_t r0 = k * chunk, rows = std::min(chunk, nrows - r0);
+        ck(copy_rows(ring + (k % 2) * slot_doubles, b->nt, b->q + (row0 + r0) * b->ld, b->ld, b->nt, rows,
+                     cudaMemcpyDeviceToHost, c->stream),
+           "download");
+        ck(cudaEventRecord(c->chunk_events[k % 2], c->stream), "event");
+    };
+    if (n > 0) d2h(0);
+    for (size_t k = 0; k < n; ++k) {
+        if (k + 1 < n) d2h(k + 1);
+        ck(cudaEventSynchronize(c->chunk_events[k % 2]), "download");
+        const size_t r0 = k * chunk, rows = std::min(chunk, nrows - r0);
+        const double* slot = ring + (k % 2) * slot_doubles;
+        // slot (pitch nt) -> host rows (pitch host_ld): the same parallel copy, mirrored
+        const int th = static_cast<int>(std::min<size_t>(file_reader_threads(), std::max<size_t>(1, rows * b->nt >> 20)));
+        auto part = [&](int i) {
+            const size_t a = rows * i / th, e = rows * (i + 1) / th;
+            if (host_ld == b->nt) {
+                std::memcpy(host + (r0 + a) * host_ld, slot + a * b->nt, (e - a) * b->nt * sizeof(double));
+            } else {
+                for (size_t r = a; r < e; ++r)
+                    std::memcpy(host + (r0 + r) * host_ld, slot + r * b->nt, b->nt * sizeof(double));
+            }
+        };
+        std::vector<std::thread> threads;
+        for (int i = 1; i < th; ++i) threads.emplace_back(part, i);
+        part(0);
+        for (auto& t : threads) t.join();
+    }
+}
+
 // Block upload from pageable host rows through the pinned ring (parallel host
 // copies ‖ pinned H2D): several times the driver's pageable copy rate.
 void staged_upload(dopinf_b200_block* b, const double* host, size_t host_ld) {
