@@ -128,6 +128,9 @@ typedef enum dopinf_b200_stage {
 #define DOPINF_B200_INJECT_STALL 1 /* the next collective is followed on the stream by a
                                     * device stall the library releases only when it
                                     * aborts: drives the timeout → abort → poison path */
+#define DOPINF_B200_INJECT_OOB_STORE 2 /* one device store just past a library buffer, now
+                                        * (guarded allocations only): the positive control
+                                        * of dopinf_b200_debug_guard_violations */
 
 typedef struct dopinf_b200_ctx dopinf_b200_ctx;
 typedef struct dopinf_b200_block dopinf_b200_block;
@@ -190,6 +193,12 @@ int dopinf_b200_ctx_poisoned(const dopinf_b200_ctx* ctx);
  * msg when rank `rank` sees a disagreement. */
 int dopinf_b200_check_uniform(const long long* table, int p, int rank, const char* what, char* msg,
                               size_t msg_cap);
+/* Guarded allocations (debug aid in place of compute-sanitizer's memcheck):
+ * with the environment variable DOPINF_B200_GUARD_BYTES=G, every device buffer
+ * the library allocates is bracketed by G bytes of a known pattern. Returns
+ * the number of buffers whose guards were found overwritten (freed ones
+ * included), or -1 when guards are off. */
+long long dopinf_b200_debug_guard_violations(void);
 /* Fault injection for tests (DOPINF_B200_INJECT_*; 0 clears). */
 int dopinf_b200_debug_inject(dopinf_b200_ctx* ctx, int what);
 /* The combine step of the ORDERED reduction on the device: out = parts[0] +

@@ -28,6 +28,7 @@ ERR_NO_ADMISSIBLE_PAIR = 11
 SUM, MAX, MIN = 0, 1, 2
 CTX_NCCL = 1
 INJECT_STALL = 1
+INJECT_OOB_STORE = 2
 GRAM_REDUCE_ORDERED, GRAM_REDUCE_NCCL = 0, 1
 GRAM_ORDER_TENSOR, GRAM_ORDER_REFERENCE = 0, 1
 
@@ -54,6 +55,7 @@ SIGNATURES = {
     "dopinf_b200_check_uniform": (C.c_int, [C.POINTER(C.c_longlong), C.c_int, C.c_int, C.c_char_p, C.c_char_p,
                                             C.c_size_t]),
     "dopinf_b200_debug_inject": (C.c_int, [_vp, C.c_int]),
+    "dopinf_b200_debug_guard_violations": (C.c_longlong, []),
     "dopinf_b200_ordered_sum": (C.c_int, [_vp, _dp, C.c_int, C.c_size_t, _dp]),
     "dopinf_b200_ctx_destroy": (None, [_vp]),
     "dopinf_b200_ctx_rank": (C.c_int, [_vp]),

@@ -613,7 +613,7 @@ int dopinf_b200_block_create(dopinf_b200_ctx* c, size_t n_vars, size_t nx_i, siz
         require(b->rows < (size_t(1) << 31), "block_create: blocks of 2^31 rows or more are not supported "
                                              "(TMA row coordinates are 32-bit); shard over more ranks");
         if (b->rows > 0) {
-            ck(cudaMalloc(&b->q, b->rows * b->ld * sizeof(double)), "block values");
+            ck(dev_alloc(reinterpret_cast<void**>(&b->q), b->rows * b->ld * sizeof(double)), "block values");
             if (b->ld != nt) {
                 ck(cudaMemsetAsync(b->q, 0, b->rows * b->ld * sizeof(double), c->stream), "memset");
             }
@@ -622,7 +622,7 @@ int dopinf_b200_block_create(dopinf_b200_ctx* c, size_t n_vars, size_t nx_i, siz
         c->sync("block_create");
     });
     if (rc != DOPINF_B200_OK) {
-        if (b->q) cudaFree(b->q);
+        if (b->q) dev_free(b->q);
         delete b;
         return rc;
     }
@@ -636,7 +636,7 @@ void dopinf_b200_block_destroy(dopinf_b200_block* b) {
     cudaGetDevice(&prev);
     cudaSetDevice(b->ctx->device);
     cudaStreamSynchronize(b->ctx->stream);
-    if (b->q) cudaFree(b->q);
+    if (b->q) dev_free(b->q);
     b->means.release();
     b->varmax.release();
     b->phi.release();

@@ -19,6 +19,7 @@
 #include "capi_internal.h"
 
 #include <chrono>
+#include <map>
 
 namespace dopinf_b200 {
 namespace capi {
@@ -38,6 +39,9 @@ __global__ void stall_kernel(volatile int* flag, unsigned long long max_ns) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     } while (*flag == 0 && t - t0 < max_ns);
 }
+
+// Positive control of the guarded allocations: one store just past a buffer.
+__global__ void poke_kernel(double* p) { *p = 1.0; }
 
 // Tags of verify_uniform: the op for an all-reduce, the root for a broadcast.
 constexpr long long kTagAllgather = 100, kTagBroadcast = 200;
@@ -162,6 +166,77 @@ void join_stream(dopinf_b200_ctx* c, cudaStream_t s) {
     cudaGetLastError();
 }
 
+// ---- guarded allocations ----------------------------------------------------------
+namespace {
+constexpr unsigned char kGuardByte = 0xA5;
+std::mutex g_guard_mu;
+std::map<void*, size_t> g_guarded;  // user pointer -> user bytes
+std::atomic<long long> g_guard_violations{0};
+
+bool guard_intact(void* user, size_t bytes) {
+    const size_t g = guard_bytes();
+    std::vector<unsigned char> h(2 * g);
+    char* base = static_cast<char*>(user) - g;
+    if (cudaMemcpy(h.data(), base, g, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(h.data() + g, static_cast<char*>(user) + bytes, g, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return true;  // a device fault is reported by the call that caused it
+    }
+    for (unsigned char v : h) {
+        if (v != kGuardByte) return false;
+    }
+    return true;
+}
+}  // namespace
+
+size_t guard_bytes() {
+    static const size_t g = [] {
+        const char* e = std::getenv("DOPINF_B200_GUARD_BYTES");
+        const long long v = e ? std::atoll(e) : 0;
+        return v > 0 ? (static_cast<size_t>(v) + 255) / 256 * 256 : size_t(0);
+    }();
+    return g;
+}
+
+cudaError_t dev_alloc(void** p, size_t bytes) {
+    const size_t g = guard_bytes();
+    if (g == 0) return cudaMalloc(p, bytes);
+    char* base = nullptr;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * g);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMemset(base, kGuardByte, g)) != cudaSuccess) return e;
+    if ((e = cudaMemset(base + g + bytes, kGuardByte, g)) != cudaSuccess) return e;
+    *p = base + g;
+    std::lock_guard<std::mutex> lock(g_guard_mu);
+    g_guarded[*p] = bytes;
+    return cudaSuccess;
+}
+
+void dev_free(void* p) {
+    const size_t g = guard_bytes();
+    if (g == 0) {
+        cudaFree(p);
+        return;
+    }
+    size_t bytes = 0;
+    {
+        std::lock_guard<std::mutex> lock(g_guard_mu);
+        auto it = g_guarded.find(p);
+        if (it == g_guarded.end()) {
+            cudaFree(p);
+            return;
+        }
+        bytes = it->second;
+        g_guarded.erase(it);
+    }
+    cudaDeviceSynchronize();
+    if (!guard_intact(p, bytes)) {
+        ++g_guard_violations;
+        std::fprintf(stderr, "dopinf_b200: guard region of a %zu-byte device buffer overwritten\n", bytes);
+    }
+    cudaFree(static_cast<char*>(p) - g);
+}
+
 }  // namespace capi
 }  // namespace dopinf_b200
 
@@ -231,6 +306,19 @@ int dopinf_b200_check_uniform(const long long* table, int p, int rank, const cha
     return DOPINF_B200_ERR_COLLECTIVE;
 }
 
+long long dopinf_b200_debug_guard_violations(void) {
+    if (guard_bytes() == 0) return -1;
+    cudaDeviceSynchronize();
+    std::vector<std::pair<void*, size_t>> live;
+    {
+        std::lock_guard<std::mutex> lock(g_guard_mu);
+        live.assign(g_guarded.begin(), g_guarded.end());
+    }
+    long long bad = g_guard_violations.load();
+    for (const auto& [p, n] : live) bad += guard_intact(p, n) ? 0 : 1;
+    return bad;
+}
+
 int dopinf_b200_set_collective_timeout(dopinf_b200_ctx* c, double seconds) {
     return guarded(c, [&] {
         require(seconds > 0.0, "set_collective_timeout: seconds must be positive");
@@ -246,7 +334,17 @@ int dopinf_b200_ctx_poisoned(const dopinf_b200_ctx* c) { return c && c->poisoned
 
 int dopinf_b200_debug_inject(dopinf_b200_ctx* c, int what) {
     return guarded(c, [&] {
-        require(what == 0 || what == DOPINF_B200_INJECT_STALL, "debug_inject: unknown fault");
+        require(what == 0 || what == DOPINF_B200_INJECT_STALL || what == DOPINF_B200_INJECT_OOB_STORE,
+                "debug_inject: unknown fault");
+        if (what == DOPINF_B200_INJECT_OOB_STORE) {
+            require(guard_bytes() >= 8, "debug_inject: out-of-bounds store needs DOPINF_B200_GUARD_BYTES");
+            double* p = c->span.get<double>(2, "span");
+            poke_kernel<<<1, 1, 0, c->stream>>>(p + c->span.bytes / sizeof(double));
+            note_launch();
+            ck(cudaGetLastError(), "poke");
+            c->sync("debug_inject");
+            return;
+        }
         require(what == 0 || c->comm, "debug_inject: the context has no NCCL communicator");
         c->inject = what;
     });

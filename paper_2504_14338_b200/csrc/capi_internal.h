@@ -65,6 +65,15 @@ inline void ckn(ncclResult_t r, const char* what) {
     }
 }
 
+// Guarded device allocations (debug aid; compute-sanitizer is unavailable on
+// the B200 pool): with DOPINF_B200_GUARD_BYTES=G set, every library
+// allocation gets G bytes of a known pattern before and after it; a kernel
+// that writes outside its buffer corrupts a guard, which the release of the
+// buffer and dopinf_b200_debug_guard_violations() detect. G = 0 (default): off.
+size_t guard_bytes();
+cudaError_t dev_alloc(void** p, size_t bytes);
+void dev_free(void* p);
+
 // Grow-only device buffer.
 struct DBuf {
     void* p = nullptr;
@@ -73,16 +82,16 @@ struct DBuf {
     T* get(size_t count, const char* what) {
         const size_t need = std::max<size_t>(count * sizeof(T), 16);
         if (need > bytes) {
-            if (p) cudaFree(p);
+            if (p) dev_free(p);
             p = nullptr;
             bytes = 0;
-            ck(cudaMalloc(&p, need), what);
+            ck(dev_alloc(&p, need), what);
             bytes = need;
         }
         return static_cast<T*>(p);
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
         p = nullptr;
         bytes = 0;
     }

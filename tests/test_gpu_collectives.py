@@ -168,3 +168,21 @@ def test_collective_timeout_aborts_and_poisons():
     assert b.values.shape == (2000, 50)
     b.close()
     c.close()
+
+
+def test_guarded_allocations_and_bitwise_repetition():
+    # compute-sanitizer is closed on the B200 pool: guard bytes around every
+    # library allocation (no kernel may write outside its buffer) and bitwise
+    # repetition of the fixed-order kernels (no race) instead
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, DOPINF_B200_GUARD_BYTES="4096")
+    res = subprocess.run([sys.executable, str(root / "tools" / "sanitize_kernels.py"), "--reps", "4"], env=env,
+                         capture_output=True, text=True, timeout=900)
+    print(res.stdout)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "guard violations: 0" in res.stdout and "sanitize run ok" in res.stdout
