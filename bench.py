@@ -134,6 +134,40 @@ def numpy_oscillator(n_vars, nx, nt, modes, noise, seed, dt=1e-3):
     return q
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def sample_rows(wl, nx_s):
+    """The CPU sample: the first nx_s points of every variable of the workload,
+    made by the same device generator as the GPU arm's batch (identical bytes:
+    the generator is a pure function of seed, variable and global point), or,
+    without a GPU, the numpy generator of the same family. Generation is
+    outside every timed region. Returns (q, source)."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            from paper_2504_14338_b200 import api
+
+            with api.DeviceContext(0) as ctx:
+                blk = api.LocalBlock(ctx, wl["n_vars"], api.RowRange(0, nx_s), wl["nt"])
+                blk.synth_oscillator(seed=wl["seed"], n_modes=wl["modes"], dt=1e-3, noise=wl["noise"])
+                q = blk.values
+                blk.close()
+            return q, "the GPU arm's own bytes (device generator, first points of each variable)"
+    except Exception:  # noqa: BLE001 - no GPU / no extension: same family from numpy
+        pass
+    return (numpy_oscillator(wl["n_vars"], nx_s, wl["nt"], wl["modes"], wl["noise"], wl["seed"]),
+            "numpy generator of the same family (no GPU for the device generator)")
+
+
 def cpu_pass(wl, steps, warmup, cores):
     """Time the reference's Steps II–III + project on a bounded row sample.
     Returns (tflops_per_s, seconds_per_step, kind, cores, sample_desc)."""
@@ -141,7 +175,7 @@ def cpu_pass(wl, steps, warmup, cores):
 
     nv, nt, r = wl["n_vars"], wl["nt"], wl["r"]
     nx_s = min(CPU_SAMPLE_NX, wl["nx"])
-    q = numpy_oscillator(nv, nx_s, nt, wl["modes"], wl["noise"], wl["seed"])
+    q, source = sample_rows(wl, nx_s)
     n_s = nv * nx_s
     flops = n_s * nt * (nt + 1) + 2 * r * nt * nt
     times = []
@@ -158,14 +192,16 @@ def cpu_pass(wl, steps, warmup, cores):
             t2 = time.perf_counter()
             if i >= warmup:
                 times.append(float(secs[0] + secs[1]) + (t2 - t1))
-        sample = (f"{nv} vars x {nx_s} pts (n={n_s}) of the same generator, K={nt}, r={r}; reference "
-                  f"center/compute_global_scales/scale_in_place + global_gram(local_gram) on {cores} in-process "
-                  f"ranks (barrier-fenced stage times) + pod::project; OPENBLAS_NUM_THREADS=1")
+        sample = (f"{nv} vars x {nx_s} pts (n={n_s} of {nv * wl['nx']} rows), K={nt}, r={r}, bytes: {source}; "
+                  f"reference center/compute_global_scales/scale_in_place + global_gram(local_gram) on {cores} "
+                  f"in-process ranks (barrier-fenced stage times) + pod::project; OPENBLAS_NUM_THREADS=1; "
+                  f"CPU {cpu_model()}; the rate is the sample's, extrapolated to the full batch (the work is "
+                  f"linear in n at fixed K)")
     else:
         o = Oracle()
         kind, used = "port", 1
         nx_s = min(nx_s, 2048)  # one scalar thread: keep the sample to ~10-30 s
-        q = numpy_oscillator(nv, nx_s, nt, wl["modes"], wl["noise"], wl["seed"])
+        q, source = sample_rows(wl, nx_s)
         n_s = nv * nx_s
         flops = n_s * nt * (nt + 1) + 2 * r * nt * nt
         for i in range(warmup + steps):
@@ -179,7 +215,8 @@ def cpu_pass(wl, steps, warmup, cores):
             o.project(tr, d)
             if i >= warmup:
                 times.append(time.perf_counter() - t0)
-        sample = f"{nv} vars x {nx_s} pts (n={n_s}), K={nt}, r={r}; C oracle port, 1 thread"
+        sample = (f"{nv} vars x {nx_s} pts (n={n_s}), K={nt}, r={r}, bytes: {source}; C oracle port, 1 thread; "
+                  f"CPU {cpu_model()}; rate extrapolated to the full batch (linear in n)")
     per_step = statistics.median(times)
     return flops / per_step / 1e12, per_step, kind, used, sample
 
@@ -197,7 +234,8 @@ def run_reference_arm(args, wl):
         "ms_per_step": round(per_step * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded damped-oscillator generator)",
         "config": {"workload": wl["name"], "sample_rows": wl["n_vars"] * min(CPU_SAMPLE_NX, wl["nx"]),
-                   "parallelism": f"{used} host threads (in-process ranks)"},
+                   "rows_total": wl["n_vars"] * wl["nx"], "extrapolated": "rate of the row sample (linear in n)",
+                   "cpu_model": cpu_model(), "parallelism": f"{used} host threads (in-process ranks)"},
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": used, "kind": kind, "sample": sample},
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -22,8 +22,11 @@ sys.path.insert(0, str(ROOT))
 
 from paper_2504_14338_b200 import api  # noqa: E402
 
-PEAK_FP64 = 37.1
-PEAK_HBM = 6447.5
+PEAK_FP64 = 37.1  # measured DMMA.8x8x4 peak (profiles/r01_fp64_peak.txt)
+try:  # driver-written HBM copy bandwidth of this pool's B200s
+    PEAK_HBM = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
+except Exception:  # noqa: BLE001
+    PEAK_HBM = 6551.4
 
 
 def stages(ctx, names):
