@@ -69,6 +69,7 @@ void run_stats(dopinf_b200_block* b, bool center) {
 }
 
 void do_center(dopinf_b200_block* b, double* means_host, bool side_copy) {
+    Nvtx nvtx_range("dopinf_b200 center_in_place");
     materialize(b);  // a second centering acts on centered values, as in the reference
     run_stats(b, true);
     b->pending_center = true;
@@ -90,6 +91,7 @@ void do_center(dopinf_b200_block* b, double* means_host, bool side_copy) {
 
 void do_global_scales(dopinf_b200_block* b, double* scales_host, size_t* degenerate,
                       const std::optional<Fail>& earlier) {
+    Nvtx nvtx_range("dopinf_b200 compute_global_scales");
     auto* c = b->ctx;
     const size_t nv = b->n_vars;
     // varmax carries one status slot after the n_vars maxima: MAX of
@@ -132,6 +134,7 @@ void do_global_scales(dopinf_b200_block* b, double* scales_host, size_t* degener
 }
 
 void do_scale(dopinf_b200_block* b, const double* scales_host) {
+    Nvtx nvtx_range("dopinf_b200 scale_in_place");
     auto* c = b->ctx;
     double* ds = c->scales.get<double>(b->n_vars + 1, "scales");
     ck(cudaMemcpyAsync(ds, scales_host, b->n_vars * sizeof(double), cudaMemcpyHostToDevice, c->stream),
@@ -182,6 +185,7 @@ int* ensure_counters(dopinf_b200_ctx* c) {
 }
 
 void do_local_gram(dopinf_b200_block* b, double* d_host) {
+    Nvtx nvtx_range("dopinf_b200 local_gram");
     auto* c = b->ctx;
     materialize(b);
     const int K = static_cast<int>(b->nt);
@@ -241,6 +245,7 @@ void do_local_gram(dopinf_b200_block* b, double* d_host) {
 // status slot set: every rank learns the lowest failed rank from the summed
 // slot and raises (settle) instead of leaving its peers to the deadline.
 void do_global_gram(dopinf_b200_ctx* c, double* d_host, const std::optional<Fail>& local_failure) {
+    Nvtx nvtx_range("dopinf_b200 global_gram");
     if (!local_failure && !c->local_valid) {
         fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "global_gram: no local Gram on this context");
     }
@@ -299,6 +304,7 @@ const double* tr_operand(dopinf_b200_ctx* c, const double* tr_host, size_t nt, s
 
 void do_project(dopinf_b200_ctx* c, const double* tr_host, const double* d_dev, size_t nt, size_t r,
                 double* qhat_host) {
+    Nvtx nvtx_range("dopinf_b200 project");
     require(r >= 1 && r <= nt, "project: r must lie in [1, nt]");
     const double* dtr = tr_operand(c, tr_host, nt, r);
     double* dq = c->qhat.get<double>(nt * r, "qhat");
@@ -314,6 +320,7 @@ void do_project(dopinf_b200_ctx* c, const double* tr_host, const double* d_dev, 
 // Φ_r = Q·T_r into b->phi (pitch basis_cols_pad(r), columns ≥ r zero);
 // returns the pitch. T_r from the host, or the context's device T_r (NULL).
 int do_basis(dopinf_b200_block* b, const double* tr, size_t r) {
+    Nvtx nvtx_range("dopinf_b200 basis");
     auto* c = b->ctx;
     require(r >= 1, "basis: bad map");
     materialize(b);
@@ -869,6 +876,7 @@ int dopinf_b200_set_gram(dopinf_b200_ctx* c, const double* d, size_t nt) {
 
 int dopinf_b200_eig_sym_desc(dopinf_b200_ctx* c, double* lambda, double* vectors) {
     return guarded(c, [&] {
+        Nvtx nvtx_range("dopinf_b200 eig_sym_desc");
         require(c->have_gram && c->K > 0, "eig_sym_desc: no Gram on this context");
         const int n = c->K;
         const size_t nn = static_cast<size_t>(n) * n;

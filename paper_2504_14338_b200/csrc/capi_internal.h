@@ -7,6 +7,7 @@
 #pragma once
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <errno.h>
 #include <fcntl.h>
@@ -73,6 +74,15 @@ inline void ckn(ncclResult_t r, const char* what) {
 size_t guard_bytes();
 cudaError_t dev_alloc(void** p, size_t bytes);
 void dev_free(void* p);
+
+// NVTX range over a stage (shows in Nsight Systems / `ncu --nvtx`; header-only
+// NVTX v3, a no-op without a tool attached).
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 // Grow-only device buffer.
 struct DBuf {

@@ -133,6 +133,7 @@ std::vector<StreamChunk> stream_chunks(const dopinf_b200_block* b, long long chu
 // Gram continues the reference's FMA chains (gram_ref.cu) in block-row order.
 void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling, double* means_host,
                     double* scales_host) {
+    Nvtx nvtx_range("dopinf_b200 streamed snapshot pass");
     auto* c = b->ctx;
     const int K = static_cast<int>(b->nt);
     const size_t count = gram::packed_count(K);
@@ -318,6 +319,7 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
 // data::read_block (data.cpp:164-202) into the device block: the file rows go
 // through the pinned ring, each H2D overlapping the next chunk's read.
 void do_block_read(dopinf_b200_block* b, const StreamSource& src) {
+    Nvtx nvtx_range("dopinf_b200 read_block");
     auto* c = b->ctx;
     b->pending_center = false;
     b->stats_valid = false;

@@ -48,6 +48,7 @@ struct GridOutcome {
 GridOutcome do_grid_search(dopinf_b200_ctx* c, const double* qhat_host, size_t r, size_t nt, const double* b1,
                            size_t n1, const double* b2, size_t n2, double max_growth, size_t nt_p,
                            double* traj_host) {
+    Nvtx nvtx_range("dopinf_b200 grid_search");
     // rom_search.cpp:187-203 (same checks, same order, same messages)
     if (n1 == 0 || n2 == 0) fail(DOPINF_B200_ERR_INVALID_ARGUMENT, "grid_search: empty candidate grid");
     require(b1 && b2, "grid_search: null candidate arrays");
@@ -361,6 +362,7 @@ void d2h_2d(dopinf_b200_ctx* c, double* host, size_t host_ld, const double* dev,
 // while chunk k + 1 computes. Layout = data::write_snapshots (data.cpp:118-129):
 // the field's rows are the variables' rows in order.
 void write_field_file(dopinf_b200_block* b, const FieldOperands& f, const Snp1& h, const std::string& path) {
+    Nvtx nvtx_range("dopinf_b200 write_field");
     auto* c = b->ctx;
     Fd fd;
     fd.fd = open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
