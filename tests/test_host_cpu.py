@@ -23,7 +23,7 @@ def lib():
 
 def declared_symbols():
     text = HEADER.read_text()
-    decl = r"(?m)^(?:int|void|uint64_t|const char)\s*\*?\s*(dopinf_b200_\w+)\s*\("
+    decl = r"(?m)^(?:int|void|uint64_t|long long|const char)\s*\*?\s*(dopinf_b200_\w+)\s*\("
     return sorted(set(re.findall(decl, text)))
 
 
