@@ -365,7 +365,10 @@ void write_field_file(dopinf_b200_block* b, const FieldOperands& f, const Snp1& 
     Nvtx nvtx_range("dopinf_b200 write_field");
     auto* c = b->ctx;
     Fd fd;
-    fd.fd = open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+    // No O_TRUNC: rewriting a field file of the previous run in place (then
+    // ftruncate to the exact size) spares ext4 freeing every block at open and
+    // flushing the replaced file at close; the bytes are the same.
+    fd.fd = open(path.c_str(), O_WRONLY | O_CREAT | O_CLOEXEC, 0644);
     if (fd.fd < 0) format_fail("cannot create snapshot file: " + path);
     std::string head("SNP1");
     for (uint64_t v : {h.n_vars, h.nx, h.nt}) head.append(reinterpret_cast<const char*>(&v), sizeof v);
@@ -377,7 +380,9 @@ void write_field_file(dopinf_b200_block* b, const FieldOperands& f, const Snp1& 
     if (!pwrite_parallel(fd.fd, head.data(), head.size(), 0)) format_fail("write failed: " + path);
     const uint64_t data_off = head.size();
     const size_t nt_p = f.nt_p, ldo = (nt_p + 1) / 2 * 2, rows = b->rows;
-    size_t ch = std::max<size_t>(128, (size_t(256) << 20) / (nt_p * sizeof(double))) / 128 * 128;
+    // 64 MB row chunks: the host's parallel writes of chunk k overlap chunk k+1's
+    // compute and D2H, and the first write starts after ~1 ms, not after 256 MB
+    size_t ch = std::max<size_t>(128, (size_t(64) << 20) / (nt_p * sizeof(double))) / 128 * 128;
     ch = std::min(ch, (rows + 127) / 128 * 128);
     const size_t n = (rows + ch - 1) / ch;
     double* dring = c->field_ring.get<double>(2 * ch * ldo, "field ring");
@@ -409,6 +414,9 @@ void write_field_file(dopinf_b200_block* b, const FieldOperands& f, const Snp1& 
         if (k > 0) flush(k - 1);  // pinned slot (k-1) % 2 is reused by chunk k + 1
     }
     if (n > 0) flush(n - 1);
+    if (ftruncate(fd.fd, static_cast<off_t>(data_off + rows * nt_p * sizeof(double))) != 0) {
+        format_fail("write failed: " + path);
+    }
     c->record(DOPINF_B200_STAGE_FIELD, 1);
     if (close(fd.fd) != 0) {
         fd.fd = -1;
