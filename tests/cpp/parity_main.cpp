@@ -917,6 +917,52 @@ int main() {
                         "gram_reduce %.3f eig_project %.3f search %.3f postprocess %.3f); reference %.3f s\n",
                         workers, t_drop, st[0], st[1], st[2], st[3], st[4], st[5], t_ref);
         }
+
+        // 7b. The drop-in's error behaviour is pipeline::run's: the same exception
+        //     class and message for each bad configuration (pipeline.cpp:94-126,
+        //     data.cpp:133-162), and the all-device options choose the same r and pair.
+        {
+            auto outcome = [](const std::function<void()>& fn) {
+                try {
+                    fn();
+                } catch (const ConfigError& e) {
+                    return "ConfigError: " + std::string(e.what());
+                } catch (const DataFormatError& e) {
+                    return "DataFormatError: " + std::string(e.what());
+                } catch (const std::exception& e) {
+                    return "other: " + std::string(e.what());
+                }
+                return std::string("no error");
+            };
+            std::vector<std::pair<std::string, std::function<void(pipeline::PipelineConfig&)>>> bad = {
+                {"probe variable", [](pipeline::PipelineConfig& c) { c.probes = {{5, 0}}; }},
+                {"probe index", [](pipeline::PipelineConfig& c) { c.probes = {{1, 16384}}; }},
+                {"nt_p shorter than nt", [](pipeline::PipelineConfig& c) { c.nt_p = 100; }},
+                {"rank above nt", [](pipeline::PipelineConfig& c) { c.fixed_rank = 601; }},
+                {"missing file", [&](pipeline::PipelineConfig& c) { c.data_path = (dir / "absent.snp1").string(); }},
+            };
+            bool same = true;
+            std::string detail;
+            for (auto& [name, mutate] : bad) {
+                pipeline::PipelineConfig c3 = cfg;
+                c3.out_dir = (dir / "bad").string();
+                mutate(c3);
+                const std::string want = outcome([&] { pipeline::run(c3); });
+                const std::string got = outcome([&] { dopinf_b200::pipeline::run(c3); });
+                same = same && want == got && want != "no error";
+                detail += name + (want == got ? " same; " : " DIFFERS (" + want + " | " + got + "); ");
+            }
+            report(same, "config 1: dopinf_b200::pipeline::run errors = pipeline::run errors", detail);
+            pipeline::PipelineConfig c4 = cfg;
+            c4.out_dir = (dir / "dropin_device").string();
+            dopinf_b200::pipeline::Options dev;
+            dev.device_eig = true;
+            dev.device_search = true;
+            const pipeline::RunResult rd = dopinf_b200::pipeline::run(c4, dev);
+            report(rd.r == refrun.r && rd.pair_opt == refrun.pair_opt,
+                   "config 1: dopinf_b200::pipeline::run with device eig and device search",
+                   "r = " + std::to_string(rd.r) + ", pair " + (rd.pair_opt == refrun.pair_opt ? "identical" : "DIFFERS"));
+        }
         fs::remove_all(dir);
     }
 
