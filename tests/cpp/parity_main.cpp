@@ -864,12 +864,19 @@ int main() {
         //    artifact but timings.csv and the field file is the reference's byte for
         //    byte, at one rank (the streamed file pass) and at three in-process ranks
         //    (size-1 contexts, the reference Comm's MAX and ascending-rank SUM).
-        for (int workers : {1, 3}) {
+        // workers 1 and 3 on config 1's settings; workers 2 with scaling off and
+        // the rank chosen by retained energy (select_rank, pipeline.cpp:289-293)
+        for (int workers : {1, 3, 2}) {
             pipeline::PipelineConfig c2 = cfg;
             c2.workers = workers;
+            if (workers == 2) {
+                c2.scaling = false;
+                c2.fixed_rank = 0;
+                c2.energy = 0.9995;
+            }
             c2.out_dir = (dir / ("ref_w" + std::to_string(workers))).string();
             auto ta = clk::now();
-            const pipeline::RunResult rr = workers == 1 ? refrun : pipeline::run(c2);
+            const pipeline::RunResult rr = workers == 1 ? refrun : pipeline::run(c2);  // (its own run otherwise)
             const double t_ref = workers == 1 ? ref_total : secs(ta);
             const std::string ref_dir = workers == 1 ? cfg.out_dir : c2.out_dir;
             c2.out_dir = (dir / ("dropin_w" + std::to_string(workers))).string();
@@ -908,7 +915,8 @@ int main() {
             }
             const bool same = differ.empty() && dr.r == rr.r && dr.pair_opt == rr.pair_opt && dr.train_err == rr.train_err;
             report(same && fgap <= 1e-10,
-                   "config 1: dopinf_b200::pipeline::run in place of pipeline::run, workers = " + std::to_string(workers),
+                   "config 1: dopinf_b200::pipeline::run in place of pipeline::run, workers = " + std::to_string(workers) +
+                       (workers == 2 ? ", scaling off, r by energy (r = " + std::to_string(rr.r) + ")" : ""),
                    std::to_string(n_same) + " artifacts byte-identical" + (differ.empty() ? "" : ", DIFFER: " + differ) +
                        "; field files rel " + fmt(fgap) + " <= 1e-10; reference " + fmt(t_ref) + " s, drop-in " +
                        fmt(t_drop) + " s");
