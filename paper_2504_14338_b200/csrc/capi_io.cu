@@ -16,6 +16,15 @@ namespace {
 // dopinf_b200_stream_pass_synth: rows are generated on the device chunk by chunk
 // into a two-slot ring — the block is never resident (config 4: 403 GB/GPU).
 constexpr long long kStreamChunkRows = 32768;   // rows per H2D chunk (315 MB at K = 1200)
+constexpr size_t kStagedSlotBytes = size_t(64) << 20;  // pinned ring slot of staged (file / pageable) copies
+
+// Rows per chunk of a staged copy: ~64 MB slots, so the pinned ring a context
+// allocates on first use is ~128 MB (page-locking costs ~0.1 s per 100 MB) and
+// the first copy starts early.
+long long staged_rows(size_t nt) {
+    const long long r = static_cast<long long>(kStagedSlotBytes / (nt * sizeof(double)));
+    return std::max<long long>(256, std::min<long long>(kStreamChunkRows, r));
+}
 
 constexpr long long kTailChunkRows = 8192;     // the pass's final chunk is cut to this size
 constexpr long long kStreamSplitRows = 2048;    // rows per Gram item inside a host chunk
@@ -66,14 +75,7 @@ void copy_rows_parallel(double* dst, const double* src, size_t sld, size_t nt, l
             for (long long r = a; r < e; ++r) std::memcpy(dst + r * nt, src + r * sld, nt * sizeof(double));
         }
     };
-    if (n <= 1) {
-        part(0);
-        return;
-    }
-    std::vector<std::thread> threads;
-    for (int i = 1; i < n; ++i) threads.emplace_back(part, i);
-    part(0);
-    for (auto& t : threads) t.join();
+    parallel_for(n, part);
 }
 
 // Staged source (SNP1 file or pageable host rows): fill pinned ring slot k % 2
@@ -137,7 +139,8 @@ void do_stream_pass(dopinf_b200_block* b, const StreamSource& src, bool scaling,
     auto* c = b->ctx;
     const int K = static_cast<int>(b->nt);
     const size_t count = gram::packed_count(K);
-    const long long chunk_rows = src.synth ? kSynthChunkRows : kStreamChunkRows;
+    const long long chunk_rows =
+        src.synth ? kSynthChunkRows : (src.fd >= 0 || src.pageable) ? staged_rows(b->nt) : kStreamChunkRows;
     const long long split_rows = src.synth ? kSynthSplitRows : kStreamSplitRows;
     const bool ref_order = c->gram_order == DOPINF_B200_GRAM_ORDER_REFERENCE;
     require(!(ref_order && src.synth),
@@ -323,14 +326,15 @@ void do_block_read(dopinf_b200_block* b, const StreamSource& src) {
     auto* c = b->ctx;
     b->pending_center = false;
     b->stats_valid = false;
-    const std::vector<StreamChunk> chunks = stream_chunks(b, kStreamChunkRows, false);
+    const long long chunk_rows = staged_rows(b->nt);
+    const std::vector<StreamChunk> chunks = stream_chunks(b, chunk_rows, false);
     if (chunks.empty()) return;
     while (c->chunk_events.size() < chunks.size() + 1) {
         cudaEvent_t e;
         ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
         c->chunk_events.push_back(e);
     }
-    const size_t slot_doubles = static_cast<size_t>(std::min<long long>(kStreamChunkRows, b->nx_i)) * b->nt;
+    const size_t slot_doubles = static_cast<size_t>(std::min<long long>(chunk_rows, b->nx_i)) * b->nt;
     auto* fring = static_cast<double*>(c->file_ring.get(2 * slot_doubles * sizeof(double)));
     c->record(DOPINF_B200_STAGE_UPLOAD, 0);
     cudaEvent_t ready = c->chunk_events[chunks.size()];
@@ -368,7 +372,7 @@ dopinf_b200_block* open_file_block(dopinf_b200_ctx* c, const char* path, size_t 
 // of the other.
 void staged_download(dopinf_b200_block* b, size_t row0, size_t nrows, double* host, size_t host_ld) {
     auto* c = b->ctx;
-    const size_t chunk = static_cast<size_t>(kStreamChunkRows);
+    const size_t chunk = static_cast<size_t>(staged_rows(b->nt));
     const size_t slot_doubles = std::min(chunk, nrows) * b->nt;
     auto* ring = static_cast<double*>(c->file_ring.get(2 * slot_doubles * sizeof(double)));
     const size_t n = (nrows + chunk - 1) / chunk;
@@ -397,10 +401,7 @@ void staged_download(dopinf_b200_block* b, size_t row0, size_t nrows, double* ho
                     std::memcpy(host + (r0 + r) * host_ld, slot + r * b->nt, b->nt * sizeof(double));
             }
         };
-        std::vector<std::thread> threads;
-        for (int i = 1; i < th; ++i) threads.emplace_back(part, i);
-        part(0);
-        for (auto& t : threads) t.join();
+        parallel_for(th, part);
     }
 }
 
@@ -510,20 +511,83 @@ int file_reader_threads() {
 
 // pread `bytes` at `off` into `dst` on up to file_reader_threads() threads.
 bool pread_parallel(int fd, void* dst, size_t bytes, uint64_t off) {
-    constexpr size_t kPiece = size_t(8) << 20;
+    constexpr size_t kPiece = size_t(4) << 20;
     const int n = static_cast<int>(std::min<size_t>(file_reader_threads(), (bytes + kPiece - 1) / kPiece));
     if (n <= 1) return pread_all(fd, dst, bytes, off);
     const size_t per = (bytes / n + 4095) / 4096 * 4096;
-    std::vector<std::thread> threads;
     std::vector<char> ok(n, 0);
-    for (int i = 0; i < n; ++i) {
+    parallel_for(n, [&](int i) {
         const size_t b0 = std::min(bytes, per * i), b1 = std::min(bytes, per * (i + 1));
-        threads.emplace_back([&, i, b0, b1] {
-            ok[i] = pread_all(fd, static_cast<char*>(dst) + b0, b1 - b0, off + b0) ? 1 : 0;
-        });
-    }
-    for (auto& t : threads) t.join();
+        ok[i] = pread_all(fd, static_cast<char*>(dst) + b0, b1 - b0, off + b0) ? 1 : 0;
+    });
     return std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
+}
+
+namespace {
+class HostPool {
+public:
+    explicit HostPool(int workers) {
+        for (int i = 0; i < workers; ++i) std::thread([this] { loop(); }).detach();  // live until exit
+    }
+    void run(int n, const std::function<void(int)>& fn) {
+        std::lock_guard<std::mutex> job(job_mu_);
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            fn_ = &fn;
+            n_ = n;
+            next_ = 0;
+            pending_ = n;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lock(mu_);
+        done_.wait(lock, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+private:
+    void work() {
+        for (;;) {
+            int i;
+            const std::function<void(int)>* fn;
+            {
+                std::lock_guard<std::mutex> lock(mu_);
+                if (!fn_ || next_ >= n_) return;
+                i = next_++;
+                fn = fn_;
+            }
+            (*fn)(i);
+            std::lock_guard<std::mutex> lock(mu_);
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lock(mu_);
+                cv_.wait(lock, [&] { return gen_ != seen; });
+                seen = gen_;
+            }
+            work();
+        }
+    }
+    std::mutex job_mu_, mu_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)>* fn_ = nullptr;
+    int n_ = 0, next_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+};
+}  // namespace
+
+void parallel_for(int n, const std::function<void(int)>& fn) {
+    if (n <= 1) {
+        if (n == 1) fn(0);
+        return;
+    }
+    static HostPool* pool = new HostPool(std::max(1, file_reader_threads() - 1));  // + the caller
+    pool->run(n, fn);
 }
 
 }  // namespace capi

@@ -380,9 +380,14 @@ void write_field_file(dopinf_b200_block* b, const FieldOperands& f, const Snp1& 
     if (!pwrite_parallel(fd.fd, head.data(), head.size(), 0)) format_fail("write failed: " + path);
     const uint64_t data_off = head.size();
     const size_t nt_p = f.nt_p, ldo = (nt_p + 1) / 2 * 2, rows = b->rows;
-    // 64 MB row chunks: the host's parallel writes of chunk k overlap chunk k+1's
-    // compute and D2H, and the first write starts after ~1 ms, not after 256 MB
-    size_t ch = std::max<size_t>(128, (size_t(64) << 20) / (nt_p * sizeof(double))) / 128 * 128;
+    // 32 MB row chunks: the host's parallel writes of chunk k overlap chunk k+1's
+    // compute and D2H, the first write starts early, and the pinned ring (2 slots,
+    // shared with the file reads) stays small — page-locking is ~0.1 s per 100 MB
+    size_t ch = std::max<size_t>(128, (size_t(32) << 20) / (nt_p * sizeof(double))) / 128 * 128;
+    // reuse the pinned ring a file pass left if its slots hold >= 1024 rows
+    // (re-pinning a larger ring costs more than the smaller chunks do)
+    const size_t have = c->file_ring.bytes / (2 * nt_p * sizeof(double)) / 128 * 128;
+    if (have >= 1024) ch = std::min(ch, have);
     ch = std::min(ch, (rows + 127) / 128 * 128);
     const size_t n = (rows + ch - 1) / ch;
     double* dring = c->field_ring.get<double>(2 * ch * ldo, "field ring");
@@ -440,19 +445,15 @@ bool pwrite_parallel(int fd, const void* src, size_t bytes, uint64_t off) {
         }
         return true;
     };
-    constexpr size_t kPiece = size_t(8) << 20;
+    constexpr size_t kPiece = size_t(4) << 20;
     const int n = static_cast<int>(std::min<size_t>(file_reader_threads(), (bytes + kPiece - 1) / kPiece));
     if (n <= 1) return write_all(static_cast<const char*>(src), bytes, off);
     const size_t per = (bytes / n + 4095) / 4096 * 4096;
-    std::vector<std::thread> threads;
     std::vector<char> ok(n, 0);
-    for (int i = 0; i < n; ++i) {
+    parallel_for(n, [&](int i) {
         const size_t b0 = std::min(bytes, per * i), b1 = std::min(bytes, per * (i + 1));
-        threads.emplace_back([&, i, b0, b1] {
-            ok[i] = write_all(static_cast<const char*>(src) + b0, b1 - b0, off + b0) ? 1 : 0;
-        });
-    }
-    for (auto& t : threads) t.join();
+        ok[i] = write_all(static_cast<const char*>(src) + b0, b1 - b0, off + b0) ? 1 : 0;
+    });
     return std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; });
 }
 
