@@ -42,7 +42,7 @@ class Oracle:
         if Oracle._lib is None:
             if not ORACLE_SO.exists():
                 ORACLE_SO.parent.mkdir(exist_ok=True)
-                subprocess.run(["gcc", "-O2", "-std=c11", "-mfma", "-ffp-contract=off", "-fPIC", "-shared", "-o",
+                subprocess.run(["gcc", "-O2", "-std=c11", "-mavx2", "-mfma", "-ffp-contract=off", "-fPIC", "-shared", "-o",
                                 str(ORACLE_SO), str(HERE / "dopinf_oracle.c"), "-lm"], check=True)
             lib = C.CDLL(str(ORACLE_SO))
             lib.oracle_rng_new.restype = C.c_void_p
@@ -72,6 +72,8 @@ class Oracle:
             lib.oracle_allreduce_sum.argtypes = [_dp, C.c_int, C.c_size_t, _dp]
             lib.oracle_gram_entries.argtypes = [_dp, C.c_size_t, C.c_size_t, _sp, _sp, C.c_size_t, _dp]
             lib.oracle_row_stats.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp]
+            lib.oracle_gram_tile.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t,
+                                             C.c_size_t, _dp]
             lib.oracle_matmul_tn.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
             lib.oracle_matmul.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
             lib.oracle_matmul_nt.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, _dp]
@@ -167,6 +169,32 @@ class Oracle:
         with ThreadPoolExecutor(threads) as ex:
             list(ex.map(run, range(threads)))
         return acc
+
+    def gram_full(self, q, threads: int = 16, tile: int = 128):
+        """linalg.cpp:50-58 over the whole of q — the reference's D bit for bit —
+        computed as independent 128×128 entry tiles on `threads` threads (the
+        oracle's gram() for data too large for one thread)."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        assert q.dtype == np.float64 and q.flags.c_contiguous
+        rows, k = q.shape
+        nb = (k + tile - 1) // tile
+        d = np.empty((k, k))
+        jobs = [(bi, bj) for bi in range(nb) for bj in range(bi, nb)]
+
+        def run(job):
+            bi, bj = job
+            i0, j0 = bi * tile, bj * tile
+            ni, nj = min(tile, k - i0), min(tile, k - j0)
+            out = np.empty((ni, nj))
+            self.lib.oracle_gram_tile(_d(q), k, rows, i0, ni, j0, nj, _d(out))
+            d[i0:i0 + ni, j0:j0 + nj] = out
+            if bi != bj:
+                d[j0:j0 + nj, i0:i0 + ni] = out.T
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(run, jobs))
+        return d
 
     def row_stats(self, q, threads: int = 16):
         """Per row: center_in_place's mean and the max |centered value|

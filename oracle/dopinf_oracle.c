@@ -265,6 +265,26 @@ void oracle_gram_entries(const double* q, size_t ld, size_t rows, const size_t* 
     }
 }
 
+/* linalg.cpp:50-58 gram over one tile of entries, rows [i0, i0+ni) × columns
+ * [j0, j0+nj) of D, all rows of q (pitch ld) in order: out (ni × nj) receives
+ * the reference's FMA chains bit for bit (each entry only ever receives
+ * fma(q(l, i), q(l, j), c), rows ascending). The j loop is the reference's
+ * axpy (element-wise FMAs, vectorisable without changing any result); tiles
+ * are independent, so a full D is computed tile by tile on several threads. */
+__attribute__((optimize("O3"))) void oracle_gram_tile(const double* q, size_t ld, size_t rows, size_t i0,
+                                                      size_t ni, size_t j0, size_t nj, double* out) {
+    memset(out, 0, ni * nj * sizeof(double));
+    for (size_t l = 0; l < rows; ++l) {
+        const double* ql = q + l * ld;
+        for (size_t i = 0; i < ni; ++i) {
+            const double a = ql[i0 + i];
+            double* o = out + i * nj;
+            const double* x = ql + j0;
+            for (size_t j = 0; j < nj; ++j) o[j] = fma(a, x[j], o[j]);
+        }
+    }
+}
+
 /* comm_inprocess.cpp:101-112: SUM all-reduce, ascending rank order
  * (pod::global_gram, pod.cpp:15-18). parts is p x count. */
 void oracle_allreduce_sum(const double* parts, int p, size_t count, double* out) {

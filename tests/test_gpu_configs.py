@@ -6,10 +6,11 @@ the host's 16 cores over the same bytes the device pass consumed, downloaded
 in slices:
 
   C2  4 vars x 262,144 pts, K=1200 (the bench config, 10.1 GB): means, scales
-      and the whole transformed block bit-identical; 2,100 Gram entries in
-      the reference's own summation order (linalg.cpp:50-58: rows ascending,
-      one FMA per row) plus every diagonal entry; D·v = Qᵀ(Q v) for a seeded
-      v; Q̂ = T_rᵀD bit-identical.
+      and the whole transformed block bit-identical; the WHOLE D against the
+      reference's own summation order (linalg.cpp:50-58: rows ascending, one
+      FMA per row; the oracle on 16 threads, tile by tile): relative Frobenius
+      error (the north star's metric), and bit-identical in the reference-order
+      mode; D·v = Qᵀ(Q v) for a seeded v; Q̂ = T_rᵀD bit-identical.
   C5  the C2 data, r in {20, 40, 80}: Φ_r rows against linalg::matmul's order
       (4,096 sampled rows + 1,000 probe rows), basis_rows and
       reconstruct_probes over a 2K horizon bit-identical to the reference.
@@ -130,6 +131,24 @@ def test_c2_transform_bitwise_whole_block(c2, oracle):
     print(f"C2 transform: {raw.shape[0]} rows bitwise ({time.time() - t0:.1f} s)")
 
 
+@pytest.fixture(scope="module")
+def c2_full_d(c2, oracle):
+    """The reference's D of the whole C2 block (linalg.cpp:50-58 order, all
+    1,048,576 rows), computed by the oracle tile by tile on 16 threads."""
+    t0 = time.time()
+    d = oracle.gram_full(c2["q"], threads=16)
+    print(f"C2 oracle full D in reference order: {time.time() - t0:.1f} s")
+    return d
+
+
+def test_c2_gram_full_matrix(c2, c2_full_d):
+    # the north star's metric on the whole D at the bench config
+    d = c2["d"]
+    err = float(np.linalg.norm(d - c2_full_d) / np.linalg.norm(c2_full_d))
+    print(f"C2 Gram: relative Frobenius error of the whole D vs the reference order {err:.3e}")
+    assert err <= GRAM_TOL
+
+
 def test_c2_gram_reference_order_and_dv(c2, oracle):
     q, d, K = c2["q"], c2["d"], c2["K"]
     _, ii, jj = sample_pairs(K, seed=22)
@@ -143,7 +162,7 @@ def test_c2_gram_reference_order_and_dv(c2, oracle):
     dv_report(d, q.T @ (q @ v), v, "C2 Gram")
 
 
-def test_c2_reference_order_gram_bitwise(c2, oracle):
+def test_c2_reference_order_gram_bitwise(c2, oracle, c2_full_d):
     # the reference-order mode on the same raw bytes (streamed from host memory):
     # scales bitwise and the sampled entries equal the reference's FMA chains bit for bit
     a = api()
@@ -162,6 +181,7 @@ def test_c2_reference_order_gram_bitwise(c2, oracle):
     acc = np.zeros(ii.size)
     oracle.gram_entries(c2["q"], ii, jj, acc, threads=16)
     assert np.array_equal(d[ii, jj], acc)  # bit-identical to linalg::gram's chains
+    assert np.array_equal(d, c2_full_d)  # ... every entry of D
     assert np.array_equal(d, d.T)
 
 

@@ -231,6 +231,7 @@ def test_sliced_checkers_match_whole_block(oracle, m, k):
     for a, b in ((0, m // 3), (m // 3, m // 2), (m // 2, m)):
         oracle.gram_entries(c[a:b], ii, jj, acc, threads=4)
     assert np.array_equal(acc, d[ii, jj])
+    assert np.array_equal(oracle.gram_full(c, threads=3, tile=16), d)  # tiled, multi-threaded
 
 
 def test_sliced_gram_entries_vs_reference(oracle, reference):
@@ -241,3 +242,4 @@ def test_sliced_gram_entries_vs_reference(oracle, reference):
     for a in range(0, 4000, 1024):
         oracle.gram_entries(q[a:a + 1024], ii, jj, acc)
     assert np.array_equal(acc, d[ii, jj])
+    assert np.array_equal(oracle.gram_full(q, threads=4, tile=32), d)
