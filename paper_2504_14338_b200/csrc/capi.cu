@@ -260,12 +260,11 @@ void do_global_gram(dopinf_b200_ctx* c, double* d_host, const std::optional<Fail
         return;
     }
     double* packed = c->packed.get<double>(count + 1, "packed");
-    if (local_failure) {
-        const double bit = failure_bit(c, true);
+    if (local_failure) {  // else the status slot is 0 (do_local_gram / the streamed pass set it)
+        double* bit = c->small_pinned<double>(1);
+        *bit = failure_bit(c, true);
         ck(cudaMemsetAsync(packed, 0, count * sizeof(double), c->stream), "memset");
-        ck(cudaMemcpyAsync(packed + count, &bit, sizeof(double), cudaMemcpyHostToDevice, c->stream), "status H2D");
-    } else {
-        // status slot 0 (set by do_local_gram / the streamed pass)
+        ck(cudaMemcpyAsync(packed + count, bit, sizeof(double), cudaMemcpyHostToDevice, c->stream), "status H2D");
     }
     double* out = c->gpacked.get<double>(count + 1, "reduced Gram");
     c->record(DOPINF_B200_STAGE_ALLREDUCE, 0);
@@ -492,8 +491,8 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
         if (pair[0]) cudaEventDestroy(pair[0]);
         if (pair[1]) cudaEventDestroy(pair[1]);
     }
-    for (DBuf* b : {&c->tiles, &c->work, &c->counters, &c->packed, &c->gpacked, &c->coll_scratch, &c->gather, &c->dmat, &c->dhost_in,
-                    &c->scales, &c->tr, &c->trt, &c->qhat, &c->sel, &c->rows_out, &c->span, &c->eig_a,
+    for (DBuf* b : {&c->tiles, &c->work, &c->counters, &c->packed, &c->gpacked, &c->coll_scratch, &c->gather,
+                    &c->dmat, &c->dhost_in, &c->scales, &c->tr, &c->trt, &c->qhat, &c->sel, &c->rows_out, &c->span, &c->eig_a,
                     &c->eig_w, &c->eig_work, &c->eig_info, &c->eig_v, &c->eig_lambda, &c->tr_dev, &c->field_qt,
                     &c->field_means, &c->field_scales, &c->field_ring, &c->rom_qhat, &c->rom_dhat, &c->rom_q2t,
                     &c->rom_qrows, &c->rom_rhs, &c->rom_g, &c->rom_lhs, &c->rom_rhsb, &c->rom_betas, &c->rom_traj,
