@@ -455,7 +455,7 @@ int dopinf_b200_ctx_create_ex(int device, int rank, int size, const unsigned cha
         if (nccl) {
             ncclUniqueId uid;
             std::memcpy(&uid, id, sizeof uid);
-            ckn(ncclCommInitRank(&c->comm, size, uid, rank), "ncclCommInitRank");
+            comm_init(c, size, uid, rank);
         }
     });
     return finish_create(c, rc, out);
@@ -485,7 +485,7 @@ void dopinf_b200_ctx_destroy(dopinf_b200_ctx* c) {
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
     if (c->stream) join_stream(c, c->stream);
-    if (c->comm && c->owns_comm) ncclCommDestroy(c->comm);
+    if (c->comm && c->owns_comm) comm_destroy(c);
     if (c->stall_flag) cudaFreeHost(c->stall_flag);
     for (auto& pair : c->ev) {
         if (pair[0]) cudaEventDestroy(pair[0]);

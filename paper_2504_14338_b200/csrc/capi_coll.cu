@@ -80,6 +80,30 @@ void abort_comm(dopinf_b200_ctx* c) {
 
 void before(dopinf_b200_ctx* c, size_t count, long long tag, const char* what);
 
+// An NCCL call on a non-blocking communicator may return ncclInProgress: its
+// host-side work (connection setup, the init itself) completes in the
+// background and must be polled; a peer that never arrives leaves it in
+// progress, so the poll has the collective deadline.
+void settle_call(dopinf_b200_ctx* c, ncclResult_t r, const std::string& what) {
+    if (r == ncclSuccess) return;
+    if (r != ncclInProgress) poison_and_fail(c, what + ": " + ncclGetErrorString(r));
+    const auto t0 = Clock::now();
+    for (;;) {
+        ncclResult_t st = ncclInProgress;
+        if (ncclCommGetAsyncError(c->comm, &st) != ncclSuccess) st = ncclInternalError;
+        if (st == ncclSuccess) return;
+        if (st != ncclInProgress) {
+            abort_comm(c);
+            poison_and_fail(c, what + ": " + ncclGetErrorString(st));
+        }
+        if (std::chrono::duration<double>(Clock::now() - t0).count() > c->coll_timeout_s) {
+            abort_comm(c);
+            poison_and_fail(c, "collective timed out waiting for peer ranks");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
+}
+
 void issued(dopinf_b200_ctx* c) {
     c->coll_pending = true;
     ++c->coll_seq;
@@ -110,8 +134,7 @@ void before(dopinf_b200_ctx* c, size_t count, long long tag, const char* what) {
     long long* pin = c->small_pinned<long long>(3 * static_cast<size_t>(p) + 3);
     std::memcpy(pin, mine, sizeof mine);
     ck(cudaMemcpyAsync(dev, pin, sizeof mine, cudaMemcpyHostToDevice, c->stream), "check H2D");
-    const ncclResult_t r = ncclAllGather(dev, dev + 3, 3, ncclInt64, c->comm, c->stream);
-    if (r != ncclSuccess) poison_and_fail(c, std::string(what) + ": " + ncclGetErrorString(r));
+    settle_call(c, ncclAllGather(dev, dev + 3, 3, ncclInt64, c->comm, c->stream), what);
     c->coll_pending = true;
     ck(cudaMemcpyAsync(pin + 3, dev + 3, 3 * static_cast<size_t>(p) * sizeof(long long), cudaMemcpyDeviceToHost,
                        c->stream),
@@ -134,23 +157,20 @@ void before(dopinf_b200_ctx* c, size_t count, long long tag, const char* what) {
 void coll_allreduce(dopinf_b200_ctx* c, const void* send, void* recv, size_t count, ncclDataType_t type,
                     ncclRedOp_t op, const char* what) {
     before(c, count, reduce_tag(op, type), what);
-    const ncclResult_t r = ncclAllReduce(send, recv, count, type, op, c->comm, c->stream);
-    if (r != ncclSuccess) poison_and_fail(c, std::string(what) + ": " + ncclGetErrorString(r));
+    settle_call(c, ncclAllReduce(send, recv, count, type, op, c->comm, c->stream), what);
     issued(c);
 }
 
 void coll_allgather(dopinf_b200_ctx* c, const void* send, void* recv, size_t count, ncclDataType_t type,
                     const char* what) {
     before(c, count, kTagAllgather, what);
-    const ncclResult_t r = ncclAllGather(send, recv, count, type, c->comm, c->stream);
-    if (r != ncclSuccess) poison_and_fail(c, std::string(what) + ": " + ncclGetErrorString(r));
+    settle_call(c, ncclAllGather(send, recv, count, type, c->comm, c->stream), what);
     issued(c);
 }
 
 void coll_broadcast(dopinf_b200_ctx* c, void* buf, size_t count, ncclDataType_t type, int root, const char* what) {
     before(c, count, kTagBroadcast + root, what);
-    const ncclResult_t r = ncclBroadcast(buf, buf, count, type, root, c->comm, c->stream);
-    if (r != ncclSuccess) poison_and_fail(c, std::string(what) + ": " + ncclGetErrorString(r));
+    settle_call(c, ncclBroadcast(buf, buf, count, type, root, c->comm, c->stream), what);
     issued(c);
 }
 
@@ -235,6 +255,43 @@ void dev_free(void* p) {
         std::fprintf(stderr, "dopinf_b200: guard region of a %zu-byte device buffer overwritten\n", bytes);
     }
     cudaFree(static_cast<char*>(p) - g);
+}
+
+// Create the rank's communicator as a non-blocking one and wait for the init
+// with the collective deadline: a peer that never joins (it failed before the
+// init) ends in CollectiveError instead of a hang in ncclCommInitRank.
+void comm_init(dopinf_b200_ctx* c, int size, const ncclUniqueId& uid, int rank) {
+    if (const char* e = std::getenv("DOPINF_B200_COLLECTIVE_TIMEOUT")) {
+        const double v = std::atof(e);
+        if (v > 0.0) c->coll_timeout_s = v;
+    }
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = ncclCommInitRankConfig(&comm, size, uid, rank, &cfg);
+    c->comm = comm;
+    if (r != ncclSuccess && r != ncclInProgress) {
+        c->comm = nullptr;
+        fail(DOPINF_B200_ERR_COLLECTIVE, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    settle_call(c, r, "ncclCommInitRank");
+}
+
+// Finalize (non-blocking: polled, bounded) and destroy an owned communicator.
+void comm_destroy(dopinf_b200_ctx* c) {
+    if (!c->comm) return;
+    ncclResult_t r = ncclCommFinalize(c->comm);
+    const auto t0 = Clock::now();
+    while (r == ncclInProgress && Clock::now() - t0 < std::chrono::seconds(20)) {
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+        if (ncclCommGetAsyncError(c->comm, &r) != ncclSuccess) break;
+    }
+    if (r == ncclSuccess) {
+        ncclCommDestroy(c->comm);
+    } else {
+        ncclCommAbort(c->comm);
+    }
+    c->comm = nullptr;
 }
 
 }  // namespace capi

@@ -379,6 +379,10 @@ void coll_allgather(dopinf_b200_ctx* c, const void* send, void* recv, size_t cou
 void coll_broadcast(dopinf_b200_ctx* c, void* buf, size_t count, ncclDataType_t type, int root, const char* what);
 // Bounded wait on a side stream (a poisoned context must not hang in teardown).
 void join_stream(dopinf_b200_ctx* c, cudaStream_t s);
+// The rank's own communicator: non-blocking init bounded by the deadline
+// (DOPINF_B200_COLLECTIVE_TIMEOUT seconds, default 60); finalize + destroy.
+void comm_init(dopinf_b200_ctx* c, int size, const ncclUniqueId& uid, int rank);
+void comm_destroy(dopinf_b200_ctx* c);
 // The status slot a rank contributes to a SUM-reduced buffer: 2^rank when it
 // failed (exact for up to 52 ranks; beyond that every failure reads as rank 52+).
 inline double failure_bit(const dopinf_b200_ctx* c, bool failed) {

@@ -170,6 +170,37 @@ def test_collective_timeout_aborts_and_poisons():
     c.close()
 
 
+def test_communicator_init_with_absent_peer_times_out():
+    # A rank whose peers never join (they failed before the init) ends with
+    # CollectiveError after the deadline instead of hanging in the init
+    # (comm_inprocess.cpp:50-63 semantics applied to communicator creation).
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = (
+        "import sys, time\n"
+        f"sys.path.insert(0, {str(root)!r})\n"
+        "from paper_2504_14338_b200 import api as a\n"
+        "uid = a.DeviceContext.unique_id()\n"
+        "t0 = time.time()\n"
+        "try:\n"
+        "    a.DeviceContext(0, rank=0, size=2, unique_id=uid)\n"
+        "    print('created')\n"
+        "except a.CollectiveError as e:\n"
+        "    print('CollectiveError', round(time.time() - t0, 2), e)\n"
+    )
+    env = dict(os.environ, DOPINF_B200_COLLECTIVE_TIMEOUT="3")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=240)
+    print(res.stdout, res.stderr[-2000:])
+    line = res.stdout.strip().splitlines()[-1]
+    assert line.startswith("CollectiveError"), res.stdout + res.stderr
+    assert "timed out waiting for peer ranks" in res.stderr  # finish_create's diagnostic
+    assert 2.5 <= float(line.split()[1]) <= 60.0
+
+
 def test_guarded_allocations_and_bitwise_repetition():
     # compute-sanitizer is closed on the B200 pool: guard bytes around every
     # library allocation (no kernel may write outside its buffer) and bitwise
