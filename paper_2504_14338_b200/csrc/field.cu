@@ -213,7 +213,25 @@ __global__ void __launch_bounds__(THREADS, 2)
             }
 
             // epilogue half by half: the first half's results are final while the
-            // second half's DMMAs still drain
+            // second half's DMMAs still drain. Interior chunks of full row tiles
+            // (all but the last chunk at nt_p % 64 != 0) take a branch-free path.
+            if (!accumulate && (c + 1) * BN <= nt_p && (rt + 1) * BM <= rows) {
+                const uint32_t sc_u = smem_u32(sm.scale), mn_u = smem_u32(sm.mean);
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi) {
+                        const int lr = wm * 32 + mi * 8 + g;
+                        const double s_row = lds64(sc_u + lr * 8), m_row = lds64(mn_u + lr * 8);
+                        double* dst = out + static_cast<size_t>(rt * BM + lr) * ldo + c * BN + wn * 32 + 2 * t;
+#pragma unroll
+                        for (int ni = 2 * h; ni < 2 * h + 2; ++ni) {
+                            __stcs(reinterpret_cast<double2*>(dst + ni * 8),
+                                   make_double2(fma(s_row, acc[mi][ni][0], m_row), fma(s_row, acc[mi][ni][1], m_row)));
+                        }
+                    }
+                continue;
+            }
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
