@@ -146,7 +146,10 @@ uint64_t dopinf_b200_kernel_launches(void);
  * this and distributes the bytes (any transport) to the other ranks. */
 int dopinf_b200_get_unique_id(unsigned char* id);
 /* One context per rank: binds `device`, creates a stream and, when size > 1,
- * an NCCL communicator from `id` (ignored when size == 1). */
+ * an NCCL communicator from `id` (ignored when size == 1). The communicator
+ * is initialised non-blocking and waited for with the collective deadline
+ * (env DOPINF_B200_COLLECTIVE_TIMEOUT seconds, default 60): a peer that never
+ * joins gives COLLECTIVE ("collective timed out waiting for peer ranks"). */
 int dopinf_b200_ctx_create(int device, int rank, int size, const unsigned char* id,
                            dopinf_b200_ctx** out);
 /* A context on the caller's NCCL communicator and CUDA stream (plain
