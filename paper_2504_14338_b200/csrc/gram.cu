@@ -84,10 +84,16 @@ __device__ __forceinline__ void decode(uint32_t e, int& wm, int& wn, bool& diag,
 // MASK: the mma tiles (bit mi*4 + ni) of the warp tile, fixed at compile
 // time so skipped tiles cost nothing (a predicated-off DMMA still occupies
 // the tensor pipe). The partial masks that occur for any K are few:
-// diagonal 0xCCFF, column edge 0x1111/0x3333/0x7777, and their combinations
-// 0x0001/0x0033/0x0477; plus the halves plan_tiles cuts from warp tiles of
-// tiles with fewer than 16 active warp tiles (0x3333/0xCCCC, 0x3333/0x4444
-// by columns; 0x0033/0x3300, 0x00CC/0xCC00 by rows).
+// diagonal 0x8CEF, column edge 0x1111/0x3333/0x7777, and their combinations
+// 0x0001/0x0023/0x0033/0x0467; plus the halves plan_tiles cuts from warp tiles
+// of tiles with fewer than 16 active warp tiles (0x3333/0xCCCC, 0x0023/0x8CCC,
+// 0x3333/0x4444 by columns; 0x0033/0x3300, 0x00CC/0xCC00 by rows).
+// Diagonal warp tiles: rows and columns of an mma tile are interleaved (even
+// or odd members of a 16-block), so inside a diagonal 16-block the (odd rows,
+// even columns) mma tile holds only entries whose transposes the (even rows,
+// odd columns) one computes; it is skipped (12 -> 10 mma) and the reduction
+// writes those entries from their transposes (D is symmetric, and the two
+// dot products are the same products summed in the same k order).
 template <uint32_t MASK>
 __device__ __forceinline__ void stage_mma(double (&acc)[16][2], const double* __restrict__ as,
                                           const double* __restrict__ bs, int xg0, int xg1, uint32_t mask) {
@@ -116,11 +122,13 @@ __device__ __forceinline__ void stage_mma_any(double (&acc)[16][2], const double
                                               const double* __restrict__ bs, int xg0, int xg1, uint32_t mask) {
     switch (mask) {
         case 0xFFFFu: stage_mma<0xFFFFu>(acc, as, bs, xg0, xg1, mask); break;
-        case 0xCCFFu: stage_mma<0xCCFFu>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x8CEFu: stage_mma<0x8CEFu>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x8CCCu: stage_mma<0x8CCCu>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x0023u: stage_mma<0x0023u>(acc, as, bs, xg0, xg1, mask); break;
         case 0x7777u: stage_mma<0x7777u>(acc, as, bs, xg0, xg1, mask); break;
         case 0x3333u: stage_mma<0x3333u>(acc, as, bs, xg0, xg1, mask); break;
         case 0x1111u: stage_mma<0x1111u>(acc, as, bs, xg0, xg1, mask); break;
-        case 0x0477u: stage_mma<0x0477u>(acc, as, bs, xg0, xg1, mask); break;
+        case 0x0467u: stage_mma<0x0467u>(acc, as, bs, xg0, xg1, mask); break;
         case 0x0033u: stage_mma<0x0033u>(acc, as, bs, xg0, xg1, mask); break;
         case 0x0001u: stage_mma<0x0001u>(acc, as, bs, xg0, xg1, mask); break;
         case 0xCCCCu: stage_mma<0xCCCCu>(acc, as, bs, xg0, xg1, mask); break;
@@ -332,6 +340,13 @@ __global__ void __launch_bounds__(512)
             const size_t idx = static_cast<size_t>(row) * (2 * static_cast<size_t>(K) - row + 1) / 2 +
                                (col - row);
             packed[idx] = vals[c];
+        } else if (row < K && col < K && diag && wm == wn && (mi >> 1) == (ni >> 1) && (mi & 1) == 0 &&
+                   (ni & 1) == 1) {
+            // below the diagonal in an (even rows, odd columns) diagonal tile:
+            // the entry (col, row) of the skipped (odd, even) tile
+            const size_t idx = static_cast<size_t>(col) * (2 * static_cast<size_t>(K) - col + 1) / 2 +
+                               (row - col);
+            packed[idx] = vals[c];
         }
     }
 }
@@ -403,6 +418,10 @@ std::vector<TileInfo> plan_tiles_uncached(int K) {
                             const int cmin = J * BT + wn * 32 + (ni >> 1) * 16 + (ni & 1);
                             bool need = rmin < K && cmin < K;
                             if (I == J) need = need && rmin <= cmin + 14;
+                            // the (odd rows, even columns) tile of a diagonal 16-block:
+                            // the reduction takes it from the (even, odd) tile's transpose
+                            if (I == J && wm == wn && (mi >> 1) == (ni >> 1) && (mi & 1) == 1 && (ni & 1) == 0)
+                                need = false;
                             if (need) mask |= 1u << (mi * 4 + ni);
                         }
                     }
