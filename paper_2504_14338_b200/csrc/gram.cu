@@ -11,7 +11,7 @@
 //     atomic queue, so the CTAs running at any moment read the same rows of
 //     Q (L2 reuse across the ~tiles CTAs that need them).
 //   * Each persistent CTA = 1 TMA producer warp + 16 consumer warps. The
-//     producer streams 40×128 row-slabs of the I and J column blocks (8 boxes
+//     producer streams 48×128 row-slabs of the I and J column blocks (8 boxes
 //     of 16 columns, 128-byte swizzle; boxes wholly beyond column K are not
 //     loaded) through a double-buffered mbarrier ring
 //     (cp.async.bulk.tensor, OOB rows/cols zero-filled); consumers run
@@ -49,7 +49,10 @@ namespace {
 
 constexpr int BT = kTileEdge;         // 128 columns per block
 constexpr int BK = kRowsPerStage;     // rows per stage
-constexpr int STAGES = 2;
+#ifndef DOPINF_GRAM_STAGES  // (build-time tuning knob)
+#define DOPINF_GRAM_STAGES 2
+#endif
+constexpr int STAGES = DOPINF_GRAM_STAGES;
 constexpr int CONSUMERS = kConsumerWarps;  // 16 = 4 consumer warpgroups
 constexpr int THREADS = (CONSUMERS + 1) * kWarp;  // + one TMA producer warp
 constexpr int FLAG_FIRST = 1, FLAG_LAST = 2, FLAG_DONE = 4;

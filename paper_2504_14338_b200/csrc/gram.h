@@ -12,7 +12,13 @@ namespace dopinf_b200 {
 namespace gram {
 
 constexpr int kTileEdge = 128;       // columns of Q per block (CTA output tile edge)
-constexpr int kRowsPerStage = 40;    // rows of Q per TMA stage (measured: 16→48.1 ms, 32→47.0, 40→46.6, 56→48.0 at C2)
+#ifndef DOPINF_GRAM_ROWS_PER_STAGE  // (build-time tuning knob)
+#define DOPINF_GRAM_ROWS_PER_STAGE 48
+#endif
+// rows of Q per TMA stage (round 1: 16→48.1 ms, 32→47.0, 40→46.6, 56→48.0 at C2;
+// round 2, two stages unless noted: 24×4→43.58, 32×3→43.01, 40→42.75, 48→42.64,
+// 56→43.41 — profiles/r02_gram_stage_variants.txt)
+constexpr int kRowsPerStage = DOPINF_GRAM_ROWS_PER_STAGE;
 constexpr int kConsumerWarps = 16;   // 4×4 grid of 32×32 warp tiles
 constexpr int kWarpFragDoubles = 16 * 32 * 2;                   // 16 mma × 32 lanes × 2
 constexpr int kItemDoubles = kConsumerWarps * kWarpFragDoubles;  // 16384 (128 KiB)
