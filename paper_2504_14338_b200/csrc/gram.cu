@@ -49,6 +49,9 @@ namespace {
 
 constexpr int BT = kTileEdge;         // 128 columns per block
 constexpr int BK = kRowsPerStage;     // rows per stage
+#ifndef DOPINF_GRAM_PARTIAL_STORE  // (build-time tuning knob) how split partials are stored
+#define DOPINF_GRAM_PARTIAL_STORE __stcs  // evict-first: keeps Q rows in L2 (-0.15 GB re-reads at C2)
+#endif
 #ifndef DOPINF_GRAM_STAGES  // (build-time tuning knob)
 #define DOPINF_GRAM_STAGES 2
 #endif
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             v.x = old.x + v.x;
                             v.y = old.y + v.y;
                         }
-                        __stcg(p, v);
+                        DOPINF_GRAM_PARTIAL_STORE(p, v);
                     }
                     acc[i][0] = acc[i][1] = 0.0;
                 }
