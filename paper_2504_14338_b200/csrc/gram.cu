@@ -49,9 +49,6 @@ namespace {
 
 constexpr int BT = kTileEdge;         // 128 columns per block
 constexpr int BK = kRowsPerStage;     // rows per stage
-#ifndef DOPINF_GRAM_PARTIAL_STORE  // (build-time tuning knob) how split partials are stored
-#define DOPINF_GRAM_PARTIAL_STORE __stcs  // evict-first: keeps Q rows in L2 (-0.15 GB re-reads at C2)
-#endif
 #ifndef DOPINF_GRAM_STAGES  // (build-time tuning knob)
 #define DOPINF_GRAM_STAGES 2
 #endif
@@ -150,7 +147,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gram_dmma_kernel(const __grid_constant__ CUtensorMap tmap, const TileInfo* __restrict__ tiles,
                      int n_tiles, int n_items, long long n_rows, int K, int chunk_rows, int big_splits,
                      int small_rows,
-                     double* __restrict__ work, int* __restrict__ counters, int accumulate) {
+                     double* __restrict__ work, int* __restrict__ counters, int accumulate, int keep_partials) {
     extern __shared__ unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -255,7 +252,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                             v.x = old.x + v.x;
                             v.y = old.y + v.y;
                         }
-                        DOPINF_GRAM_PARTIAL_STORE(p, v);
+                        // one-launch partials are read once by the reduce: evict-first keeps
+                        // Q's rows in L2 (-0.15 GB of re-reads at C2); streamed launches
+                        // re-read their slots in the next chunk: keep those in L2
+                        if (keep_partials) {
+                            __stcg(p, v);
+                        } else {
+                            __stcs(p, v);
+                        }
                     }
                     acc[i][0] = acc[i][1] = 0.0;
                 }
@@ -600,7 +604,7 @@ cudaError_t launch_gram(const Plan& plan, const CUtensorMap& map, const TileInfo
     gram_dmma_kernel<<<plan.grid, THREADS, smem_bytes(), stream>>>(
         map, d_tiles, plan.n_tiles, plan.n_items, plan.n_rows, plan.K, plan.chunk_rows, plan.big_splits,
         plan.small_rows,
-        work, counters, accumulate ? 1 : 0);
+        work, counters, accumulate ? 1 : 0, plan.streamed ? 1 : 0);
     note_launch();
     return cudaGetLastError();
 }
@@ -615,6 +619,7 @@ Plan make_stream_plan(long long chunk_rows, int K, int num_sms, long long split_
     p.n_splits = static_cast<int>(std::max<long long>(1, (chunk_rows + split - 1) / split));
     p.big_splits = p.n_splits;
     p.small_rows = p.chunk_rows;
+    p.streamed = true;
     p.n_items = p.n_splits * p.n_tiles;
     p.grid = std::min(num_sms, p.n_items);
     p.workspace_doubles = static_cast<size_t>(p.n_items) * kItemDoubles;

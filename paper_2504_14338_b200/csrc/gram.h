@@ -42,6 +42,7 @@ struct Plan {
     int small_rows = 0;   // rows of the remaining (tail) splits
     int n_items = 0;
     int grid = 0;
+    bool streamed = false;  // make_stream_plan: the split slots are re-read by the next chunk's launch
     size_t workspace_doubles = 0;
 };
 
