@@ -27,45 +27,65 @@ namespace project {
 namespace {
 
 // ---- Q̂ = T_rᵀ D, reference order ---------------------------------------------
-constexpr int kPjCols = 32;   // columns j per block (one warp = 32 consecutive j)
-constexpr int kPjRows = 4;    // rows i per thread (independent FMA chains)
-constexpr int kPjWarps = 4;   // row groups per block → 16 rows of Q̂ per block
-constexpr int kPjL = 64;      // l-slab staged in shared memory
+// One FMA chain per output (the chains are the parallelism: r·K of them), so a
+// step costs one FMA latency once its operands are in shared memory. Block =
+// 8 warps = 8 rows i × 32 columns j; slabs of kPjL values of l (D rows and T_r
+// rows) arrive by cp.async into a double buffer while the previous slab's
+// chains run.
+constexpr int kPjCols = 32;   // columns j per block (lane = j)
+constexpr int kPjWarps = 8;   // rows i per block (warp = i)
+constexpr int kPjL = 128;     // l-slab staged in shared memory
+
+__device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+
+struct ProjectSmem {
+    double ds[2][kPjL][kPjCols];
+    double ts[2][kPjL][kPjWarps];
+};
 
 __global__ void __launch_bounds__(kPjCols * kPjWarps)
     project_kernel(const double* __restrict__ tr, const double* __restrict__ d, int K, int r,
                    double* __restrict__ qhat) {
-    __shared__ double ds[kPjL][kPjCols];
-    __shared__ double ts[kPjL][kPjRows * kPjWarps];
-    const int lane = threadIdx.x % 32, wg = threadIdx.x / 32;
-    const int j0 = blockIdx.x * kPjCols, i0 = blockIdx.y * kPjRows * kPjWarps;
-    const int j = j0 + lane;
-    double acc[kPjRows] = {0.0, 0.0, 0.0, 0.0};
-    for (int l0 = 0; l0 < K; l0 += kPjL) {
-        const int nl = min(kPjL, K - l0);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ProjectSmem& sm = *reinterpret_cast<ProjectSmem*>(smem_raw);
+    const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+    const int j0 = blockIdx.x * kPjCols, i0 = blockIdx.y * kPjWarps;
+    const int j = j0 + lane, i = i0 + w;
+    const int n_slabs = (K + kPjL - 1) / kPjL;
+    auto stage = [&](int slab, int buf) {
+        const int l0 = slab * kPjL;
         for (int e = threadIdx.x; e < kPjL * kPjCols; e += blockDim.x) {
             const int l = e / kPjCols, c = e % kPjCols;
-            ds[l][c] = (l < nl && j0 + c < K) ? d[static_cast<size_t>(l0 + l) * K + j0 + c] : 0.0;
+            const bool ok = l0 + l < K && j0 + c < K;
+            cp_async8(smem_u32(&sm.ds[buf][l][c]), ok ? d + static_cast<size_t>(l0 + l) * K + j0 + c : d, ok);
         }
-        for (int e = threadIdx.x; e < kPjL * kPjRows * kPjWarps; e += blockDim.x) {
-            const int l = e / (kPjRows * kPjWarps), c = e % (kPjRows * kPjWarps);
-            ts[l][c] = (l < nl && i0 + c < r) ? tr[static_cast<size_t>(l0 + l) * r + i0 + c] : 0.0;
+        for (int e = threadIdx.x; e < kPjL * kPjWarps; e += blockDim.x) {
+            const int l = e / kPjWarps, c = e % kPjWarps;
+            const bool ok = l0 + l < K && i0 + c < r;
+            cp_async8(smem_u32(&sm.ts[buf][l][c]), ok ? tr + static_cast<size_t>(l0 + l) * r + i0 + c : tr, ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    double acc = 0.0;
+    stage(0, 0);
+    for (int slab = 0; slab < n_slabs; ++slab) {
+        const int buf = slab & 1;
+        if (slab + 1 < n_slabs) {
+            stage(slab + 1, buf ^ 1);  // the buffer the previous slab used (all threads are past it)
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         __syncthreads();
-        for (int l = 0; l < nl; ++l) {
-            const double dv = ds[l][lane];
-#pragma unroll
-            for (int k = 0; k < kPjRows; ++k) acc[k] = fma(ts[l][wg * kPjRows + k], dv, acc[k]);
-        }
-        __syncthreads();
+        const int nl = min(kPjL, K - slab * kPjL);
+#pragma unroll 8
+        for (int l = 0; l < nl; ++l) acc = fma(sm.ts[buf][l][w], sm.ds[buf][l][lane], acc);
+        __syncthreads();  // everyone is done with `buf` before it is refilled
     }
-    if (j < K) {
-#pragma unroll
-        for (int k = 0; k < kPjRows; ++k) {
-            const int i = i0 + wg * kPjRows + k;
-            if (i < r) qhat[static_cast<size_t>(i) * K + j] = acc[k];
-        }
-    }
+    if (j < K && i < r) qhat[static_cast<size_t>(i) * K + j] = acc;
 }
 
 __global__ void basis_rows_kernel(const double* __restrict__ q, size_t ld, int K,
@@ -294,8 +314,11 @@ int basis_cols_pad(int r) {
 
 cudaError_t launch_project(const double* tr, const double* d, int K, int r, double* qhat,
                            cudaStream_t stream) {
-    dim3 grid((K + kPjCols - 1) / kPjCols, (r + kPjRows * kPjWarps - 1) / (kPjRows * kPjWarps));
-    project_kernel<<<grid, kPjCols * kPjWarps, 0, stream>>>(tr, d, K, r, qhat);
+    dim3 grid((K + kPjCols - 1) / kPjCols, (r + kPjWarps - 1) / kPjWarps);
+    const cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(project_kernel),
+                                             static_cast<int>(sizeof(ProjectSmem)));
+    if (e != cudaSuccess) return e;
+    project_kernel<<<grid, kPjCols * kPjWarps, sizeof(ProjectSmem), stream>>>(tr, d, K, r, qhat);
     note_launch();
     return cudaGetLastError();
 }
