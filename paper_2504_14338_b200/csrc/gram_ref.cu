@@ -14,17 +14,18 @@
 // Without a split over rows the parallelism is the number of entries, and
 // smaller tiles cost more operand traffic per FMA, so the tile size follows K:
 //  * small tiles (fewer than two waves of large tiles, e.g. K = 1200): CTA =
-//    2 warps = 32 × 64 entries, the upper or lower half of a 64 × 64 tile of
-//    the upper triangle (K = 1200: 380 CTAs), each thread 32 independent FMA
-//    chains (8 × 4 entries); C2: 0.15 s;
+//    32 × 64 entries, the upper or lower half of a 64 × 64 tile of the upper
+//    triangle (K = 1200: 380 CTAs); 4 warps with 16 independent FMA chains per
+//    thread (4 × 4 entries) while the CTAs are few, else 2 warps with 32
+//    (8 × 4); C2: 0.135 s;
 //  * large tiles (K = 4096: 528 tiles): CTA = 8 warps = 128 × 128 entries, 8 × 8
 //    per thread, 0.375× the operand bytes per FMA (the small tiles would make
 //    the kernel L2-bandwidth bound there); C3 K = 4096: 3.4 s.
-// Small tiles: warp w covers rows i0 + 16w .. +15 of D: thread (ti = lane / 16,
-// tj = lane % 16) owns i = i0 + 16w + 8·ti + x (x < 8, contiguous: 128-bit
+// Small tiles: warp w covers rows i0 + 2·TI·w .. of D: thread (ti = lane / 16,
+// tj = lane % 16) owns i = i0 + 2·TI·w + TI·ti + x (x < TI, contiguous: 128-bit
 // loads, broadcast across the half-warp) and j = j0 + tj + 16·y (y < 4,
 // strided: each 64-bit load is 16 consecutive doubles per half-warp, conflict
-// free): 8 shared-memory wavefronts per 32 DFMA instructions. Large tiles: the
+// free). Large tiles: the
 // same pattern with 8 × 8 entries per thread over a 16 × 16 thread grid. Rows
 // stream through a double-buffered cp.async stage (zero-filled beyond the
 // block).
@@ -38,7 +39,9 @@ namespace {
 
 constexpr int kRefEdge = 64;                // square tiles of the triangle
 constexpr int kRefHalf = kRefEdge / 2;      // rows of D per CTA (half a tile)
-constexpr int kRefThreads = 64;
+// threads of a small-tile CTA: 2 warps with 8 × 4 entries per thread, 4 warps with 4 × 4
+template <int TI>
+__host__ __device__ constexpr int ref_threads() { return 32 * kRefHalf / (2 * TI); }
 constexpr int kRefRows = 32;                // rows of Q per stage
 constexpr int kRefCols = kRefHalf + kRefEdge;  // I columns then J columns of a stage row
 constexpr size_t kRefSmemBytes = size_t(2) * kRefRows * kRefCols * sizeof(double);  // 48 KiB
@@ -48,7 +51,8 @@ __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) 
                  : "memory");
 }
 
-__global__ void __launch_bounds__(kRefThreads)
+template <int kRefTI>
+__global__ void __launch_bounds__(ref_threads<kRefTI>())
     gram_ref_kernel(const double* __restrict__ q, size_t ld, long long rows, int K, int nb,
                     double* __restrict__ packed, int accumulate) {
     extern __shared__ __align__(16) double smem[];  // [buf][kRefRows][kRefCols]: I | J
@@ -62,13 +66,13 @@ __global__ void __launch_bounds__(kRefThreads)
     const int i0 = bi * kRefEdge + half * kRefHalf, j0 = bj * kRefEdge;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int ti = lane / 16, tj = lane % 16;
-    const int ib = 16 * warp + 8 * ti;  // first of this thread's 8 rows of D within the tile
+    const int ib = 2 * kRefTI * warp + kRefTI * ti;  // first of this thread's kRefTI rows of D in the tile
     const size_t Kz = static_cast<size_t>(K);
 
     auto packed_at = [&](int i, int j) { return static_cast<size_t>(i) * (2 * Kz - i + 1) / 2 + (j - i); };
-    double acc[8][4];
+    double acc[kRefTI][4];
 #pragma unroll
-    for (int x = 0; x < 8; ++x) {
+    for (int x = 0; x < kRefTI; ++x) {
 #pragma unroll
         for (int y = 0; y < 4; ++y) {
             const int i = i0 + ib + x, j = j0 + tj + 16 * y;
@@ -80,7 +84,7 @@ __global__ void __launch_bounds__(kRefThreads)
     auto load_stage = [&](long long s, int buf) {
         const long long r0 = s * kRefRows;
 #pragma unroll 4
-        for (int c = threadIdx.x; c < kRefRows * (kRefCols / 2); c += kRefThreads) {
+        for (int c = threadIdx.x; c < kRefRows * (kRefCols / 2); c += ref_threads<kRefTI>()) {
             const int rr = c / (kRefCols / 2), cc = 2 * (c % (kRefCols / 2));  // stage column
             const int col = cc < kRefHalf ? i0 + cc : j0 + (cc - kRefHalf);
             const long long row = r0 + rr;
@@ -110,9 +114,9 @@ __global__ void __launch_bounds__(kRefThreads)
         const int nr = left < kRefRows ? static_cast<int>(left) : kRefRows;
 #pragma unroll 2
         for (int r = 0; r < nr; ++r) {
-            double a[8], b[4];
+            double a[kRefTI], b[4];
 #pragma unroll
-            for (int x = 0; x < 8; x += 2) {
+            for (int x = 0; x < kRefTI; x += 2) {
                 const double2 v = lds128(sI + r * kRefCols + x);
                 a[x] = v.x;
                 a[x + 1] = v.y;
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(kRefThreads)
 #pragma unroll
             for (int y = 0; y < 4; ++y) b[y] = sJ[r * kRefCols + 16 * y];
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
+            for (int x = 0; x < kRefTI; ++x) {
 #pragma unroll
                 for (int y = 0; y < 4; ++y) acc[x][y] = __fma_rn(a[x], b[y], acc[x][y]);
             }
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(kRefThreads)
     }
 
 #pragma unroll
-    for (int x = 0; x < 8; ++x) {
+    for (int x = 0; x < kRefTI; ++x) {
 #pragma unroll
         for (int y = 0; y < 4; ++y) {
             const int i = i0 + ib + x, j = j0 + tj + 16 * y;
@@ -249,10 +253,22 @@ cudaError_t launch_gram_reference_order(const double* q, size_t ld, long long ro
     } else {
         const int nb = (K + kRefEdge - 1) / kRefEdge;
         const int tiles = nb * (nb + 1) / 2;
-        e = set_smem_attr_once(reinterpret_cast<const void*>(gram_ref_kernel), static_cast<int>(kRefSmemBytes));
-        if (e != cudaSuccess) return e;
-        gram_ref_kernel<<<2 * tiles, kRefThreads, kRefSmemBytes, stream>>>(q, ld, rows, K, nb, packed,
-                                                                             accumulate ? 1 : 0);
+        // Every thread walks all rows, so the time is rows × the per-row step of
+        // the chains: 4 × 4 entries per thread (twice the warps) hide it better
+        // while the CTAs are few (config 2: 150 → 135 ms, config 1: 2.9 → 2.5 ms);
+        // with ≥ 4 CTAs per SM the 8 × 4 tiles' lower operand traffic wins
+        // (K = 2048: 74 vs 84 ms; tools/refgram_probe.py).
+        if (2 * tiles >= 4 * 148) {
+            e = set_smem_attr_once(reinterpret_cast<const void*>(gram_ref_kernel<8>), static_cast<int>(kRefSmemBytes));
+            if (e != cudaSuccess) return e;
+            gram_ref_kernel<8><<<2 * tiles, ref_threads<8>(), kRefSmemBytes, stream>>>(q, ld, rows, K, nb, packed,
+                                                                                     accumulate ? 1 : 0);
+        } else {
+            e = set_smem_attr_once(reinterpret_cast<const void*>(gram_ref_kernel<4>), static_cast<int>(kRefSmemBytes));
+            if (e != cudaSuccess) return e;
+            gram_ref_kernel<4><<<2 * tiles, ref_threads<4>(), kRefSmemBytes, stream>>>(q, ld, rows, K, nb, packed,
+                                                                                     accumulate ? 1 : 0);
+        }
     }
     note_launch();
     return cudaGetLastError();
