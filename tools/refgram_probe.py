@@ -1,5 +1,6 @@
 """Times the reference-order Gram (gram_ref.cu) on resident blocks: config 2
-(4 x 262144 x 1200), config 1 (2 x 16384 x 600) and K in argv (dev tool)."""
+(4 x 262144 x 1200), config 1 (2 x 16384 x 600) and three single-variable
+shapes at K = 256 / 512 / 2048 (dev tool)."""
 import sys
 from pathlib import Path
 
