@@ -13,6 +13,7 @@ log() { echo "[$(date +%T)] $*" | tee -a "$out/round_profile.log"; }
 
 log "gpu tests"
 timeout 1500 python -m pytest tests -m gpu -q > "$out/rp_gpu_tests.txt" 2>&1; log "gpu tests rc=$?"
+timeout 900 python -m pytest tests/test_gpu_configs.py -m gpu -q -s > "$out/rp_config_parity.txt" 2>&1; log "config parity rc=$?"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$out/rp_smoke.txt" 2>&1; log "smoke rc=$?"
 [ -x tests/cpp/_build/parity ] && { timeout 900 tests/cpp/_build/parity > "$out/rp_parity_harness.txt" 2>&1; log "harness rc=$?"; }
 
