@@ -15,9 +15,9 @@
 // smaller tiles cost more operand traffic per FMA, so the tile size follows K:
 //  * small tiles (fewer than two waves of large tiles, e.g. K = 1200): CTA =
 //    32 × 64 entries, the upper or lower half of a 64 × 64 tile of the upper
-//    triangle (K = 1200: 380 CTAs); 4 warps with 16 independent FMA chains per
-//    thread (4 × 4 entries) while the CTAs are few, else 2 warps with 32
-//    (8 × 4); C2: 0.135 s;
+//    triangle (K = 1200: 380 CTAs); 8, 4 or 2 warps with 8, 16 or 32
+//    independent FMA chains per thread (2 × 4, 4 × 4 or 8 × 4 entries) as the
+//    CTA count grows; C2: 0.135 s;
 //  * large tiles (K = 4096: 528 tiles): CTA = 8 warps = 128 × 128 entries, 8 × 8
 //    per thread, 0.375× the operand bytes per FMA (the small tiles would make
 //    the kernel L2-bandwidth bound there); C3 K = 4096: 3.4 s.
@@ -254,21 +254,27 @@ cudaError_t launch_gram_reference_order(const double* q, size_t ld, long long ro
         const int nb = (K + kRefEdge - 1) / kRefEdge;
         const int tiles = nb * (nb + 1) / 2;
         // Every thread walks all rows, so the time is rows × the per-row step of
-        // the chains: 4 × 4 entries per thread (twice the warps) hide it better
-        // while the CTAs are few (config 2: 150 → 135 ms, config 1: 2.9 → 2.5 ms);
-        // with ≥ 4 CTAs per SM the 8 × 4 tiles' lower operand traffic wins
-        // (K = 2048: 74 vs 84 ms; tools/refgram_probe.py).
-        if (2 * tiles >= 4 * 148) {
-            e = set_smem_attr_once(reinterpret_cast<const void*>(gram_ref_kernel<8>), static_cast<int>(kRefSmemBytes));
-            if (e != cudaSuccess) return e;
-            gram_ref_kernel<8><<<2 * tiles, ref_threads<8>(), kRefSmemBytes, stream>>>(q, ld, rows, K, nb, packed,
-                                                                                     accumulate ? 1 : 0);
+        // its chains, and more warps hide that step better while the CTAs are
+        // few; with many CTAs the larger thread tiles' lower operand traffic
+        // wins (tools/refgram_probe.py, profiles/r02_refgram_ti_ab.txt):
+        //   < 1 CTA per SM:  2 × 4 entries per thread, 8 warps (K = 256: 78 → 69 ms, config 1: 2.5 → 2.2 ms)
+        //   < 4 CTAs per SM: 4 × 4, 4 warps (config 2: 150 → 135 ms)
+        //   otherwise:       8 × 4, 2 warps (K = 2048: 74 ms; 4 × 4 84 ms)
+        const int ctas = 2 * tiles;
+        auto run = [&](auto kern, int threads) {
+            cudaError_t err = set_smem_attr_once(reinterpret_cast<const void*>(kern), static_cast<int>(kRefSmemBytes));
+            if (err != cudaSuccess) return err;
+            kern<<<ctas, threads, kRefSmemBytes, stream>>>(q, ld, rows, K, nb, packed, accumulate ? 1 : 0);
+            return cudaSuccess;
+        };
+        if (ctas < 148) {
+            e = run(gram_ref_kernel<2>, ref_threads<2>());
+        } else if (ctas < 4 * 148) {
+            e = run(gram_ref_kernel<4>, ref_threads<4>());
         } else {
-            e = set_smem_attr_once(reinterpret_cast<const void*>(gram_ref_kernel<4>), static_cast<int>(kRefSmemBytes));
-            if (e != cudaSuccess) return e;
-            gram_ref_kernel<4><<<2 * tiles, ref_threads<4>(), kRefSmemBytes, stream>>>(q, ld, rows, K, nb, packed,
-                                                                                     accumulate ? 1 : 0);
+            e = run(gram_ref_kernel<8>, ref_threads<8>());
         }
+        if (e != cudaSuccess) return e;
     }
     note_launch();
     return cudaGetLastError();
