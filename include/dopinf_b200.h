@@ -204,6 +204,12 @@ int dopinf_b200_check_uniform(const long long* table, int p, int rank, const cha
 long long dopinf_b200_debug_guard_violations(void);
 /* Fault injection for tests (DOPINF_B200_INJECT_*; 0 clears). */
 int dopinf_b200_debug_inject(dopinf_b200_ctx* ctx, int what);
+/* Host-only check of the Gram tile plan for K (no GPU needed): the number of
+ * packed upper-triangle entries (K(K+1)/2), how many of them the split-n
+ * reduction writes, how many it would write more than once, and the 8x8 DMMA
+ * tiles executed per 4-row k-step over all output tiles. */
+int dopinf_b200_debug_gram_coverage(int K, long long* entries, long long* covered, long long* duplicates,
+                                    long long* mma_tiles);
 /* The combine step of the ORDERED reduction on the device: out = parts[0] +
  * parts[1] + ... + parts[p-1] element-wise, left to right (kernels::add in
  * ascending rank order, comm_inprocess.cpp:101-112). parts: host p x count. */

@@ -39,6 +39,7 @@ UNIQUE_ID_BYTES = 128
 _dp = C.POINTER(C.c_double)
 _sp = C.POINTER(C.c_size_t)
 _vp = C.c_void_p
+_llp = C.POINTER(C.c_longlong)
 
 # name: (restype, argtypes)
 SIGNATURES = {
@@ -56,6 +57,7 @@ SIGNATURES = {
                                             C.c_size_t]),
     "dopinf_b200_debug_inject": (C.c_int, [_vp, C.c_int]),
     "dopinf_b200_debug_guard_violations": (C.c_longlong, []),
+    "dopinf_b200_debug_gram_coverage": (C.c_int, [C.c_int, _llp, _llp, _llp, _llp]),
     "dopinf_b200_ordered_sum": (C.c_int, [_vp, _dp, C.c_int, C.c_size_t, _dp]),
     "dopinf_b200_ctx_destroy": (None, [_vp]),
     "dopinf_b200_ctx_rank": (C.c_int, [_vp]),

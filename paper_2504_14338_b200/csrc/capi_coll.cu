@@ -363,6 +363,23 @@ int dopinf_b200_check_uniform(const long long* table, int p, int rank, const cha
     return DOPINF_B200_ERR_COLLECTIVE;
 }
 
+int dopinf_b200_debug_gram_coverage(int K, long long* entries, long long* covered, long long* duplicates,
+                                    long long* mma_tiles) {
+    if (K < 1 || !entries || !covered || !duplicates || !mma_tiles) return DOPINF_B200_ERR_INVALID_ARGUMENT;
+    try {
+        const gram::CoverageReport r = gram::coverage(K);
+        *entries = r.entries;
+        *covered = r.covered;
+        *duplicates = r.duplicates;
+        *mma_tiles = r.mma_tiles;
+        return DOPINF_B200_OK;
+    } catch (const std::bad_alloc&) {
+        return DOPINF_B200_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        return DOPINF_B200_ERR_DEVICE;
+    }
+}
+
 long long dopinf_b200_debug_guard_violations(void) {
     if (guard_bytes() == 0) return -1;
     cudaDeviceSynchronize();

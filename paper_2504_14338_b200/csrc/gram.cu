@@ -67,7 +67,7 @@ struct __align__(1024) Smem {
 };
 
 // Warp-tile entry: wm | wn << 2 | diag << 4 | mma mask << 16 (0 mask = idle).
-__device__ __forceinline__ void decode(uint32_t e, int& wm, int& wn, bool& diag, uint32_t& mask) {
+__host__ __device__ __forceinline__ void decode(uint32_t e, int& wm, int& wn, bool& diag, uint32_t& mask) {
     wm = e & 3;
     wn = (e >> 2) & 3;
     diag = (e >> 4) & 1;
@@ -97,6 +97,26 @@ __device__ __forceinline__ void decode(uint32_t e, int& wm, int& wn, bool& diag,
 // odd columns) one computes; it is skipped (12 -> 10 mma) and the reduction
 // writes those entries from their transposes (D is symmetric, and the two
 // dot products are the same products summed in the same k order).
+// Where accumulator element c of lane `lane` in mma tile `mma` of warp tile
+// (wm, wn) of output tile (I, J) lands in the packed upper triangle, or -1
+// (below the diagonal or beyond K). Below-diagonal entries of an (even rows,
+// odd columns) mma tile inside a diagonal 16-block are the entries of the
+// skipped (odd, even) tile: they land at their transposes. Shared by the
+// reduction and the host-side coverage check (dopinf_b200_debug_gram_coverage).
+__host__ __device__ __forceinline__ long long scatter_index(int I, int J, int wm, int wn, bool diag, int mma,
+                                                            int lane, int c, int K) {
+    const int g = lane >> 2, t = lane & 3;
+    const int mi = mma >> 2, ni = mma & 3;
+    const int row = I * BT + wm * 32 + (mi >> 1) * 16 + 2 * g + (mi & 1);
+    const int col = J * BT + wn * 32 + (ni >> 1) * 16 + 2 * (2 * t + c) + (ni & 1);
+    if (row >= K || col >= K) return -1;
+    const long long Kl = K;
+    if (row <= col) return static_cast<long long>(row) * (2 * Kl - row + 1) / 2 + (col - row);
+    if (diag && wm == wn && (mi >> 1) == (ni >> 1) && (mi & 1) == 0 && (ni & 1) == 1)
+        return static_cast<long long>(col) * (2 * Kl - col + 1) / 2 + (row - col);
+    return -1;
+}
+
 template <uint32_t MASK>
 __device__ __forceinline__ void stage_mma(double (&acc)[16][2], const double* __restrict__ as,
                                           const double* __restrict__ bs, int xg0, int xg1, uint32_t mask) {
@@ -338,26 +358,11 @@ __global__ void __launch_bounds__(512)
                sum);
         return;
     }
-    const int g = lane >> 2, t = lane & 3;
-    const int mi = mma >> 2, ni = mma & 3;
-    const int row = tiles[tile].I * BT + wm * 32 + (mi >> 1) * 16 + 2 * g + (mi & 1);
     const double vals[2] = {sum.x, sum.y};
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-        const int n = 2 * t + c;
-        const int col = tiles[tile].J * BT + wn * 32 + (ni >> 1) * 16 + 2 * n + (ni & 1);
-        if (row < K && col < K && row <= col) {
-            const size_t idx = static_cast<size_t>(row) * (2 * static_cast<size_t>(K) - row + 1) / 2 +
-                               (col - row);
-            packed[idx] = vals[c];
-        } else if (row < K && col < K && diag && wm == wn && (mi >> 1) == (ni >> 1) && (mi & 1) == 0 &&
-                   (ni & 1) == 1) {
-            // below the diagonal in an (even rows, odd columns) diagonal tile:
-            // the entry (col, row) of the skipped (odd, even) tile
-            const size_t idx = static_cast<size_t>(col) * (2 * static_cast<size_t>(K) - col + 1) / 2 +
-                               (row - col);
-            packed[idx] = vals[c];
-        }
+        const long long idx = scatter_index(tiles[tile].I, tiles[tile].J, wm, wn, diag, mma, lane, c, K);
+        if (idx >= 0) packed[idx] = vals[c];
     }
 }
 
@@ -664,6 +669,36 @@ cudaError_t launch_reduce(const Plan& plan, const TileInfo* d_tiles, const doubl
     }
     note_launch();
     return cudaGetLastError();
+}
+
+CoverageReport coverage(int K) {
+    CoverageReport r;
+    const std::vector<TileInfo> tiles = plan_tiles(K);
+    const size_t count = packed_count(K);
+    std::vector<unsigned char> hits(count, 0);
+    for (const TileInfo& ti : tiles) {
+        for (int w = 0; w < kConsumerWarps; ++w) {
+            int wm, wn;
+            bool diag;
+            uint32_t mask;
+            decode(ti.warp[w], wm, wn, diag, mask);
+            for (int mma = 0; mma < 16; ++mma) {
+                if (!((mask >> mma) & 1u)) continue;
+                ++r.mma_tiles;
+                for (int lane = 0; lane < kWarp; ++lane) {
+                    for (int c = 0; c < 2; ++c) {
+                        const long long idx = scatter_index(ti.I, ti.J, wm, wn, diag, mma, lane, c, K);
+                        if (idx < 0) continue;
+                        if (hits[idx] == 1) ++r.duplicates;
+                        if (hits[idx] < 2) ++hits[idx];
+                    }
+                }
+            }
+        }
+    }
+    for (unsigned char h : hits) r.covered += h ? 1 : 0;
+    r.entries = static_cast<long long>(count);
+    return r;
 }
 
 cudaError_t launch_unpack(const double* packed, int K, double* d, cudaStream_t stream) {

@@ -65,6 +65,14 @@ size_t reduce_scratch_doubles(const Plan& plan, int groups);
 cudaError_t launch_reduce(const Plan& plan, const TileInfo* d_tiles, const double* work,
                           double* packed, cudaStream_t stream, int groups = 1, double* scratch = nullptr);
 cudaError_t launch_unpack(const double* packed, int K, double* d, cudaStream_t stream);
+// Host-side check of the tile plan for K: how many packed upper-triangle
+// entries the reduction writes (covered, of entries) and how many it would
+// write twice; mma_tiles = 8×8 DMMA tiles executed per 4-row k-step over all
+// output tiles (the executed work, for the useful-work ratio).
+struct CoverageReport {
+    long long entries = 0, covered = 0, duplicates = 0, mma_tiles = 0;
+};
+CoverageReport coverage(int K);
 // out[e] = parts[0][e] + parts[1][e] + ... (rank r's part at parts + r*stride).
 cudaError_t launch_ordered_sum(const double* parts, int p, size_t count, size_t stride, double* out,
                                cudaStream_t stream);
